@@ -1,0 +1,148 @@
+/* include/dfa.h -- C-ABI of the B200-native Dilated Flash Attention forward.
+ *
+ * Drop-in boundary for the reference's hot path
+ *   attnkit::dilated_attention<S>(q, k, v, cfg, head_offset, workers)
+ *     (/root/reference/proj/include/attnkit/attention.hpp:280-301)
+ * and the helpers it is built from (AttentionConfig::validate :44-65,
+ * make_segment_view :84-98, flop_count :370-387, the recompose fault hook
+ * :237-241).  The reference exposes a header-only C++ template API with no
+ * FFI; these entry points are what an FFI for that path binds (plain
+ * pointers and sizes, no C++ or torch types).  include/dfa.hpp rebuilds the
+ * reference-shaped C++ API (same names, same exception types) on top.
+ *
+ * Tensor layout (all device entry points): q, k are [B, N, h, d] and v, o are
+ * [B, N, h, d_v], row-major and contiguous -- i.e. per image the reference's
+ * multi-head concat layout [N, h*d] (attention.hpp:350-357).  The single-head
+ * reference call is B = 1, h = 1.  Head j uses offset head_offsets[j]; rows
+ * selected by no view of head j are written as exact zeros (attention.hpp:
+ * 243-245, 270).
+ *
+ * Ownership: the caller owns every buffer; no entry point allocates device
+ * memory on the hot path (dfa_workspace_* is the explicit exception, created
+ * once up front).  Threading: reentrant and stream-ordered; the only global
+ * state is the fault-injection flag (mirrors attention.hpp:240).
+ */
+#ifndef DFA_H_
+#define DFA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error taxonomy: 1:1 with the reference's exception types
+ * (common.hpp:13-30 and std::out_of_range at attention.hpp:87-90,287-288). */
+typedef enum {
+  DFA_OK = 0,
+  DFA_ERR_CONFIG = 1,       /* attnkit::config_error    */
+  DFA_ERR_DIMENSION = 2,    /* attnkit::dimension_error */
+  DFA_ERR_OUT_OF_RANGE = 3, /* std::out_of_range        */
+  DFA_ERR_CONTRACT = 4,     /* attnkit::contract_error  */
+  DFA_ERR_CUDA = 5,         /* CUDA runtime/driver failure (no reference analogue) */
+  DFA_ERR_UNSUPPORTED = 6   /* valid config outside what the device kernels implement */
+} dfa_status_t;
+
+typedef enum { DFA_F32 = 0, DFA_BF16 = 1 } dfa_dtype_t;
+
+/* attention.hpp:15 Kernel{naive, tiled}.  Validated exactly as the reference
+ * does (tile_size >= 1 when tiled); on the GPU every kernel streams keys in
+ * tiles, so the flag selects nothing else. */
+typedef enum { DFA_KERNEL_NAIVE = 0, DFA_KERNEL_TILED = 1 } dfa_kernel_t;
+
+/* Which device path dfa_forward takes for a given call (dfa_query_path). */
+typedef enum {
+  DFA_PATH_NONE = 0,
+  DFA_PATH_SM100_TCGEN05 = 1, /* bf16, TMA + tcgen05/TMEM (sm_100a)          */
+  DFA_PATH_SIMT = 2           /* f32 validation / general-geometry kernel    */
+} dfa_path_t;
+
+/* attention.hpp:24-33 AttentionConfig. */
+typedef struct {
+  int64_t seq_len;             /* N                                         */
+  int64_t segment_len;         /* w                                         */
+  int64_t interval;            /* r                                         */
+  int64_t num_heads;           /* h                                         */
+  int64_t head_dim;            /* d   (q/k width)                           */
+  int64_t value_dim;           /* d_v (v/o width); 0 means d_v = d          */
+  const int64_t* head_offsets; /* h offsets gamma_j in [0, r)               */
+  int32_t kernel;              /* dfa_kernel_t                              */
+  int64_t tile_size;           /* tiled kernel only                         */
+  int32_t scale_scores;        /* nonzero: scores *= 1/sqrt(d) after q.k    */
+} dfa_config_t;
+
+/* Thread-local message of the last failing call on this thread (the text the
+ * reference's exception would carry, common.hpp:50-55 msg()). */
+const char* dfa_last_error(void);
+
+/* attention.hpp:44-65 AttentionConfig::validate(require_full_coverage). */
+dfa_status_t dfa_validate(const dfa_config_t* cfg, int32_t require_full_coverage);
+
+/* attention.hpp:84-98 make_segment_view: global rows {i*w+g, i*w+g+r, ...}
+ * clipped to segment i.  Writes min(count, cap) indices; *count = full count.
+ * Errors: DFA_ERR_OUT_OF_RANGE for a bad segment index or offset. */
+dfa_status_t dfa_segment_view(int64_t seq_len, int64_t segment_len, int64_t interval, int64_t segment_index,
+                              int64_t offset, int64_t* rows, int64_t cap, int64_t* count);
+
+/* attention.hpp:370-387 flop_count (multiplications only). */
+dfa_status_t dfa_flop_count(const dfa_config_t* cfg, uint64_t* dense_mults, uint64_t* dilated_mults,
+                            double* ratio);
+
+/* Device path dfa_forward would take (no launch).  *path = dfa_path_t. */
+dfa_status_t dfa_query_path(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t* path);
+
+/* Batched multi-head forward on DEVICE pointers (attention.hpp:280-301 run
+ * for every image b and head j with gamma_j = head_offsets[j]).
+ *   q, k: [B, N, h, d]; v, o: [B, N, h, d_v] of `dtype`;
+ *   lse : optional fp32 [B, h, N] (natural-log log-sum-exp of the scaled
+ *         scores of each kept row; -inf for rows no view selects).  NULL = off.
+ *   stream: a cudaStream_t (NULL = legacy default stream).
+ * Stream-ordered: returns after the launch, not after completion. */
+dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
+                         const void* v, void* o, float* lse, void* stream);
+
+/* Reference-shaped single-head call on HOST buffers, synchronous:
+ * q, k [N x d], v [N x d_v] -> out [N x d_v] (attention.hpp:280-282).
+ * `workers` is accepted and ignored (the GPU grid replaces parallel_for).
+ * Uses `ws` (see below) for device staging. */
+typedef struct dfa_workspace dfa_workspace_t;
+dfa_status_t dfa_workspace_create(size_t bytes, dfa_workspace_t** ws);
+dfa_status_t dfa_workspace_destroy(dfa_workspace_t* ws);
+dfa_status_t dfa_dilated_attention_host(const dfa_config_t* cfg, dfa_dtype_t dtype, const void* q, const void* k,
+                                        const void* v, int64_t head_offset, int32_t workers, void* out,
+                                        dfa_workspace_t* ws);
+
+/* Batched forward on HOST buffers (the end-to-end call): H2D copy of q, k, v,
+ * dfa_forward, D2H copy of o (and lse if non-NULL), stream synchronize.  Pinned
+ * host buffers give full PCIe bandwidth; pageable ones work, slower. */
+dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                              const void* k, const void* v, void* o, float* lse, dfa_workspace_t* ws,
+                              void* stream);
+
+/* attention.hpp:237-241 fault::recompose_perturb: when armed, every forward
+ * adds 1e-3 to output element 0 so the parity harness demonstrably fails. */
+void dfa_set_fault_perturb(int32_t armed);
+int32_t dfa_get_fault_perturb(void);
+
+/* Bytes a dfa_forward_host call needs in its workspace. */
+dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t with_lse,
+                                 size_t* bytes);
+
+/* Test hook: 0 = automatic dispatch (default), DFA_PATH_SIMT = force the SIMT
+ * kernel, DFA_PATH_SM100_TCGEN05 = require the tcgen05 kernel (calls it does
+ * not cover fail with DFA_ERR_UNSUPPORTED).  Process-wide. */
+void dfa_set_path_override(int32_t path);
+
+/* Number of device kernels the last dfa_forward on this thread launched
+ * (evidence for bench.py's gpu_launches). */
+int32_t dfa_last_launch_count(void);
+
+/* Library version, e.g. 100 = 0.1.0. */
+int32_t dfa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFA_H_ */

@@ -1,0 +1,366 @@
+"""B200-native Dilated Flash Attention (SAM-Lightening, arxiv 2403.09195).
+
+Host-side mirror of the reference operator API for the hot path
+(/root/reference/proj/include/attnkit/attention.hpp), calling the sm_100a
+kernels through the C-ABI in include/dfa.h (libdfa.so):
+
+    AttentionConfig            attention.hpp:24-66
+    make_segment_view          attention.hpp:84-98
+    dilated_attention          attention.hpp:280-301  (single head, [N, d])
+    dfa_forward                batched multi-head [B, N, h, d] (the device API)
+    flop_count / flop_csv_*    attention.hpp:370-394
+    fault_perturb              attention.hpp:237-241
+
+Errors mirror the reference's exception taxonomy (common.hpp:13-30):
+ConfigError, DimensionError, ContractError and OutOfRange (an IndexError,
+the std::out_of_range analogue).  PyTorch is used only for device memory and
+streams; every forward runs a CUDA kernel from libdfa.so -- there is no CPU
+path, and a CPU tensor is rejected.
+"""
+from __future__ import annotations
+
+import contextlib
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+from . import _lib
+from ._lib import lib
+
+__all__ = [
+    "AttentionConfig",
+    "SegmentView",
+    "FlopCount",
+    "ConfigError",
+    "DimensionError",
+    "ContractError",
+    "OutOfRange",
+    "CudaError",
+    "UnsupportedError",
+    "make_segment_view",
+    "flop_count",
+    "flop_csv_header",
+    "flop_csv_row",
+    "dilated_attention",
+    "dfa_forward",
+    "dfa_forward_host",
+    "query_path",
+    "fault_perturb",
+    "last_launch_count",
+]
+
+
+class DfaError(RuntimeError):
+    """Base of the errors raised by the C-ABI."""
+
+
+class ConfigError(DfaError):
+    """attnkit::config_error."""
+
+
+class DimensionError(DfaError):
+    """attnkit::dimension_error."""
+
+
+class ContractError(DfaError):
+    """attnkit::contract_error."""
+
+
+class OutOfRange(IndexError):
+    """std::out_of_range (segment index / offset outside its range)."""
+
+
+class CudaError(DfaError):
+    """A CUDA runtime/driver failure inside the library."""
+
+
+class UnsupportedError(DfaError):
+    """A valid configuration the device kernels do not implement."""
+
+
+_ERRORS = {
+    _lib.DFA_ERR_CONFIG: ConfigError,
+    _lib.DFA_ERR_DIMENSION: DimensionError,
+    _lib.DFA_ERR_OUT_OF_RANGE: OutOfRange,
+    _lib.DFA_ERR_CONTRACT: ContractError,
+    _lib.DFA_ERR_CUDA: CudaError,
+    _lib.DFA_ERR_UNSUPPORTED: UnsupportedError,
+}
+
+
+def _check(status: int) -> None:
+    if status != _lib.DFA_OK:
+        msg = lib.dfa_last_error().decode()
+        raise _ERRORS.get(status, DfaError)(msg)
+
+
+@dataclass
+class AttentionConfig:
+    """attention.hpp:24-33.  kernel is "naive" or "tiled" (validated; the GPU always tiles)."""
+
+    seq_len: int = 0
+    segment_len: int = 0
+    interval: int = 1
+    num_heads: int = 1
+    head_dim: int = 0
+    head_offsets: List[int] = field(default_factory=list)
+    kernel: str = "naive"
+    tile_size: int = 1
+    scale_scores: bool = True
+    value_dim: int = 0  # 0 => d_v = d (the reference infers d_v from v)
+
+    def num_segments(self) -> int:
+        return (self.seq_len + self.segment_len - 1) // self.segment_len
+
+    def model_dim(self) -> int:
+        return self.num_heads * self.head_dim
+
+    @staticmethod
+    def spread_offsets(heads: int, interval: int) -> List[int]:
+        """attention.hpp:38-42: gamma_j = j mod r."""
+        return [j % interval for j in range(heads)]
+
+    def _c(self):
+        n = max(1, len(self.head_offsets), self.num_heads)
+        offs = (ctypes.c_int64 * n)(*[int(g) for g in self.head_offsets])
+        kern = {"naive": 0, "tiled": 1}.get(self.kernel, -1)
+        c = _lib.DfaConfig(
+            self.seq_len,
+            self.segment_len,
+            self.interval,
+            self.num_heads,
+            self.head_dim,
+            self.value_dim,
+            ctypes.cast(offs, ctypes.POINTER(ctypes.c_int64)) if self.head_offsets else None,
+            kern,
+            self.tile_size,
+            1 if self.scale_scores else 0,
+        )
+        c._keep = offs  # keep the offsets array alive with the struct
+        return c
+
+    def validate(self, require_full_coverage: bool = False) -> None:
+        """attention.hpp:44-65; raises ConfigError with the reference's message."""
+        if len(self.head_offsets) != self.num_heads:
+            raise ConfigError(f"attention: {len(self.head_offsets)} offsets for {self.num_heads} heads")
+        c = self._c()
+        _check(lib.dfa_validate(ctypes.byref(c), 1 if require_full_coverage else 0))
+
+
+@dataclass
+class SegmentView:
+    """attention.hpp:70-76."""
+
+    segment_index: int
+    offset: int
+    row_indices: List[int]
+
+
+def make_segment_view(seq_len: int, segment_len: int, interval: int, segment_index: int, offset: int) -> SegmentView:
+    """attention.hpp:84-98 (via the C-ABI)."""
+    count = ctypes.c_int64(0)
+    _check(lib.dfa_segment_view(seq_len, segment_len, interval, segment_index, offset, None, 0, ctypes.byref(count)))
+    rows = (ctypes.c_int64 * max(1, count.value))()
+    _check(lib.dfa_segment_view(seq_len, segment_len, interval, segment_index, offset, rows, count.value,
+                                ctypes.byref(count)))
+    return SegmentView(segment_index, offset, list(rows[: count.value]))
+
+
+@dataclass
+class FlopCount:
+    """attention.hpp:364-368 (multiplications only)."""
+
+    dense_mults: int
+    dilated_mults: int
+    ratio: float
+
+
+def flop_count(cfg: AttentionConfig) -> FlopCount:
+    """attention.hpp:370-387."""
+    if len(cfg.head_offsets) != cfg.num_heads:
+        cfg.validate()
+    c = cfg._c()
+    dn, dl, rt = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_double(0)
+    _check(lib.dfa_flop_count(ctypes.byref(c), ctypes.byref(dn), ctypes.byref(dl), ctypes.byref(rt)))
+    return FlopCount(dn.value, dl.value, rt.value)
+
+
+def flop_csv_header() -> str:
+    """attention.hpp:389."""
+    return "N,w,r,h,d,dense_mults,dilated_mults,ratio"
+
+
+def _fmt_double(x: float) -> str:
+    # std::ostream default formatting (%g with 6 significant digits).
+    return f"{x:g}"
+
+
+def flop_csv_row(cfg: AttentionConfig, fc: FlopCount) -> str:
+    """attention.hpp:391-394."""
+    return (f"{cfg.seq_len},{cfg.segment_len},{cfg.interval},{cfg.num_heads},{cfg.head_dim},"
+            f"{fc.dense_mults},{fc.dilated_mults},{_fmt_double(fc.ratio)}")
+
+
+# ----------------------------------------------------------------- device API
+def _torch():
+    import torch  # noqa: WPS433 -- torch is plumbing (device memory, streams)
+
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return _lib.DFA_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.DFA_BF16
+    raise DimensionError(f"dfa: unsupported dtype {t.dtype} (float32 or bfloat16)")
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def query_path(cfg: AttentionConfig, dtype: str = "bf16", batch: int = 1) -> int:
+    """Which device kernel dfa_forward takes (DFA_PATH_* in include/dfa.h)."""
+    c = cfg._c()
+    out = ctypes.c_int32(0)
+    _check(lib.dfa_query_path(ctypes.byref(c), _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16, batch,
+                              ctypes.byref(out)))
+    return out.value
+
+
+def last_launch_count() -> int:
+    return int(lib.dfa_last_launch_count())
+
+
+def dfa_forward(q, k, v, cfg: AttentionConfig, out=None, lse=None, stream=None):
+    """Batched multi-head forward: q, k [B, N, h, d], v [B, N, h, d_v] (CUDA,
+    contiguous, float32 or bfloat16) -> o [B, N, h, d_v].  Head j uses offset
+    cfg.head_offsets[j].  `lse`: optional float32 [B, h, N] output tensor."""
+    torch = _torch()
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not t.is_cuda:
+            raise DimensionError(f"dfa_forward: {name} is not a CUDA tensor (no CPU path)")
+        if t.dim() != 4:
+            raise DimensionError(f"dfa_forward: {name} must be [B, N, h, d], got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise DimensionError(f"dfa_forward: {name} must be contiguous")
+    B, N, h, d = q.shape
+    dv = v.shape[3]
+    if tuple(k.shape) != (B, N, h, d):
+        raise DimensionError(f"dfa_forward: query/key shape mismatch {tuple(q.shape)} vs {tuple(k.shape)}")
+    if tuple(v.shape[:3]) != (B, N, h):
+        raise DimensionError(f"dfa_forward: key/value shape mismatch {tuple(k.shape)} vs {tuple(v.shape)}")
+    if q.dtype != k.dtype or q.dtype != v.dtype:
+        raise DimensionError("dfa_forward: q, k, v dtypes differ")
+    if N != cfg.seq_len:
+        raise DimensionError(f"dfa_forward: expected {cfg.seq_len} rows, got {N}")
+    if h != cfg.num_heads or len(cfg.head_offsets) != h:
+        raise ConfigError(f"attention: {len(cfg.head_offsets)} offsets for {h} heads")
+    if d != cfg.head_dim:
+        raise DimensionError(f"dfa_forward: head_dim {cfg.head_dim} but q has width {d}")
+    if out is None:
+        out = torch.empty((B, N, h, dv), dtype=q.dtype, device=q.device)
+    elif tuple(out.shape) != (B, N, h, dv) or out.dtype != q.dtype or not out.is_contiguous():
+        raise DimensionError("dfa_forward: bad output tensor")
+    if lse is not None and (tuple(lse.shape) != (B, h, N) or lse.dtype != torch.float32 or not lse.is_contiguous()):
+        raise DimensionError("dfa_forward: lse must be float32 [B, h, N]")
+    c = cfg._c()
+    c.value_dim = dv
+    _check(lib.dfa_forward(ctypes.byref(c), _dtype_code(q), B, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                           out.data_ptr(), lse.data_ptr() if lse is not None else None, _stream_ptr(stream)))
+    return out
+
+
+def dilated_attention(q, k, v, cfg: AttentionConfig, head_offset: int, workers: int = 1, stream=None):
+    """attention.hpp:280-301 on CUDA tensors: q, k [N, d], v [N, d_v] -> [N, d_v].
+
+    Same checks and error types as the reference: cfg.validate(); q/k widths
+    and k/v rows must agree (require_qkv :102-110); q and k need cfg.seq_len
+    rows (:285-286); head_offset in [0, r) else OutOfRange (:287-288).
+    `workers` is accepted and ignored (the GPU grid replaces parallel_for)."""
+    del workers
+    cfg.validate()
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if t.dim() != 2:
+            raise DimensionError(f"dilated_attention: expected rank-2 tensor, got {list(t.shape)}")
+    if q.shape[1] != k.shape[1]:
+        raise DimensionError(f"dilated_attention: query/key width mismatch {list(q.shape)} vs {list(k.shape)}")
+    if k.shape[0] != v.shape[0]:
+        raise DimensionError(f"dilated_attention: key/value row mismatch {list(k.shape)} vs {list(v.shape)}")
+    if q.shape[0] != cfg.seq_len or k.shape[0] != cfg.seq_len:
+        raise DimensionError(f"dilated_attention: expected {cfg.seq_len} rows, got {q.shape[0]}")
+    if head_offset < 0 or head_offset >= cfg.interval:
+        raise OutOfRange(f"dilated_attention: head offset {head_offset} outside [0, {cfg.interval})")
+    one = AttentionConfig(cfg.seq_len, cfg.segment_len, cfg.interval, 1, q.shape[1], [head_offset], cfg.kernel,
+                          cfg.tile_size, cfg.scale_scores)
+    N, d = q.shape
+    out = dfa_forward(q.contiguous().view(1, N, 1, d), k.contiguous().view(1, N, 1, d),
+                      v.contiguous().view(1, N, 1, v.shape[1]), one, stream=stream)
+    return out.view(N, v.shape[1])
+
+
+class Workspace:
+    """Device staging buffer for the host-buffer entry points (dfa_workspace_t)."""
+
+    def __init__(self, nbytes: int):
+        self.handle = ctypes.c_void_p(0)
+        self.nbytes = nbytes
+        _check(lib.dfa_workspace_create(nbytes, ctypes.byref(self.handle)))
+
+    @staticmethod
+    def bytes_for(cfg: AttentionConfig, dtype: str, batch: int, with_lse: bool = False) -> int:
+        c = cfg._c()
+        out = ctypes.c_size_t(0)
+        _check(lib.dfa_workspace_bytes(ctypes.byref(c), _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16, batch,
+                                       1 if with_lse else 0, ctypes.byref(out)))
+        return out.value
+
+    def close(self) -> None:
+        if self.handle:
+            lib.dfa_workspace_destroy(self.handle)
+            self.handle = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter teardown
+            pass
+
+
+def dfa_forward_host(q, k, v, out, cfg: AttentionConfig, ws: Workspace, dtype: str = "bf16", lse=None, stream=None):
+    """End-to-end call on HOST tensors (pinned CPU torch tensors or anything
+    exposing data_ptr()): H2D, forward, D2H, synchronize -- all inside the
+    C-ABI (dfa_forward_host)."""
+    B = q.shape[0]
+    c = cfg._c()
+    c.value_dim = v.shape[-1]
+    code = _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16
+    sp = _stream_ptr(stream) if stream is not None else None
+    _check(lib.dfa_forward_host(ctypes.byref(c), code, B, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                lse.data_ptr() if lse is not None else None, ws.handle, sp))
+    return out
+
+
+@contextlib.contextmanager
+def fault_perturb():
+    """attention.hpp:237-241: arm the recompose fault hook inside the block."""
+    lib.dfa_set_fault_perturb(1)
+    try:
+        yield
+    finally:
+        lib.dfa_set_fault_perturb(0)
+
+
+@contextlib.contextmanager
+def path_override(path: int):
+    """Test hook: force DFA_PATH_SIMT or require DFA_PATH_SM100_TCGEN05."""
+    lib.dfa_set_path_override(path)
+    try:
+        yield
+    finally:
+        lib.dfa_set_path_override(0)

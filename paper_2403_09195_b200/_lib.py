@@ -1,0 +1,104 @@
+"""ctypes binding of the C-ABI in include/dfa.h (libdfa.so, built in-tree).
+
+There is no fallback: if libdfa.so is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdfa.so")
+
+DFA_OK = 0
+DFA_ERR_CONFIG = 1
+DFA_ERR_DIMENSION = 2
+DFA_ERR_OUT_OF_RANGE = 3
+DFA_ERR_CONTRACT = 4
+DFA_ERR_CUDA = 5
+DFA_ERR_UNSUPPORTED = 6
+
+DFA_F32 = 0
+DFA_BF16 = 1
+
+DFA_PATH_NONE = 0
+DFA_PATH_SM100_TCGEN05 = 1
+DFA_PATH_SIMT = 2
+
+# Every function include/dfa.h declares (tests check the .so exports them).
+EXPORTED = (
+    "dfa_last_error",
+    "dfa_validate",
+    "dfa_segment_view",
+    "dfa_flop_count",
+    "dfa_query_path",
+    "dfa_forward",
+    "dfa_workspace_create",
+    "dfa_workspace_destroy",
+    "dfa_dilated_attention_host",
+    "dfa_forward_host",
+    "dfa_set_fault_perturb",
+    "dfa_get_fault_perturb",
+    "dfa_workspace_bytes",
+    "dfa_set_path_override",
+    "dfa_last_launch_count",
+    "dfa_version",
+)
+
+
+class DfaConfig(ctypes.Structure):
+    """Mirror of dfa_config_t (include/dfa.h)."""
+
+    _fields_ = [
+        ("seq_len", ctypes.c_int64),
+        ("segment_len", ctypes.c_int64),
+        ("interval", ctypes.c_int64),
+        ("num_heads", ctypes.c_int64),
+        ("head_dim", ctypes.c_int64),
+        ("value_dim", ctypes.c_int64),
+        ("head_offsets", ctypes.POINTER(ctypes.c_int64)),
+        ("kernel", ctypes.c_int32),
+        ("tile_size", ctypes.c_int64),
+        ("scale_scores", ctypes.c_int32),
+    ]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `make -C paper_2403_09195_b200/csrc` "
+            "(or __graft_entry__.build()); there is no CPU fallback"
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    c_i64, c_i32, c_vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+    p_cfg = ctypes.POINTER(DfaConfig)
+    p_i64 = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "dfa_last_error": (ctypes.c_char_p, []),
+        "dfa_validate": (c_i32, [p_cfg, c_i32]),
+        "dfa_segment_view": (c_i32, [c_i64, c_i64, c_i64, c_i64, c_i64, p_i64, c_i64, p_i64]),
+        "dfa_flop_count": (
+            c_i32,
+            [p_cfg, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double)],
+        ),
+        "dfa_query_path": (c_i32, [p_cfg, c_i32, c_i64, ctypes.POINTER(c_i32)]),
+        "dfa_forward": (c_i32, [p_cfg, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+        "dfa_workspace_create": (c_i32, [ctypes.c_size_t, ctypes.POINTER(c_vp)]),
+        "dfa_workspace_destroy": (c_i32, [c_vp]),
+        "dfa_dilated_attention_host": (c_i32, [p_cfg, c_i32, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+        "dfa_forward_host": (c_i32, [p_cfg, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+        "dfa_set_fault_perturb": (None, [c_i32]),
+        "dfa_get_fault_perturb": (c_i32, []),
+        "dfa_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_i32, ctypes.POINTER(ctypes.c_size_t)]),
+        "dfa_set_path_override": (None, [c_i32]),
+        "dfa_last_launch_count": (c_i32, []),
+        "dfa_version": (c_i32, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()

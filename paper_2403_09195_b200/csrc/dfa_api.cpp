@@ -1,0 +1,293 @@
+// C-ABI layer (include/dfa.h): validation with the reference's rules and
+// messages, geometry resolution, device-path dispatch, host-buffer entry
+// points and the fault hook.  No CPU compute path exists: every forward is a
+// device kernel (tcgen05 for bf16/d=64 geometries, SIMT otherwise).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/dfa.h"
+#include "dfa_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int32_t g_launches = 0;
+std::atomic<int32_t> g_fault{0};
+std::atomic<int32_t> g_path_override{0};
+
+dfa_status_t fail(dfa_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+// attention.hpp:44-65, same order of checks and the same message text.
+dfa_status_t validate(const dfa_config_t* c, int32_t full) {
+  if (!c) return fail(DFA_ERR_CONFIG, "attention: null config");
+  const long long n = c->seq_len, w = c->segment_len, r = c->interval, h = c->num_heads, d = c->head_dim;
+  if (n < 1) return fail(DFA_ERR_CONFIG, "attention: seq_len must be positive");
+  if (w < 1 || w > n) return fail(DFA_ERR_CONFIG, "attention: need 1 <= w <= N, got w=%lld N=%lld", w, n);
+  if (r < 1 || r > w) return fail(DFA_ERR_CONFIG, "attention: need 1 <= r <= w, got r=%lld w=%lld", r, w);
+  if (h < 1) return fail(DFA_ERR_CONFIG, "attention: num_heads must be positive");
+  if (d < 1) return fail(DFA_ERR_CONFIG, "attention: head_dim must be positive");
+  if (!c->head_offsets) return fail(DFA_ERR_CONFIG, "attention: 0 offsets for %lld heads", h);
+  for (long long j = 0; j < h; ++j) {
+    const long long g = c->head_offsets[j];
+    if (g < 0 || g >= r) return fail(DFA_ERR_CONFIG, "attention: offset %lld outside [0, %lld)", g, r);
+  }
+  if (c->kernel == DFA_KERNEL_TILED && c->tile_size < 1)
+    return fail(DFA_ERR_CONFIG, "attention: tile_size must be >= 1");
+  if (c->kernel != DFA_KERNEL_NAIVE && c->kernel != DFA_KERNEL_TILED)
+    return fail(DFA_ERR_CONFIG, "attention: unknown kernel %d", (int)c->kernel);
+  if (c->value_dim < 0) return fail(DFA_ERR_CONFIG, "attention: value_dim must be non-negative");
+  if (full) {
+    for (long long cls = 0; cls < r; ++cls) {
+      bool hit = false;
+      for (long long j = 0; j < h && !hit; ++j) hit = (c->head_offsets[j] % r) == cls;
+      if (!hit)
+        return fail(DFA_ERR_CONFIG,
+                    "attention: offset class %lld of interval %lld is covered by no head; full coverage needs h >= r",
+                    cls, r);
+    }
+  }
+  return DFA_OK;
+}
+
+dfa_status_t resolve(const dfa_config_t* c, int64_t batch, dfa_impl::Geometry* g) {
+  dfa_status_t st = validate(c, 0);
+  if (st != DFA_OK) return st;
+  if (batch < 0) return fail(DFA_ERR_DIMENSION, "dfa_forward: negative batch %lld", (long long)batch);
+  if (c->num_heads > dfa_impl::kMaxHeads)
+    return fail(DFA_ERR_UNSUPPORTED, "dfa_forward: %lld heads exceeds the device limit %d",
+                (long long)c->num_heads, dfa_impl::kMaxHeads);
+  g->B = batch;
+  g->N = c->seq_len;
+  g->w = c->segment_len;
+  g->r = c->interval;
+  g->h = c->num_heads;
+  g->d = c->head_dim;
+  g->dv = c->value_dim > 0 ? c->value_dim : c->head_dim;
+  if (g->d > 256 || g->dv > 256)
+    return fail(DFA_ERR_UNSUPPORTED, "dfa_forward: head_dim %lld / value_dim %lld exceed the device limit 256",
+                (long long)g->d, (long long)g->dv);
+  g->n_seg = (g->N + g->w - 1) / g->w;
+  g->m_max = (g->w + g->r - 1) / g->r;
+  // attention.hpp:112-115: Scalar(1)/sqrt(Scalar(d)) in the working precision.
+  g->scale = c->scale_scores ? 1.0f / sqrtf((float)g->d) : 1.0f;
+  for (int j = 0; j < dfa_impl::kMaxHeads; ++j) g->offsets[j] = j < g->h ? (int32_t)c->head_offsets[j] : 0;
+  return DFA_OK;
+}
+
+int pick_path(const dfa_impl::Geometry& g, dfa_dtype_t dtype, const void* q, const void* k, const void* v,
+              const void* o) {
+  const int ov = g_path_override.load();
+  if (ov == DFA_PATH_SIMT) return DFA_PATH_SIMT;
+  if (dfa_impl::sm100_supported(g, dtype, q, k, v, o)) return DFA_PATH_SM100_TCGEN05;
+  if (ov == DFA_PATH_SM100_TCGEN05) return DFA_PATH_NONE;  // forced but not applicable
+  return DFA_PATH_SIMT;
+}
+
+size_t elem_size(dfa_dtype_t t) { return t == DFA_F32 ? 4 : 2; }
+
+}  // namespace
+
+struct dfa_workspace {
+  void* dev = nullptr;
+  size_t bytes = 0;
+};
+
+extern "C" {
+
+const char* dfa_last_error(void) { return g_last_error.c_str(); }
+int32_t dfa_version(void) { return 100; }
+int32_t dfa_last_launch_count(void) { return g_launches; }
+void dfa_set_fault_perturb(int32_t armed) { g_fault.store(armed ? 1 : 0); }
+int32_t dfa_get_fault_perturb(void) { return g_fault.load(); }
+void dfa_set_path_override(int32_t path) { g_path_override.store(path); }
+
+dfa_status_t dfa_validate(const dfa_config_t* cfg, int32_t require_full_coverage) {
+  return validate(cfg, require_full_coverage);
+}
+
+// attention.hpp:84-98
+dfa_status_t dfa_segment_view(int64_t n, int64_t w, int64_t r, int64_t i, int64_t g, int64_t* rows, int64_t cap,
+                              int64_t* count) {
+  if (w < 1 || r < 1) return fail(DFA_ERR_CONFIG, "segment view: need w >= 1 and r >= 1");
+  const int64_t n_seg = (n + w - 1) / w;
+  if (i < 0 || i >= n_seg)
+    return fail(DFA_ERR_OUT_OF_RANGE, "segment index %lld outside [0, %lld)", (long long)i, (long long)n_seg);
+  if (g < 0 || g >= r)
+    return fail(DFA_ERR_OUT_OF_RANGE, "segment offset %lld outside [0, %lld)", (long long)g, (long long)r);
+  const int64_t begin = i * w;
+  const int64_t end = begin + w < n ? begin + w : n;
+  int64_t c = 0;
+  for (int64_t row = begin + g; row < end; row += r) {
+    if (rows && c < cap) rows[c] = row;
+    ++c;
+  }
+  if (count) *count = c;
+  return DFA_OK;
+}
+
+// attention.hpp:370-387
+dfa_status_t dfa_flop_count(const dfa_config_t* cfg, uint64_t* dense, uint64_t* dilated, double* ratio) {
+  dfa_status_t st = validate(cfg, 0);
+  if (st != DFA_OK) return st;
+  const uint64_t n = (uint64_t)cfg->seq_len, d = (uint64_t)cfg->head_dim, h = (uint64_t)cfg->num_heads;
+  uint64_t dl = 0;
+  const int64_t n_seg = (cfg->seq_len + cfg->segment_len - 1) / cfg->segment_len;
+  for (int64_t j = 0; j < cfg->num_heads; ++j)
+    for (int64_t i = 0; i < n_seg; ++i) {
+      int64_t m = 0;
+      dfa_segment_view(cfg->seq_len, cfg->segment_len, cfg->interval, i, cfg->head_offsets[j], nullptr, 0, &m);
+      dl += 2u * (uint64_t)m * (uint64_t)m * d;
+    }
+  const uint64_t dn = h * 2u * n * n * d;
+  if (dense) *dense = dn;
+  if (dilated) *dilated = dl;
+  if (ratio) *ratio = (double)dn / (double)dl;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_query_path(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t* path) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(cfg, batch, &g);
+  if (st != DFA_OK) return st;
+  // Alignment is a property of the call's pointers; assume allocator alignment.
+  static const char aligned[16] __attribute__((aligned(16))) = {0};
+  *path = pick_path(g, dtype, aligned, aligned, aligned, aligned);
+  return DFA_OK;
+}
+
+dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
+                         const void* v, void* o, float* lse, void* stream) {
+  g_launches = 0;
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(cfg, batch, &g);
+  if (st != DFA_OK) return st;
+  if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_CONFIG, "dfa_forward: unknown dtype %d", (int)dtype);
+  if (batch == 0) return DFA_OK;
+  if (!q || !k || !v || !o) return fail(DFA_ERR_DIMENSION, "dfa_forward: null tensor pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int path = pick_path(g, dtype, q, k, v, o);
+  cudaError_t err = cudaSuccess;
+  int launches = 0;
+  if (path == DFA_PATH_SM100_TCGEN05) {
+    const char* why = "";
+    launches = dfa_impl::launch_sm100(g, q, k, v, o, lse, s, &err, &why);
+    if (launches == 0 && err != cudaSuccess)
+      return fail(DFA_ERR_CUDA, "dfa_forward: sm100 path: %s (%s)", why, cudaGetErrorString(err));
+  } else if (path == DFA_PATH_SIMT) {
+    launches = dfa_impl::launch_simt(g, dtype, q, k, v, o, lse, s, &err);
+  } else {
+    return fail(DFA_ERR_UNSUPPORTED, "dfa_forward: forced tcgen05 path does not cover this call");
+  }
+  if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "dfa_forward: launch failed: %s", cudaGetErrorString(err));
+  if (g_fault.load()) {
+    launches += dfa_impl::launch_perturb(dtype, o, s);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "dfa_forward: fault hook: %s", cudaGetErrorString(err));
+  }
+  g_launches = launches;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_workspace_create(size_t bytes, dfa_workspace_t** ws) {
+  if (!ws) return fail(DFA_ERR_DIMENSION, "dfa_workspace_create: null handle");
+  auto* w = new dfa_workspace;
+  if (bytes) {
+    cudaError_t err = cudaMalloc(&w->dev, bytes);
+    if (err != cudaSuccess) {
+      delete w;
+      return fail(DFA_ERR_CUDA, "dfa_workspace_create: %s", cudaGetErrorString(err));
+    }
+  }
+  w->bytes = bytes;
+  *ws = w;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_workspace_destroy(dfa_workspace_t* ws) {
+  if (!ws) return DFA_OK;
+  if (ws->dev) cudaFree(ws->dev);
+  delete ws;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                              const void* k, const void* v, void* o, float* lse, dfa_workspace_t* ws,
+                              void* stream) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(cfg, batch, &g);
+  if (st != DFA_OK) return st;
+  if (batch == 0) return DFA_OK;
+  if (!ws) return fail(DFA_ERR_DIMENSION, "dfa_forward_host: null workspace");
+  const size_t es = elem_size(dtype);
+  const size_t bqk = (size_t)(g.B * g.N * g.h * g.d) * es;
+  const size_t bv = (size_t)(g.B * g.N * g.h * g.dv) * es;
+  const size_t bl = lse ? (size_t)(g.B * g.h * g.N) * 4 : 0;
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t need = up(bqk) * 2 + up(bv) * 2 + up(bl);
+  if (ws->bytes < need)
+    return fail(DFA_ERR_DIMENSION, "dfa_forward_host: workspace has %zu bytes, needs %zu", ws->bytes, need);
+  char* base = static_cast<char*>(ws->dev);
+  void* dq = base;
+  void* dk = base + up(bqk);
+  void* dv = base + 2 * up(bqk);
+  void* dout = base + 2 * up(bqk) + up(bv);
+  float* dl = lse ? reinterpret_cast<float*>(base + 2 * up(bqk) + 2 * up(bv)) : nullptr;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t err;
+  if ((err = cudaMemcpyAsync(dq, q, bqk, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (err = cudaMemcpyAsync(dk, k, bqk, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+      (err = cudaMemcpyAsync(dv, v, bv, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return fail(DFA_ERR_CUDA, "dfa_forward_host: H2D: %s", cudaGetErrorString(err));
+  st = dfa_forward(cfg, dtype, batch, dq, dk, dv, dout, dl, stream);
+  if (st != DFA_OK) return st;
+  if ((err = cudaMemcpyAsync(o, dout, bv, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (lse && (err = cudaMemcpyAsync(lse, dl, bl, cudaMemcpyDeviceToHost, s)) != cudaSuccess))
+    return fail(DFA_ERR_CUDA, "dfa_forward_host: D2H: %s", cudaGetErrorString(err));
+  if ((err = cudaStreamSynchronize(s)) != cudaSuccess)
+    return fail(DFA_ERR_CUDA, "dfa_forward_host: %s", cudaGetErrorString(err));
+  return DFA_OK;
+}
+
+dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t with_lse,
+                                 size_t* bytes) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(cfg, batch, &g);
+  if (st != DFA_OK) return st;
+  const size_t es = elem_size(dtype);
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  *bytes = up((size_t)(g.B * g.N * g.h * g.d) * es) * 2 + up((size_t)(g.B * g.N * g.h * g.dv) * es) * 2 +
+           (with_lse ? up((size_t)(g.B * g.h * g.N) * 4) : 0);
+  return DFA_OK;
+}
+
+// attention.hpp:280-301 on host buffers: single head at `head_offset`.
+dfa_status_t dfa_dilated_attention_host(const dfa_config_t* cfg, dfa_dtype_t dtype, const void* q, const void* k,
+                                        const void* v, int64_t head_offset, int32_t workers, void* out,
+                                        dfa_workspace_t* ws) {
+  (void)workers;
+  dfa_status_t st = validate(cfg, 0);
+  if (st != DFA_OK) return st;
+  if (head_offset < 0 || head_offset >= cfg->interval)
+    return fail(DFA_ERR_OUT_OF_RANGE, "dilated_attention: head offset %lld outside [0, %lld)",
+                (long long)head_offset, (long long)cfg->interval);
+  dfa_config_t one = *cfg;
+  one.num_heads = 1;
+  one.head_offsets = &head_offset;
+  return dfa_forward_host(&one, dtype, 1, q, k, v, out, nullptr, ws, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,36 @@
+// Internal declarations shared by the C-ABI layer (dfa_api.cpp) and the
+// device kernels (dfa_simt.cu, dfa_sm100.cu).  Not installed.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dfa_impl {
+
+constexpr int kMaxHeads = 256;  // head offsets travel in the kernel parameter block
+
+// Validated geometry of one dfa_forward call.
+struct Geometry {
+  int64_t B, N, w, r, h, d, dv;
+  int64_t n_seg;  // ceil(N / w)            attention.hpp:35
+  int64_t m_max;  // ceil(w / r): rows per full view
+  float scale;    // 1/sqrt(d) or 1         attention.hpp:112-115
+  int32_t offsets[kMaxHeads];
+};
+
+// Generic SIMT kernel: any geometry, f32 (validation mode) or bf16 I/O,
+// fp32 arithmetic, online softmax over key tiles.  Returns launches issued.
+int launch_simt(const Geometry& g, int dtype, const void* q, const void* k, const void* v, void* o, float* lse,
+                cudaStream_t stream, cudaError_t* err);
+
+// True when the tcgen05/TMA kernel covers this call.
+bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o);
+
+// tcgen05/TMEM/TMA kernel (bf16 in/out, fp32 accumulate).  Returns launches.
+int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
+                 cudaStream_t stream, cudaError_t* err, const char** why);
+
+// Fault hook (attention.hpp:272): out[0] += 1e-3.
+int launch_perturb(int dtype, void* o, cudaStream_t stream);
+
+}  // namespace dfa_impl

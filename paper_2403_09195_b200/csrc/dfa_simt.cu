@@ -1,0 +1,192 @@
+// Generic SIMT Dilated Flash Attention kernel (sm_100a).
+//
+// The validation / general-geometry device path: any (N, w, r, gamma), tail
+// segments (w does not divide N), empty views (gamma >= tail length), any
+// d, d_v <= 256, fp32 (the north_star's fp32 validation mode) or bf16 I/O.
+// Arithmetic is fp32 FFMA with an online softmax over key tiles -- the
+// recurrence of the reference's tiled kernel (attention.hpp:170-205) -- and
+// accurate expf/logf.  One CTA = (image b, head j, segment i, chunk of 128
+// kept query rows); thread t owns query row t of the view.  Chunk 0 of each
+// segment also writes the segment's unselected rows as exact zeros
+// (attention.hpp:243-245, 270), so the output is fully defined without a
+// memset.  Index math is the closed form of make_segment_view
+// (attention.hpp:84-98): view rows are seg_begin + gamma + t*r.
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "dfa_internal.h"
+
+namespace dfa_impl {
+namespace {
+
+struct SimtParams {
+  int64_t N, w, r, h, d, dv, n_chunks;
+  float scale;
+  int32_t offsets[kMaxHeads];
+};
+
+template <typename T>
+__device__ __forceinline__ float to_f(T x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) {
+  return x;
+}
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) {
+  return x;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+template <typename T, int DMAX, int KT>
+__global__ void __launch_bounds__(128) simt_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                   const T* __restrict__ v, T* __restrict__ o,
+                                                   float* __restrict__ lse, const __grid_constant__ SimtParams p) {
+  __shared__ float ks[KT][DMAX];
+  __shared__ float vs[KT][DMAX];
+
+  const int tid = threadIdx.x;
+  const int64_t seg = blockIdx.x / p.n_chunks;
+  const int64_t chunk = blockIdx.x % p.n_chunks;
+  const int64_t j = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const int64_t g = p.offsets[j];
+  const int64_t seg_begin = seg * p.w;
+  const int64_t seg_end = min(seg_begin + p.w, p.N);
+  const int64_t seg_rows = seg_end - seg_begin;
+  const int64_t m = g >= seg_rows ? 0 : (seg_rows - g + p.r - 1) / p.r;  // attention.hpp:96
+  const int64_t hd = p.h * p.d, hdv = p.h * p.dv;
+  const T* qb = q + b * p.N * hd + j * p.d;
+  const T* kb = k + b * p.N * hd + j * p.d;
+  const T* vb = v + b * p.N * hdv + j * p.dv;
+  T* ob = o + b * p.N * hdv + j * p.dv;
+  float* lb = lse ? lse + (b * p.h + j) * p.N : nullptr;
+
+  // Rows of this segment that the view does not select: exact zeros.
+  if (chunk == 0) {
+    for (int64_t l = tid; l < seg_rows; l += blockDim.x) {
+      if (l % p.r == g && l >= g) continue;
+      T* orow = ob + (seg_begin + l) * hdv;
+      for (int64_t c = 0; c < p.dv; ++c) orow[c] = from_f<T>(0.0f);
+      if (lb) lb[seg_begin + l] = -INFINITY;
+    }
+  }
+  if (chunk * 128 >= m) return;
+
+  const int64_t t = chunk * 128 + tid;
+  const bool active = t < m;
+  const int64_t row = seg_begin + g + t * p.r;
+  float qr[DMAX], acc[DMAX];
+#pragma unroll
+  for (int c = 0; c < DMAX; ++c) {
+    qr[c] = (active && c < p.d) ? to_f(qb[row * hd + c]) : 0.0f;
+    acc[c] = 0.0f;
+  }
+  float mx = -INFINITY, l = 0.0f;
+
+  for (int64_t k0 = 0; k0 < m; k0 += KT) {
+    __syncthreads();
+    for (int e = tid; e < KT * DMAX; e += blockDim.x) {
+      const int jj = e / DMAX, c = e % DMAX;
+      const int64_t tk = k0 + jj;
+      const int64_t krow = seg_begin + g + tk * p.r;
+      ks[jj][c] = (tk < m && c < p.d) ? to_f(kb[krow * hd + c]) : 0.0f;
+      vs[jj][c] = (tk < m && c < p.dv) ? to_f(vb[krow * hdv + c]) : 0.0f;
+    }
+    __syncthreads();
+    if (!active) continue;
+    float s[KT];
+    float tmax = -INFINITY;
+#pragma unroll
+    for (int jj = 0; jj < KT; ++jj) {
+      float dot = 0.0f;
+#pragma unroll
+      for (int c = 0; c < DMAX; ++c) dot = fmaf(qr[c], ks[jj][c], dot);
+      s[jj] = (k0 + jj < m) ? dot * p.scale : -INFINITY;
+      tmax = fmaxf(tmax, s[jj]);
+    }
+    const float nmax = fmaxf(mx, tmax);
+    const float corr = expf(mx - nmax);
+    l *= corr;
+#pragma unroll
+    for (int c = 0; c < DMAX; ++c) acc[c] *= corr;
+#pragma unroll
+    for (int jj = 0; jj < KT; ++jj) {
+      const float pj = expf(s[jj] - nmax);
+      l += pj;
+#pragma unroll
+      for (int c = 0; c < DMAX; ++c) acc[c] = fmaf(pj, vs[jj][c], acc[c]);
+    }
+    mx = nmax;
+  }
+  if (active) {
+    const float inv = 1.0f / l;
+    T* orow = ob + row * hdv;
+#pragma unroll
+    for (int c = 0; c < DMAX; ++c)
+      if (c < p.dv) orow[c] = from_f<T>(acc[c] * inv);
+    if (lb) lb[row] = mx + logf(l);
+  }
+}
+
+template <typename T, int DMAX, int KT>
+int launch_t(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
+             cudaStream_t stream, cudaError_t* err) {
+  SimtParams p;
+  p.N = g.N;
+  p.w = g.w;
+  p.r = g.r;
+  p.h = g.h;
+  p.d = g.d;
+  p.dv = g.dv;
+  p.n_chunks = (g.m_max + 127) / 128;
+  if (p.n_chunks < 1) p.n_chunks = 1;
+  p.scale = g.scale;
+  for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
+  dim3 grid((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
+  simt_kernel<T, DMAX, KT><<<grid, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o, lse, p);
+  *err = cudaGetLastError();
+  return 1;
+}
+
+template <typename T>
+int launch_dtype(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
+                 cudaStream_t stream, cudaError_t* err) {
+  const int64_t dm = g.d > g.dv ? g.d : g.dv;
+  if (dm <= 16) return launch_t<T, 16, 64>(g, q, k, v, o, lse, stream, err);
+  if (dm <= 32) return launch_t<T, 32, 64>(g, q, k, v, o, lse, stream, err);
+  if (dm <= 64) return launch_t<T, 64, 32>(g, q, k, v, o, lse, stream, err);
+  if (dm <= 128) return launch_t<T, 128, 16>(g, q, k, v, o, lse, stream, err);
+  return launch_t<T, 256, 8>(g, q, k, v, o, lse, stream, err);
+}
+
+template <typename T>
+__global__ void perturb_kernel(T* o) {
+  o[0] = from_f<T>(to_f(o[0]) + 1e-3f);
+}
+
+}  // namespace
+
+int launch_simt(const Geometry& g, int dtype, const void* q, const void* k, const void* v, void* o, float* lse,
+                cudaStream_t stream, cudaError_t* err) {
+  if (dtype == 0) return launch_dtype<float>(g, q, k, v, o, lse, stream, err);
+  return launch_dtype<__nv_bfloat16>(g, q, k, v, o, lse, stream, err);
+}
+
+int launch_perturb(int dtype, void* o, cudaStream_t stream) {
+  if (dtype == 0)
+    perturb_kernel<float><<<1, 1, 0, stream>>>((float*)o);
+  else
+    perturb_kernel<__nv_bfloat16><<<1, 1, 0, stream>>>((__nv_bfloat16*)o);
+  return 1;
+}
+
+}  // namespace dfa_impl
