@@ -1,4 +1,5 @@
-// Dilated Flash Attention forward for sm_100a: TMA + tcgen05 + TMEM.
+// Dilated Flash Attention forward for sm_100a: TMA + tcgen05 + TMEM,
+// persistent and warp-specialised.
 //
 // Reference path: attnkit::dilated_attention (attention.hpp:280-301):
 // per segment i and head offset gamma, gather rows i*w+gamma+t*r
@@ -7,30 +8,37 @@
 // back into a zero-initialised [N, d] (recompose :246-274).
 //
 // B200 restatement.  With N % r == 0 the [B, N, h, d] bf16 tensor IS the
-// contiguous 4-D tensor [B*N/r][r][h][d]; row n of image b sits at
-// (t' = (b*N+n)/r, gamma' = n % r).  For head j the view rows of ALL segments
+// contiguous 5-D tensor [B][N/r][r][h][d]; row n of image b sits at
+// (b, t' = n / r, gamma' = n % r).  For head j the view rows of ALL segments
 // are the t'-stream at gamma' = gamma_j, and segment i is the contiguous block
-// t' in [i*m, i*m+m) (m = w/r when r | w; the tail segment is shorter).  So the
-// segment + strided gather of the reference is a plain TMA box
-// (d=64, h=1, gamma'=1, t'=128) at coordinates (0, j, gamma_j, t'0): no index
-// arrays, no gather kernel.  Attention is block-diagonal in t'-space.
+// t' in [i*m, i*m+m) (m = w/r when r | w; the tail segment is shorter).  The
+// segment + strided gather of the reference is therefore a plain TMA box
+// (d=64, h=1, gamma'=1, t'=128, b=1) at (0, j, gamma_j, t'0, b): no index
+// arrays, no gather kernel.  Attention is block-diagonal in t'-space.  The
+// recompose scatter is the same box stored back, plus r-1 boxes of zeros for
+// the other offset classes (attention.hpp:243-245, 270), so every output byte
+// is written exactly once and no memset is needed.
 //
-// One CTA = one 128-row query tile of one (b, j) t'-stream.  Key tiles of 128
-// t'-rows cover the union of the segments the query tile touches; keys outside
-// a query's own segment are masked (only needed when m is not a multiple of
-// 128 or at the tail).  Per key tile:
-//   S = Q K^T       tcgen05.mma M=128 N=128 K=64, fp32 accumulator in TMEM
-//   softmax         4 warps, thread = query row = TMEM lane; tcgen05.ld of the
-//                   row, exp2 with the 1/sqrt(d)*log2(e) fold, running max with
-//                   a lazy (threshold 2^8) rescale of O, P packed to bf16 and
-//                   written back into TMEM over the consumed S columns
-//   O += P V        tcgen05.mma with A = P from TMEM, B = V (MN-major) in smem
-// Epilogue: O / l, bf16, stored at rows t'*r + gamma_j; the same threads write
-// the rows of the other r-1 offset classes as exact zeros, so the output
-// needs no memset and every byte of o is written exactly once.
+// Work unit = 256 consecutive t'-rows of one (b, j) stream: query tile A
+// (rows t0..t0+127) and query tile B (t0+128..t0+255).  Key tiles of 128
+// t'-rows cover the union of the segments either tile touches and are loaded
+// ONCE per unit (for m >= 256 both tiles share them).  Keys outside a query's
+// own segment are masked (only when m is not a multiple of 128, or at tails).
 //
-// Warp roles (160 threads): warps 0-3 softmax + epilogue (TMEM lanes 0-127),
-// warp 4 = producer: one elected lane issues all TMA loads and MMAs.
+// Warp roles (384 threads, one CTA per SM, persistent over units):
+//   warp 0      TMA producer: Q_A/Q_B (2-deep), K/V tiles (3-deep ring)
+//   warp 1      MMA issuer (one elected lane):
+//                 S_x = Q_x K^T   tcgen05.mma M=128 N=128 K=64 -> TMEM (fp32)
+//                 O_x += P_x V    tcgen05.mma A = P_x from TMEM, B = V (MN-major)
+//               ping-ponging slot A and slot B so one softmax overlaps the
+//               other slot's MMAs
+//   warp 2      TMEM allocator (512 columns: S_A, S_B, O_A, O_B)
+//   warps 4-7   slot A softmax + epilogue (TMEM lanes 0-127, thread = row)
+//   warps 8-11  slot B softmax + epilogue
+// Softmax: tcgen05.ld of the 128-score row, exp2 with the 1/sqrt(d)*log2(e)
+// fold, lazy (2^8 threshold) rescale of O in TMEM, P packed to bf16 and
+// tcgen05.st over the consumed S columns.  Epilogue: O/l -> bf16 -> 128B-
+// swizzled smem staging -> TMA store; zero rows by TMA store from a zero tile.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -45,83 +53,122 @@
 namespace dfa_impl {
 namespace {
 
-constexpr int kD = 64;                // head_dim handled by this kernel
-constexpr int kBM = 128;              // query rows per CTA (MMA M)
-constexpr int kBN = 128;              // keys per tile (MMA N of Q K^T, K of P V)
-constexpr int kTileBytes = 128 * 128; // 128 rows x 128 B (64 bf16), SW128
-constexpr int kStages = 2;            // K/V ring depth
-constexpr int kThreads = 160;
-constexpr uint32_t kTmemCols = 256;   // S/P at [0,128), O at [128,192)
-constexpr uint32_t kColS = 0, kColO = 128;
+constexpr int kD = 64;                 // head_dim handled by this kernel
+constexpr int kBM = 128;               // query rows per slot (MMA M)
+constexpr int kBN = 128;               // keys per tile (MMA N of Q K^T, K of P V)
+constexpr int kUnitRows = 2 * kBM;     // t'-rows per work unit
+constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 bf16), SW128
+constexpr int kQStages = 2;
+constexpr int kKVStages = 3;
+constexpr int kThreads = 384;
+constexpr uint32_t kTmemCols = 512;
+__host__ __device__ constexpr uint32_t col_s(int slot) { return 128u * slot; }        // S_A, S_B (P aliases)
+__host__ __device__ constexpr uint32_t col_o(int slot) { return 256u + 64u * slot; }  // O_A, O_B
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units: p <= 2^8 before a rescale
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: p <= 2^8 between rescales
 
 struct __align__(1024) SmemLayout {
-  uint8_t q[kTileBytes];
-  uint8_t k[kStages][kTileBytes];
-  uint8_t v[kStages][kTileBytes];
-  uint64_t bar_q;
-  uint64_t bar_full[kStages];
-  uint64_t bar_empty[kStages];
-  uint64_t bar_s;
-  uint64_t bar_p;
-  uint64_t bar_o;
+  uint8_t q[kQStages][2][kTileBytes];
+  uint8_t k[kKVStages][kTileBytes];
+  uint8_t v[kKVStages][kTileBytes];
+  uint8_t ostage[2][kTileBytes];
+  uint8_t zero[kTileBytes];
+  uint64_t q_full[kQStages], q_empty[kQStages];
+  uint64_t kv_full[kKVStages], kv_empty[kKVStages];
+  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
   uint32_t tmem_base;
 };
 
 struct Sm100Params {
-  int64_t N, T;        // T = N / r (t'-stream length per (b, j))
-  int64_t m;           // t'-rows per full segment (w / r)
-  int32_t r, h, n_qt;  // n_qt = ceil(T / 128)
-  float c;             // scale * log2(e)
+  int32_t N, T;      // T = N / r (t'-stream length per (b, j))
+  int32_t m;         // t'-rows per full segment (w / r)
+  int32_t r, h;
+  int32_t n_pairs;   // ceil(T / 256) work units per (b, j) stream
+  int32_t n_units;   // B * h * n_pairs
+  float c;           // scale * log2(e)
   float scale;
   int32_t offsets[kMaxHeads];
 };
 
-__device__ __forceinline__ uint32_t tmem_addr(uint32_t base, uint32_t lane, uint32_t col) {
-  return base + (lane << 16) + col;
+// Geometry of one work unit, identical in every role.
+struct Unit {
+  int32_t b, j, gamma;
+  int32_t t0;         // first t' of slot A
+  int32_t kv_lo;      // first key t' (a segment start)
+  int32_t n_kv;       // key tiles in the unit
+  int32_t kt0[2], kt1[2];  // key-tile range [kt0, kt1) of each slot (empty if kt0 == kt1)
+};
+
+__device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
+  Unit x;
+  const int32_t pair = u % p.n_pairs;
+  const int32_t bj = u / p.n_pairs;
+  x.j = bj % p.h;
+  x.b = bj / p.h;
+  x.gamma = p.offsets[x.j];
+  x.t0 = pair * kUnitRows;
+  int32_t lo[2], hi[2];
+  for (int s = 0; s < 2; ++s) {
+    const int32_t r0 = x.t0 + s * kBM;
+    const int32_t r1 = min(r0 + kBM, p.T);
+    if (r0 < r1) {
+      lo[s] = (r0 / p.m) * p.m;
+      hi[s] = min(((r1 - 1) / p.m + 1) * p.m, p.T);
+    } else {
+      lo[s] = hi[s] = -1;
+    }
+  }
+  x.kv_lo = lo[0];
+  const int32_t kv_hi = hi[1] >= 0 ? max(hi[0], hi[1]) : hi[0];
+  x.n_kv = (kv_hi - x.kv_lo + kBN - 1) / kBN;
+  for (int s = 0; s < 2; ++s) {
+    if (lo[s] < 0) {
+      x.kt0[s] = x.kt1[s] = 0;
+    } else {
+      x.kt0[s] = (lo[s] - x.kv_lo) / kBN;
+      x.kt1[s] = (hi[s] - x.kv_lo + kBN - 1) / kBN;
+    }
+  }
+  return x;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                     const __grid_constant__ CUtensorMap tm_v, __nv_bfloat16* __restrict__ o,
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                      float* __restrict__ lse, const __grid_constant__ Sm100Params p) {
   extern __shared__ uint8_t smem_raw[];
-  SmemLayout& sm = *reinterpret_cast<SmemLayout*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  SmemLayout& sm =
+      *reinterpret_cast<SmemLayout*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
 
-  // Work item: query tile qt of stream (b, j).
-  const int64_t idx = blockIdx.x;
-  const int32_t qt = (int32_t)(idx % p.n_qt);
-  const int64_t bj = idx / p.n_qt;
-  const int32_t j = (int32_t)(bj % p.h);
-  const int64_t b = bj / p.h;
-  const int32_t gamma = p.offsets[j];
-  const int64_t t0 = (int64_t)qt * kBM;                 // first query t' (stream-local)
-  const int64_t t_last = min(t0 + kBM, p.T) - 1;        // last valid query t'
-  const int64_t kv_lo = (t0 / p.m) * p.m;               // first key t' (segment start)
-  const int64_t kv_hi = min((t_last / p.m + 1) * p.m, p.T);
-  const int32_t n_kv = (int32_t)((kv_hi - kv_lo + kBN - 1) / kBN);
-  const int64_t row0 = b * p.T;                          // stream origin in global t'
+  // zero tile for the unselected offset classes
+  for (uint32_t i = threadIdx.x; i < kTileBytes / 16; i += kThreads)
+    ptx::st_shared_v4(ptx::smem_u32(sm.zero) + 16 * i, 0u, 0u, 0u, 0u);
+  ptx::fence_proxy_async_smem();
 
-  if (warp == 4) {
-    if (lane == 0) {
-      ptx::mbar_init(&sm.bar_q, 1);
-      for (int s = 0; s < kStages; ++s) {
-        ptx::mbar_init(&sm.bar_full[s], 1);
-        ptx::mbar_init(&sm.bar_empty[s], 1);
-      }
-      ptx::mbar_init(&sm.bar_s, 1);
-      ptx::mbar_init(&sm.bar_p, kBM);
-      ptx::mbar_init(&sm.bar_o, 1);
-      ptx::fence_barrier_init();
-      ptx::tma_prefetch_desc(&tm_q);
-      ptx::tma_prefetch_desc(&tm_k);
-      ptx::tma_prefetch_desc(&tm_v);
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kQStages; ++s) {
+      ptx::mbar_init(&sm.q_full[s], 1);
+      ptx::mbar_init(&sm.q_empty[s], 1);
     }
-  } else if (warp == 0) {
+    for (int s = 0; s < kKVStages; ++s) {
+      ptx::mbar_init(&sm.kv_full[s], 1);
+      ptx::mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&sm.s_full[s], 1);
+      ptx::mbar_init(&sm.p_full[s], kBM);
+      ptx::mbar_init(&sm.o_full[s], 1);
+      ptx::mbar_init(&sm.o_empty[s], kBM);
+    }
+    ptx::fence_barrier_init();
+    ptx::tma_prefetch_desc(&tm_q);
+    ptx::tma_prefetch_desc(&tm_k);
+    ptx::tma_prefetch_desc(&tm_v);
+    ptx::tma_prefetch_desc(&tm_o);
+  } else if (warp == 2) {
     ptx::tmem_alloc<kTmemCols>(&sm.tmem_base);
   }
   ptx::tc_fence_before();
@@ -129,177 +176,260 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = sm.tmem_base;
 
-  if (warp == 4) {
-    // ------------------------------------------------------------ producer
+  if (warp == 0) {
+    // ============================================================ producer
     if (ptx::elect_one()) {
       const uint64_t pol_q = ptx::policy_evict_first();
-      const uint64_t pol_kv = ptx::policy_evict_last();
-      ptx::mbar_arrive_expect_tx(&sm.bar_q, kTileBytes);
-      ptx::tma_load_4d(sm.q, &tm_q, &sm.bar_q, 0, j, gamma, (int32_t)(row0 + t0), pol_q);
-      for (int kt = 0; kt < n_kv && kt < kStages; ++kt) {
-        const int32_t kr = (int32_t)(row0 + kv_lo + (int64_t)kt * kBN);
-        ptx::mbar_arrive_expect_tx(&sm.bar_full[kt], 2 * kTileBytes);
-        ptx::tma_load_4d(sm.k[kt], &tm_k, &sm.bar_full[kt], 0, j, gamma, kr, pol_kv);
-        ptx::tma_load_4d(sm.v[kt], &tm_v, &sm.bar_full[kt], 0, j, gamma, kr, pol_kv);
-      }
-      constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);  // K-major A and B
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, kD, 0, 1);   // A (TMEM) K-major, V MN-major
-      const uint32_t q_addr = ptx::smem_u32(sm.q);
-      auto issue_qk = [&](int kt) {
-        const int s = kt % kStages;
-        ptx::mbar_wait(&sm.bar_full[s], (kt / kStages) & 1);
-        ptx::tc_fence_after();
-        const uint32_t k_addr = ptx::smem_u32(sm.k[s]);
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          ptx::mma_ss(tbase + kColS, ptx::sdesc_sw128(q_addr + kk * 32), ptx::sdesc_sw128(k_addr + kk * 32),
-                      idesc_qk, kk > 0);
+      const uint64_t pol_kv = ptx::policy_evict_first();
+      uint32_t i = 0, g = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
+        const Unit x = make_unit(p, u);
+        const uint32_t qs = i % kQStages;
+        ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&sm.q_full[qs], 2 * kTileBytes);
+        ptx::tma_load_5d(sm.q[qs][0], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0, x.b, pol_q);
+        ptx::tma_load_5d(sm.q[qs][1], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0 + kBM, x.b, pol_q);
+        for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
+          const uint32_t st = g % kKVStages;
+          ptx::mbar_wait(&sm.kv_empty[st], ((g / kKVStages) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
+          const int32_t kr = x.kv_lo + kt * kBN;
+          ptx::tma_load_5d(sm.k[st], &tm_k, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol_kv);
+          ptx::tma_load_5d(sm.v[st], &tm_v, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol_kv);
         }
-        ptx::tc_commit(&sm.bar_s);
+      }
+    }
+  } else if (warp == 1) {
+    // ========================================================== MMA issuer
+    if (ptx::elect_one()) {
+      constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);  // K-major Q and K
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, kD, 0, 1);   // P from TMEM, V MN-major
+      // Per-slot cursor over the (unit, key tile) steps the slot takes part in.
+      struct Cursor {
+        int32_t u, i, kt, g;  // unit id, local unit index, key tile, global key-tile index
+        Unit x;
+        bool valid;
       };
-      ptx::mbar_wait(&sm.bar_q, 0);
-      issue_qk(0);
-      for (int kt = 0; kt < n_kv; ++kt) {
-        const int s = kt % kStages;
-        ptx::mbar_wait(&sm.bar_p, kt & 1);  // softmax wrote P_kt (and rescaled O)
-        ptx::tc_fence_after();
-        const uint32_t v_addr = ptx::smem_u32(sm.v[s]);
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          ptx::mma_ts(tbase + kColO, tbase + kColS + kk * 8, ptx::sdesc_sw128(v_addr + kk * 2048), idesc_pv,
-                      (kt > 0 || kk > 0) ? 1u : 0u);
-        }
-        ptx::tc_commit(&sm.bar_empty[s]);
-        if (kt + 1 < n_kv) issue_qk(kt + 1);  // in-order after PV_kt: safe to overwrite P_kt
-        if (kt + kStages < n_kv) {
-          ptx::mbar_wait(&sm.bar_empty[s], (kt / kStages) & 1);
-          const int32_t kr = (int32_t)(row0 + kv_lo + (int64_t)(kt + kStages) * kBN);
-          ptx::mbar_arrive_expect_tx(&sm.bar_full[s], 2 * kTileBytes);
-          ptx::tma_load_4d(sm.k[s], &tm_k, &sm.bar_full[s], 0, j, gamma, kr, pol_kv);
-          ptx::tma_load_4d(sm.v[s], &tm_v, &sm.bar_full[s], 0, j, gamma, kr, pol_kv);
-        }
-      }
-      ptx::tc_commit(&sm.bar_o);
-    }
-  } else {
-    // ----------------------------------------------- softmax + epilogue
-    const uint32_t row = warp * 32 + lane;  // query row in tile == TMEM lane
-    const int64_t tq = t0 + row;            // stream-local t'
-    const bool valid_q = tq < p.T;
-    const int64_t hd = (int64_t)p.h * kD;
-    __nv_bfloat16* const ob = o + (b * p.N) * hd + (int64_t)j * kD;
+      int32_t qk_left[kQStages] = {0, 0};
+      int32_t qk_unit[kQStages] = {-1, -1};
+      uint32_t sc[2] = {0, 0};  // QK issued per slot
+      uint32_t pc[2] = {0, 0};  // p_full phases consumed per slot
+      uint32_t oc[2] = {0, 0};  // units completed per slot
 
-    // Zero rows of the other offset classes while the first tiles load.
-    if (valid_q) {
-      for (int32_t gz = 0; gz < p.r; ++gz) {
-        if (gz == gamma) continue;
-        uint8_t* dst = reinterpret_cast<uint8_t*>(ob + (tq * p.r + gz) * hd);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) ptx::st_global_v4(dst + 16 * c, 0u, 0u, 0u, 0u);
-        if (lse) lse[(b * p.h + j) * p.N + tq * p.r + gz] = -INFINITY;
-      }
-    }
-
-    // The query's own segment, as a key range in t'.
-    const int64_t seg_lo = valid_q ? (tq / p.m) * p.m : 0;
-    const int64_t seg_hi = valid_q ? min(seg_lo + p.m, p.T) : 0;
-    const uint32_t lane_base = (warp * 32) << 16;
-    float mref = -INFINITY;  // running reference max (raw score units)
-    float l = 0.0f;
-    for (int kt = 0; kt < n_kv; ++kt) {
-      ptx::mbar_wait(&sm.bar_s, kt & 1);
-      ptx::tc_fence_after();
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tbase + lane_base + kColS + 32 * c, sr[c]);
-      ptx::tmem_ld_wait();
-      const int64_t k0 = kv_lo + (int64_t)kt * kBN;
-      const int32_t lo = (int32_t)(seg_lo - k0 < 0 ? 0 : (seg_lo - k0 > kBN ? kBN : seg_lo - k0));
-      const int32_t hi = (int32_t)(seg_hi - k0 < 0 ? 0 : (seg_hi - k0 > kBN ? kBN : seg_hi - k0));
-      float tmax = -INFINITY;
-      if (lo == 0 && hi == kBN) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) tmax = fmaxf(tmax, __uint_as_float(sr[c][e]));
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int col = 32 * c + e;
-            const float s = (col >= lo && col < hi) ? __uint_as_float(sr[c][e]) : -INFINITY;
-            sr[c][e] = __float_as_uint(s);
-            tmax = fmaxf(tmax, s);
+      // advance cursor c of slot s to the next step with kt in the slot's range
+      auto advance = [&](Cursor& c, int s) {
+        while (c.valid) {
+          ++c.kt;
+          ++c.g;
+          if (c.kt >= c.x.n_kv) {
+            c.u += gridDim.x;
+            ++c.i;
+            if (c.u >= p.n_units) {
+              c.valid = false;
+              return;
+            }
+            c.x = make_unit(p, c.u);
+            c.kt = 0;
           }
-      }
-      // Lazy rescale: move the reference max only when the new max exceeds it
-      // by more than 2^8 in probability (FA4-style); otherwise p <= 256.
-      // (tcgen05.ld/st are warp-collective: the O round trip is warp-uniform,
-      // lanes that keep their reference max use corr = 1.)
-      const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
-      const bool fix_o = move && mref != -INFINITY;
-      if (__any_sync(0xffffffffu, fix_o)) {
-        const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
-        l *= corr;
-        uint32_t orow[2][32];
-        ptx::tmem_ld32(tbase + lane_base + kColO, orow[0]);
-        ptx::tmem_ld32(tbase + lane_base + kColO + 32, orow[1]);
-        ptx::tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) orow[c][e] = __float_as_uint(__uint_as_float(orow[c][e]) * corr);
-        ptx::tmem_st32(tbase + lane_base + kColO, orow[0]);
-        ptx::tmem_st32(tbase + lane_base + kColO + 32, orow[1]);
-      }
-      if (move) mref = tmax;
-      const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
-      float lsum = 0.0f;
-      uint32_t pk[2][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[c][e]), p.c, neg));
-          const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[c][e + 1]), p.c, neg));
-          lsum += p0 + p1;
-          pk[c >> 1][(c & 1) * 16 + e / 2] = ptx::pack_bf16x2(p0, p1);
+          if (c.kt >= c.x.kt0[s] && c.kt < c.x.kt1[s]) return;
         }
-      l += lsum;
-      ptx::tmem_st32(tbase + lane_base + kColS, pk[0]);
-      ptx::tmem_st32(tbase + lane_base + kColS + 32, pk[1]);
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&sm.bar_p);
-    }
+      };
+      auto first = [&](int s) {
+        Cursor c;
+        c.u = blockIdx.x;
+        c.i = 0;
+        c.kt = -1;
+        c.g = -1;
+        c.valid = c.u < p.n_units;
+        if (c.valid) {
+          c.x = make_unit(p, c.u);
+          advance(c, s);
+        }
+        return c;
+      };
+      auto issue_qk = [&](const Cursor& c, int s) {
+        const uint32_t qs = c.i % kQStages;
+        ptx::mbar_wait(&sm.q_full[qs], (c.i / kQStages) & 1);
+        const uint32_t st = c.g % kKVStages;
+        ptx::mbar_wait(&sm.kv_full[st], (c.g / kKVStages) & 1);
+        ptx::tc_fence_after();
+        const uint32_t qa = ptx::smem_u32(sm.q[qs][s]);
+        const uint32_t ka = ptx::smem_u32(sm.k[st]);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          ptx::mma_ss(tbase + col_s(s), ptx::sdesc_sw128(qa + kk * 32), ptx::sdesc_sw128(ka + kk * 32), idesc_qk,
+                      kk > 0);
+        ptx::tc_commit(&sm.s_full[s]);
+        ++sc[s];
+        if (qk_unit[qs] != c.i) {
+          qk_unit[qs] = c.i;
+          qk_left[qs] = (c.x.kt1[0] - c.x.kt0[0]) + (c.x.kt1[1] - c.x.kt0[1]);
+        }
+        if (--qk_left[qs] == 0) ptx::tc_commit(&sm.q_empty[qs]);  // Q tiles of this unit consumed
+      };
 
-    // ---------------------------------------------------------- epilogue
-    ptx::mbar_wait(&sm.bar_o, 0);
-    ptx::tc_fence_after();
-    uint32_t orow[2][32];
-    ptx::tmem_ld32(tbase + lane_base + kColO, orow[0]);
-    ptx::tmem_ld32(tbase + lane_base + kColO + 32, orow[1]);
-    ptx::tmem_ld_wait();
-    if (valid_q) {
-      const float inv = 1.0f / l;
-      uint8_t* dst = reinterpret_cast<uint8_t*>(ob + (tq * p.r + gamma) * hd);
+      Cursor cur[2] = {first(0), first(1)};
+      if (cur[0].valid) issue_qk(cur[0], 0);
+      if (cur[1].valid) issue_qk(cur[1], 1);
+      uint32_t g = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Unit x = make_unit(p, u);
+        for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
+          const uint32_t st = g % kKVStages;
+          const uint32_t va = ptx::smem_u32(sm.v[st]);
 #pragma unroll
-      for (int c = 0; c < 2; ++c)
+          for (int s = 0; s < 2; ++s) {
+            if (kt < x.kt0[s] || kt >= x.kt1[s]) continue;
+            ptx::mbar_wait(&sm.p_full[s], pc[s] & 1);
+            ++pc[s];
+            const bool first_kt = kt == x.kt0[s];
+            if (first_kt) ptx::mbar_wait(&sm.o_empty[s], (oc[s] & 1) ^ 1);
+            ptx::tc_fence_after();
 #pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          const float* f = reinterpret_cast<const float*>(&orow[c][e]);
-          ptx::st_global_v4(dst + (c * 32 + e) * 2, ptx::pack_bf16x2(f[0] * inv, f[1] * inv),
-                            ptx::pack_bf16x2(f[2] * inv, f[3] * inv), ptx::pack_bf16x2(f[4] * inv, f[5] * inv),
-                            ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
+            for (int kk = 0; kk < kBN / 16; ++kk)
+              ptx::mma_ts(tbase + col_o(s), tbase + col_s(s) + kk * 8, ptx::sdesc_sw128(va + kk * 2048), idesc_pv,
+                          (!first_kt || kk > 0) ? 1u : 0u);
+            if (kt == x.kt1[s] - 1) {
+              ptx::tc_commit(&sm.o_full[s]);
+              ++oc[s];
+            }
+            // Look ahead: the slot's next Q K^T (in-order after this P V, so it
+            // may overwrite P_s in TMEM).
+            advance(cur[s], s);
+            if (cur[s].valid) issue_qk(cur[s], s);
+          }
+          ptx::tc_commit(&sm.kv_empty[st]);
         }
-      if (lse) lse[(b * p.h + j) * p.N + tq * p.r + gamma] = mref * p.scale + logf(l);
+      }
     }
+  } else if (warp >= 4) {
+    // ============================================= softmax + epilogue slots
+    const int s = (warp - 4) / 4;                 // slot
+    const uint32_t row = (warp % 4) * 32 + lane;  // query row in tile == TMEM lane
+    const uint32_t lane_base = ((warp % 4) * 32) << 16;
+    const uint32_t tS = tbase + lane_base + col_s(s);
+    const uint32_t tO = tbase + lane_base + col_o(s);
+    const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
+    const bool leader = (warp % 4) == 0 && lane == 0;
+    uint32_t sc = 0, oc = 0;
+    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+      const Unit x = make_unit(p, u);
+      if (x.kt0[s] == x.kt1[s]) continue;  // no rows for this slot
+      const int32_t ts0 = x.t0 + s * kBM;
+      const int32_t tq = ts0 + (int32_t)row;
+      const bool valid_q = tq < p.T;
+      const int32_t seg_lo = valid_q ? (tq / p.m) * p.m : 0;
+      const int32_t seg_hi = valid_q ? min(seg_lo + p.m, p.T) : 0;
+      float mref = -INFINITY;
+      float l = 0.0f;
+      for (int32_t kt = x.kt0[s]; kt < x.kt1[s]; ++kt) {
+        ptx::mbar_wait(&sm.s_full[s], sc & 1);
+        ++sc;
+        ptx::tc_fence_after();
+        uint32_t sr[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + 32 * c, sr[c]);
+        ptx::tmem_ld_wait();
+        const int32_t k0 = x.kv_lo + kt * kBN;
+        const int32_t lo = min(max(seg_lo - k0, 0), kBN);
+        const int32_t hi = min(max(seg_hi - k0, 0), kBN);
+        float tmax = -INFINITY;
+        if (lo == 0 && hi == kBN) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) tmax = fmaxf(tmax, __uint_as_float(sr[c][e]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int col = 32 * c + e;
+              const float v = (col >= lo && col < hi) ? __uint_as_float(sr[c][e]) : -INFINITY;
+              sr[c][e] = __float_as_uint(v);
+              tmax = fmaxf(tmax, v);
+            }
+        }
+        // Lazy rescale (warp-uniform: tcgen05.ld/st are warp collectives).
+        const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
+        const bool fix_o = move && mref != -INFINITY;
+        if (__any_sync(0xffffffffu, fix_o)) {
+          const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
+          l *= corr;
+          uint32_t orow[2][32];
+          ptx::tmem_ld32(tO, orow[0]);
+          ptx::tmem_ld32(tO + 32, orow[1]);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) orow[c][e] = __float_as_uint(__uint_as_float(orow[c][e]) * corr);
+          ptx::tmem_st32(tO, orow[0]);
+          ptx::tmem_st32(tO + 32, orow[1]);
+        }
+        if (move) mref = tmax;
+        const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
+        float ls0 = 0.0f, ls1 = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[c][e]), p.c, neg));
+            const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[c][e + 1]), p.c, neg));
+            ls0 += p0;
+            ls1 += p1;
+            pk[e / 2] = ptx::pack_bf16x2(p0, p1);
+          }
+          ptx::tmem_st16(tS + 16 * c, pk);
+        }
+        l += ls0 + ls1;
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.p_full[s]);
+      }
+
+      // ------------------------------------------------------- epilogue
+      ptx::mbar_wait(&sm.o_full[s], oc & 1);
+      ++oc;
+      ptx::tc_fence_after();
+      uint32_t orow[2][32];
+      ptx::tmem_ld32(tO, orow[0]);
+      ptx::tmem_ld32(tO + 32, orow[1]);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&sm.o_empty[s]);  // O_s may be overwritten by the next unit
+      const float inv = valid_q ? 1.0f / l : 0.0f;
+      // the previous unit's TMA store must have finished reading the staging tile
+      if (leader) ptx::tma_store_wait_read<0>();
+      ptx::named_bar_sync(1 + s, kBM);
+      // 128B-swizzled staging row: 16B chunk c of row r at ((c ^ (r & 7)) * 16)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float* f = reinterpret_cast<const float*>(&orow[c >> 2][(c & 3) * 8]);
+        const uint32_t addr = stage_addr + row * 128 + ((c ^ (row & 7)) * 16);
+        ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0] * inv, f[1] * inv), ptx::pack_bf16x2(f[2] * inv, f[3] * inv),
+                          ptx::pack_bf16x2(f[4] * inv, f[5] * inv), ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1 + s, kBM);
+      if (leader) {
+        ptx::tma_store_5d(&tm_o, sm.ostage[s], 0, x.j, x.gamma, ts0, x.b);
+        for (int32_t gz = 0; gz < p.r; ++gz)
+          if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
+        ptx::tma_store_commit();
+      }
+      if (lse && valid_q) {
+        float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N + (int64_t)tq * p.r;
+        for (int32_t gz = 0; gz < p.r; ++gz) lb[gz] = (gz == x.gamma) ? mref * p.scale + logf(l) : -INFINITY;
+      }
+    }
+    if (leader) ptx::tma_store_wait_all<0>();
   }
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tbase);
   }
@@ -323,52 +453,68 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-// [B*N/r][r][h][64] bf16 view; box (64, 1, 1, 128), 128-byte swizzle.
-bool make_map(CUtensorMap* map, const void* base, int64_t rows_div_r, int64_t r, int64_t h) {
+// [B][N/r][r][h][64] bf16 view; box (64, 1, 1, 128, 1), 128-byte swizzle.
+// The t' extent is N/r per image, so boxes never cross into the next image:
+// out-of-range rows are zero-filled on load and dropped on store.
+bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)h, (cuuint64_t)r, (cuuint64_t)rows_div_r};
-  cuuint64_t strides[3] = {(cuuint64_t)kD * 2, (cuuint64_t)h * kD * 2, (cuuint64_t)r * h * kD * 2};
-  cuuint32_t box[4] = {kD, 1, 1, 128};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+  cuuint64_t dims[5] = {(cuuint64_t)kD, (cuuint64_t)h, (cuuint64_t)r, (cuuint64_t)(N / r), (cuuint64_t)B};
+  cuuint64_t strides[4] = {(cuuint64_t)kD * 2, (cuuint64_t)h * kD * 2, (cuuint64_t)r * h * kD * 2,
+                           (cuuint64_t)N * h * kD * 2};
+  cuuint32_t box[5] = {kD, 1, 1, 128, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS;
 }
 
+int num_sms() {
+  static int n = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  });
+  return n;
+}
+
 }  // namespace
 
 bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o) {
-  if (dtype != 1) return false;                   // bf16 only
-  if (g.d != kD || g.dv != kD) return false;       // head_dim 64
-  if (g.N % g.r != 0) return false;                // t'-stream view needs r | N
-  if (g.w % g.r != 0) return false;                // segments are contiguous t'-blocks
+  if (dtype != 1) return false;              // bf16 only
+  if (g.d != kD || g.dv != kD) return false;  // head_dim 64
+  if (g.N % g.r != 0) return false;           // t'-stream view needs r | N
+  if (g.w % g.r != 0) return false;           // segments are contiguous t'-blocks
   if (g.h > kMaxHeads) return false;
   auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
   if (!al(q) || !al(k) || !al(v) || !al(o)) return false;
-  const int64_t T = g.N / g.r;
-  if (g.B * T > (int64_t)INT32_MAX - 256) return false;  // TMA coordinates are int32
+  if (g.N > (int64_t)INT32_MAX / 2 || g.B > (int64_t)INT32_MAX) return false;  // TMA coordinates are int32
+  const int64_t units = g.B * g.h * ((g.N / g.r + kUnitRows - 1) / kUnitRows);
+  if (units > (int64_t)INT32_MAX) return false;
   return true;
 }
 
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why) {
-  const int64_t T = g.N / g.r;
-  CUtensorMap mq, mk, mv;
-  if (!make_map(&mq, q, g.B * T, g.r, g.h) || !make_map(&mk, k, g.B * T, g.r, g.h) ||
-      !make_map(&mv, v, g.B * T, g.r, g.h)) {
+  CUtensorMap mq, mk, mv, mo;
+  if (!make_map(&mq, q, g.B, g.N, g.r, g.h) || !make_map(&mk, k, g.B, g.N, g.r, g.h) ||
+      !make_map(&mv, v, g.B, g.N, g.r, g.h) || !make_map(&mo, o, g.B, g.N, g.r, g.h)) {
     *why = "cuTensorMapEncodeTiled failed";
     *err = cudaErrorInvalidValue;
     return 0;
   }
   Sm100Params p;
-  p.N = g.N;
-  p.T = T;
-  p.m = g.w / g.r;
+  p.N = (int32_t)g.N;
+  p.T = (int32_t)(g.N / g.r);
+  p.m = (int32_t)(g.w / g.r);
   p.r = (int32_t)g.r;
   p.h = (int32_t)g.h;
-  p.n_qt = (int32_t)((T + kBM - 1) / kBM);
+  p.n_pairs = (p.T + kUnitRows - 1) / kUnitRows;
+  p.n_units = (int32_t)(g.B * g.h * p.n_pairs);
   p.scale = g.scale;
   p.c = g.scale * kLog2e;
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
@@ -383,8 +529,8 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
     *why = "cudaFuncSetAttribute failed";
     return 0;
   }
-  const int64_t n_cta = g.B * g.h * p.n_qt;
-  dfa_sm100_kernel<<<(unsigned)n_cta, kThreads, smem, stream>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, p);
+  const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
+  dfa_sm100_kernel<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p);
   *err = cudaGetLastError();
   return 1;
 }

@@ -1,0 +1,130 @@
+// C++ drop-in check for include/dfa.hpp, written like the reference's own
+// tests (test_attention.cpp).  Host part runs anywhere (no kernel launch);
+// `gpu <dir>` also runs dfa::dilated_attention on host tensors and dumps
+// q, k, v, out (float32, raw) into <dir> for tests/test_cpp_api.py to check
+// against the oracle.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "dfa.hpp"
+
+// Minimal stand-in with attnkit::Tensor's rank-2 surface.
+struct Tensor {
+  std::vector<dfa::Index> shape;
+  std::vector<float> buf;
+  explicit Tensor(std::vector<dfa::Index> s) : shape(std::move(s)), buf(static_cast<size_t>(shape[0] * shape[1])) {}
+  dfa::Index rank() const { return static_cast<dfa::Index>(shape.size()); }
+  dfa::Index rows() const { return shape[0]; }
+  dfa::Index cols() const { return shape[1]; }
+  float* data() { return buf.data(); }
+  const float* data() const { return buf.data(); }
+};
+
+static int failures = 0;
+#define CHECK(cond)                                                   \
+  do {                                                                \
+    if (!(cond)) {                                                    \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);     \
+      ++failures;                                                     \
+    }                                                                 \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)        \
+  do {                                  \
+    bool ok = false;                    \
+    try {                               \
+      expr;                             \
+    } catch (const T&) {                \
+      ok = true;                        \
+    } catch (...) {                     \
+    }                                   \
+    CHECK(ok && #expr " throws " #T);   \
+  } while (0)
+
+static dfa::AttentionConfig basic_cfg(dfa::Index n, dfa::Index w, dfa::Index r, int h = 1, dfa::Index d = 4) {
+  dfa::AttentionConfig cfg;
+  cfg.seq_len = n;
+  cfg.segment_len = w;
+  cfg.interval = r;
+  cfg.num_heads = h;
+  cfg.head_dim = d;
+  cfg.head_offsets = dfa::AttentionConfig::spread_offsets(h, r);
+  return cfg;
+}
+
+static void host_checks() {
+  // test_attention.cpp:36-54
+  CHECK_THROWS_AS(basic_cfg(8, 9, 1).validate(), dfa::config_error);
+  CHECK_THROWS_AS(basic_cfg(8, 4, 5).validate(), dfa::config_error);
+  CHECK_THROWS_AS(basic_cfg(0, 4, 2).validate(), dfa::config_error);
+  auto cfg = basic_cfg(8, 4, 2);
+  cfg.head_offsets = {2};
+  CHECK_THROWS_AS(cfg.validate(), dfa::config_error);
+  cfg.head_offsets = {0, 0};
+  CHECK_THROWS_AS(cfg.validate(), dfa::config_error);
+  auto cov = basic_cfg(8, 4, 2, 2);
+  cov.head_offsets = {0, 0};
+  cov.validate(false);
+  CHECK_THROWS_AS(cov.validate(true), dfa::config_error);
+  // test_attention.cpp:148-210
+  CHECK((dfa::make_segment_view(8, 4, 2, 1, 0).row_indices == std::vector<dfa::Index>{4, 6}));
+  CHECK((dfa::make_segment_view(8, 4, 1, 0, 0).row_indices == std::vector<dfa::Index>{0, 1, 2, 3}));
+  CHECK((dfa::make_segment_view(10, 4, 2, 2, 1).row_indices == std::vector<dfa::Index>{9}));
+  CHECK_THROWS_AS(dfa::make_segment_view(8, 4, 2, 2, 0), std::out_of_range);
+  CHECK_THROWS_AS(dfa::make_segment_view(8, 4, 2, -1, 0), std::out_of_range);
+  CHECK_THROWS_AS(dfa::make_segment_view(8, 4, 2, 0, 2), std::out_of_range);
+  // test_attention.cpp:444-482
+  auto fc = dfa::flop_count(basic_cfg(4096, 512, 2, 1, 64));
+  CHECK(fc.dense_mults == 2ull * 4096 * 4096 * 64);
+  CHECK(fc.dilated_mults == 8ull * 2 * 256 * 256 * 64);
+  CHECK(fc.ratio == 32.0);
+  CHECK(dfa::flop_count(basic_cfg(4096, 2048, 2, 1, 64)).ratio == 8.0);
+  CHECK(dfa::flop_csv_header() == "N,w,r,h,d,dense_mults,dilated_mults,ratio");
+  CHECK(dfa::flop_csv_row(basic_cfg(4096, 512, 2, 1, 64), fc) == "4096,512,2,1,64,2147483648,67108864,32");
+}
+
+static void dump(const std::string& path, const Tensor& t) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  std::fwrite(t.data(), sizeof(float), t.buf.size(), f);
+  std::fclose(f);
+}
+
+static void gpu_checks(const std::string& dir) {
+  std::mt19937_64 rng(901);
+  std::normal_distribution<double> nd;
+  auto randn = [&](dfa::Index r, dfa::Index c) {
+    Tensor t({r, c});
+    for (auto& x : t.buf) x = static_cast<float>(nd(rng));
+    return t;
+  };
+  const auto cfg = basic_cfg(4096, 512, 2, 1, 64);
+  auto q = randn(4096, 64), k = randn(4096, 64), v = randn(4096, 64);
+  Tensor out = dfa::dilated_attention(q, k, v, cfg, 1);
+  dump(dir + "/q.f32", q);
+  dump(dir + "/k.f32", k);
+  dump(dir + "/v.f32", v);
+  dump(dir + "/o.f32", out);
+  // rows of the other offset class are exact zeros (attention.hpp:243-245)
+  for (dfa::Index i = 0; i < 4096; i += 2)
+    for (dfa::Index c = 0; c < 64; ++c) CHECK(out.buf[static_cast<size_t>(i * 64 + c)] == 0.0f);
+  // error paths keep the reference's exception types
+  CHECK_THROWS_AS(dfa::dilated_attention(q, k, v, cfg, 2), std::out_of_range);
+  Tensor bad({4095, 64});
+  CHECK_THROWS_AS(dfa::dilated_attention(bad, k, v, cfg, 0), dfa::dimension_error);
+  // fault hook demonstrably perturbs the output
+  {
+    dfa::fault::ScopedPerturb armed;
+    Tensor p = dfa::dilated_attention(q, k, v, cfg, 1);
+    CHECK(p.buf[0] != out.buf[0]);
+  }
+}
+
+int main(int argc, char** argv) {
+  host_checks();
+  if (argc > 2 && std::string(argv[1]) == "gpu") gpu_checks(argv[2]);
+  std::printf("%s (%d failures)\n", failures ? "FAIL" : "PASS", failures);
+  return failures ? 1 : 0;
+}
