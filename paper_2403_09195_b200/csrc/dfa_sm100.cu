@@ -62,8 +62,9 @@ constexpr int kQStages = 2;
 constexpr int kKVStages = 3;
 constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
-__host__ __device__ constexpr uint32_t col_s(int slot) { return 128u * slot; }        // S_A, S_B (P aliases)
-__host__ __device__ constexpr uint32_t col_o(int slot) { return 256u + 64u * slot; }  // O_A, O_B
+constexpr int kSBufs = 3;                                  // rotating S/P buffers
+__host__ __device__ constexpr uint32_t col_s(int buf) { return 128u * buf; }          // S_0..S_2 (P aliases)
+__host__ __device__ constexpr uint32_t col_o(int slot) { return 384u + 64u * slot; }  // O_A, O_B
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: p <= 2^8 between rescales
 
@@ -75,7 +76,10 @@ struct __align__(1024) SmemLayout {
   uint8_t zero[kTileBytes];
   uint64_t q_full[kQStages], q_empty[kQStages];
   uint64_t kv_full[kKVStages], kv_empty[kKVStages];
-  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t s_full[2][kSBufs];  // MMA -> slot s: S ready in buffer b
+  uint64_t p_full[kSBufs];     // slot -> MMA: P written in buffer b (128 arrivals)
+  uint64_t pv_done[2];         // MMA -> slot s: its latest P V completed
+  uint64_t o_full[2], o_empty[2];
   uint32_t tmem_base;
 };
 
@@ -93,10 +97,12 @@ struct Sm100Params {
 // Geometry of one work unit, identical in every role.
 struct Unit {
   int32_t b, j, gamma;
-  int32_t t0;         // first t' of slot A
-  int32_t kv_lo;      // first key t' (a segment start)
-  int32_t n_kv;       // key tiles in the unit
-  int32_t kt0[2], kt1[2];  // key-tile range [kt0, kt1) of each slot (empty if kt0 == kt1)
+  int32_t t0;              // first t' of slot A
+  int32_t kv_lo;           // first key t' (a segment start)
+  int32_t n_kv;            // key tiles in the unit
+  int32_t kt0a, kt1a, kt0b, kt1b;  // key-tile range [kt0, kt1) of slot A / B (empty if equal)
+  __device__ __forceinline__ int32_t kt0(int s) const { return s ? kt0b : kt0a; }
+  __device__ __forceinline__ int32_t kt1(int s) const { return s ? kt1b : kt1a; }
 };
 
 __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
@@ -108,6 +114,7 @@ __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
   x.gamma = p.offsets[x.j];
   x.t0 = pair * kUnitRows;
   int32_t lo[2], hi[2];
+#pragma unroll
   for (int s = 0; s < 2; ++s) {
     const int32_t r0 = x.t0 + s * kBM;
     const int32_t r1 = min(r0 + kBM, p.T);
@@ -121,16 +128,77 @@ __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
   x.kv_lo = lo[0];
   const int32_t kv_hi = hi[1] >= 0 ? max(hi[0], hi[1]) : hi[0];
   x.n_kv = (kv_hi - x.kv_lo + kBN - 1) / kBN;
-  for (int s = 0; s < 2; ++s) {
-    if (lo[s] < 0) {
-      x.kt0[s] = x.kt1[s] = 0;
-    } else {
-      x.kt0[s] = (lo[s] - x.kv_lo) / kBN;
-      x.kt1[s] = (hi[s] - x.kv_lo + kBN - 1) / kBN;
-    }
+  x.kt0a = (lo[0] - x.kv_lo) / kBN;
+  x.kt1a = (hi[0] - x.kv_lo + kBN - 1) / kBN;
+  if (lo[1] < 0) {
+    x.kt0b = x.kt1b = 0;
+  } else {
+    x.kt0b = (lo[1] - x.kv_lo) / kBN;
+    x.kt1b = (hi[1] - x.kv_lo + kBN - 1) / kBN;
   }
   return x;
 }
+
+// The CTA's step sequence, identical in every role: units u = blockIdx.x +
+// i*gridDim.x, key tiles kt of the unit, slots s (A then B) that use kt.
+// Step k uses S buffer k % 3.
+struct Step {
+  Unit x;
+  int32_t u, i, kt, g, k, s;  // unit, local unit index, key tile, CTA-global key tile, step, slot
+  bool valid;
+
+  __device__ __forceinline__ bool uses(int32_t slot, int32_t tile) const {
+    return tile >= x.kt0(slot) && tile < x.kt1(slot);
+  }
+  __device__ __forceinline__ bool first_of_slot() const { return kt == x.kt0(s); }
+  __device__ __forceinline__ bool last_of_slot() const { return kt == x.kt1(s) - 1; }
+  __device__ __forceinline__ bool last_use_of_tile() const { return s == 1 || !uses(1, kt); }
+
+  __device__ __forceinline__ void next(const Sm100Params& p) {
+    while (true) {
+      if (++s == 2) {
+        s = 0;
+        ++g;
+        if (++kt >= x.n_kv) {
+          u += gridDim.x;
+          ++i;
+          if (u >= p.n_units) {
+            valid = false;
+            return;
+          }
+          x = make_unit(p, u);
+          kt = 0;
+        }
+      }
+      if (uses(s, kt)) {
+        ++k;
+        return;
+      }
+    }
+  }
+  __device__ __forceinline__ void start(const Sm100Params& p) {
+    u = blockIdx.x;
+    i = 0;
+    kt = 0;
+    g = 0;
+    k = -1;
+    s = -1;
+    valid = u < p.n_units;
+    if (!valid) return;
+    x = make_unit(p, u);
+    while (true) {
+      if (++s == 2) {  // (only reached if slot A does not use tile 0: impossible)
+        s = 0;
+        ++g;
+        ++kt;
+      }
+      if (uses(s, kt)) {
+        ++k;
+        return;
+      }
+    }
+  }
+};
 
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -157,9 +225,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.kv_full[s], 1);
       ptx::mbar_init(&sm.kv_empty[s], 1);
     }
+    for (int b = 0; b < kSBufs; ++b) {
+      ptx::mbar_init(&sm.s_full[0][b], 1);
+      ptx::mbar_init(&sm.s_full[1][b], 1);
+      ptx::mbar_init(&sm.p_full[b], kBM);
+    }
     for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(&sm.s_full[s], 1);
-      ptx::mbar_init(&sm.p_full[s], kBM);
+      ptx::mbar_init(&sm.pv_done[s], 1);
       ptx::mbar_init(&sm.o_full[s], 1);
       ptx::mbar_init(&sm.o_empty[s], kBM);
     }
@@ -176,26 +248,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = sm.tmem_base;
 
+  // Registers: 384 x 168 at launch; the producer/MMA warpgroup gives most of
+  // its share to the two softmax warpgroups (128 x 64 + 256 x 216 <= 64512).
+  if (warp < 4) ptx::setmaxnreg_dec<64>();
   if (warp == 0) {
     // ============================================================ producer
     if (ptx::elect_one()) {
-      const uint64_t pol_q = ptx::policy_evict_first();
-      const uint64_t pol_kv = ptx::policy_evict_first();
+      const uint64_t pol = ptx::policy_evict_first();  // every byte is read once
       uint32_t i = 0, g = 0;
       for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
         const Unit x = make_unit(p, u);
         const uint32_t qs = i % kQStages;
         ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&sm.q_full[qs], 2 * kTileBytes);
-        ptx::tma_load_5d(sm.q[qs][0], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0, x.b, pol_q);
-        ptx::tma_load_5d(sm.q[qs][1], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0 + kBM, x.b, pol_q);
+        ptx::tma_load_5d(sm.q[qs][0], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0, x.b, pol);
+        ptx::tma_load_5d(sm.q[qs][1], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0 + kBM, x.b, pol);
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
           const uint32_t st = g % kKVStages;
           ptx::mbar_wait(&sm.kv_empty[st], ((g / kKVStages) & 1) ^ 1);
           ptx::mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
           const int32_t kr = x.kv_lo + kt * kBN;
-          ptx::tma_load_5d(sm.k[st], &tm_k, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol_kv);
-          ptx::tma_load_5d(sm.v[st], &tm_v, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol_kv);
+          ptx::tma_load_5d(sm.k[st], &tm_k, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol);
+          ptx::tma_load_5d(sm.v[st], &tm_v, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol);
         }
       }
     }
@@ -204,191 +278,178 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (ptx::elect_one()) {
       constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);  // K-major Q and K
       constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, kD, 0, 1);   // P from TMEM, V MN-major
-      // Per-slot cursor over the (unit, key tile) steps the slot takes part in.
-      struct Cursor {
-        int32_t u, i, kt, g;  // unit id, local unit index, key tile, global key-tile index
-        Unit x;
-        bool valid;
-      };
-      int32_t qk_left[kQStages] = {0, 0};
-      int32_t qk_unit[kQStages] = {-1, -1};
-      uint32_t sc[2] = {0, 0};  // QK issued per slot
-      uint32_t pc[2] = {0, 0};  // p_full phases consumed per slot
-      uint32_t oc[2] = {0, 0};  // units completed per slot
+      // Q-stage bookkeeping: unit index owning each stage and QKs left on it.
+      int32_t qk_left0 = 0, qk_left1 = 0, qk_unit0 = -1, qk_unit1 = -1;
+      uint32_t oc_par = 0;  // bit s: parity of slot s's completed-unit count
 
-      // advance cursor c of slot s to the next step with kt in the slot's range
-      auto advance = [&](Cursor& c, int s) {
-        while (c.valid) {
-          ++c.kt;
-          ++c.g;
-          if (c.kt >= c.x.n_kv) {
-            c.u += gridDim.x;
-            ++c.i;
-            if (c.u >= p.n_units) {
-              c.valid = false;
-              return;
-            }
-            c.x = make_unit(p, c.u);
-            c.kt = 0;
-          }
-          if (c.kt >= c.x.kt0[s] && c.kt < c.x.kt1[s]) return;
-        }
-      };
-      auto first = [&](int s) {
-        Cursor c;
-        c.u = blockIdx.x;
-        c.i = 0;
-        c.kt = -1;
-        c.g = -1;
-        c.valid = c.u < p.n_units;
-        if (c.valid) {
-          c.x = make_unit(p, c.u);
-          advance(c, s);
-        }
-        return c;
-      };
-      auto issue_qk = [&](const Cursor& c, int s) {
-        const uint32_t qs = c.i % kQStages;
-        ptx::mbar_wait(&sm.q_full[qs], (c.i / kQStages) & 1);
-        const uint32_t st = c.g % kKVStages;
-        ptx::mbar_wait(&sm.kv_full[st], (c.g / kKVStages) & 1);
+      auto issue_qk = [&](const Step& st) {
+        const uint32_t qs = st.i % kQStages;
+        ptx::mbar_wait(&sm.q_full[qs], (st.i / kQStages) & 1);
+        const uint32_t ks = st.g % kKVStages;
+        ptx::mbar_wait(&sm.kv_full[ks], (st.g / kKVStages) & 1);
         ptx::tc_fence_after();
-        const uint32_t qa = ptx::smem_u32(sm.q[qs][s]);
-        const uint32_t ka = ptx::smem_u32(sm.k[st]);
+        const uint32_t qa = ptx::smem_u32(sm.q[qs][st.s]);
+        const uint32_t ka = ptx::smem_u32(sm.k[ks]);
+        const uint32_t b = st.k % kSBufs;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
-          ptx::mma_ss(tbase + col_s(s), ptx::sdesc_sw128(qa + kk * 32), ptx::sdesc_sw128(ka + kk * 32), idesc_qk,
+          ptx::mma_ss(tbase + col_s(b), ptx::sdesc_sw128(qa + kk * 32), ptx::sdesc_sw128(ka + kk * 32), idesc_qk,
                       kk > 0);
-        ptx::tc_commit(&sm.s_full[s]);
-        ++sc[s];
-        if (qk_unit[qs] != c.i) {
-          qk_unit[qs] = c.i;
-          qk_left[qs] = (c.x.kt1[0] - c.x.kt0[0]) + (c.x.kt1[1] - c.x.kt0[1]);
+        ptx::tc_commit(&sm.s_full[st.s][b]);
+        int32_t& unit_ref = qs ? qk_unit1 : qk_unit0;
+        int32_t& left_ref = qs ? qk_left1 : qk_left0;
+        if (unit_ref != st.i) {
+          unit_ref = st.i;
+          left_ref = (st.x.kt1a - st.x.kt0a) + (st.x.kt1b - st.x.kt0b);
         }
-        if (--qk_left[qs] == 0) ptx::tc_commit(&sm.q_empty[qs]);  // Q tiles of this unit consumed
+        if (--left_ref == 0) ptx::tc_commit(&sm.q_empty[qs]);  // both Q tiles of the unit consumed
       };
 
-      Cursor cur[2] = {first(0), first(1)};
-      if (cur[0].valid) issue_qk(cur[0], 0);
-      if (cur[1].valid) issue_qk(cur[1], 1);
-      uint32_t g = 0;
-      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-        const Unit x = make_unit(p, u);
-        for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
-          const uint32_t st = g % kKVStages;
-          const uint32_t va = ptx::smem_u32(sm.v[st]);
+      Step pv, qk;
+      pv.start(p);
+      qk.start(p);
+      for (int n = 0; n < kSBufs && qk.valid; ++n) {
+        issue_qk(qk);
+        qk.next(p);
+      }
+      while (pv.valid) {
+        const uint32_t b = pv.k % kSBufs;
+        const int s = pv.s;
+        ptx::mbar_wait(&sm.p_full[b], (pv.k / kSBufs) & 1);
+        if (pv.first_of_slot()) ptx::mbar_wait(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u);
+        ptx::tc_fence_after();
+        const uint32_t va = ptx::smem_u32(sm.v[pv.g % kKVStages]);
+        const bool first = pv.first_of_slot();
 #pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            if (kt < x.kt0[s] || kt >= x.kt1[s]) continue;
-            ptx::mbar_wait(&sm.p_full[s], pc[s] & 1);
-            ++pc[s];
-            const bool first_kt = kt == x.kt0[s];
-            if (first_kt) ptx::mbar_wait(&sm.o_empty[s], (oc[s] & 1) ^ 1);
-            ptx::tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < kBN / 16; ++kk)
-              ptx::mma_ts(tbase + col_o(s), tbase + col_s(s) + kk * 8, ptx::sdesc_sw128(va + kk * 2048), idesc_pv,
-                          (!first_kt || kk > 0) ? 1u : 0u);
-            if (kt == x.kt1[s] - 1) {
-              ptx::tc_commit(&sm.o_full[s]);
-              ++oc[s];
-            }
-            // Look ahead: the slot's next Q K^T (in-order after this P V, so it
-            // may overwrite P_s in TMEM).
-            advance(cur[s], s);
-            if (cur[s].valid) issue_qk(cur[s], s);
-          }
-          ptx::tc_commit(&sm.kv_empty[st]);
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          ptx::mma_ts(tbase + col_o(s), tbase + col_s(b) + kk * 8, ptx::sdesc_sw128(va + kk * 2048), idesc_pv,
+                      (!first || kk > 0) ? 1u : 0u);
+        ptx::tc_commit(&sm.pv_done[s]);
+        if (pv.last_of_slot()) {
+          ptx::tc_commit(&sm.o_full[s]);
+          oc_par ^= 1u << s;
         }
+        if (pv.last_use_of_tile()) ptx::tc_commit(&sm.kv_empty[pv.g % kKVStages]);
+        // S buffer b is free once this P V has read it (in-order execution).
+        if (qk.valid) {
+          issue_qk(qk);
+          qk.next(p);
+        }
+        pv.next(p);
       }
     }
   } else if (warp >= 4) {
     // ============================================= softmax + epilogue slots
+    ptx::setmaxnreg_inc<216>();
     const int s = (warp - 4) / 4;                 // slot
     const uint32_t row = (warp % 4) * 32 + lane;  // query row in tile == TMEM lane
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
-    const uint32_t tS = tbase + lane_base + col_s(s);
     const uint32_t tO = tbase + lane_base + col_o(s);
     const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
     const bool leader = (warp % 4) == 0 && lane == 0;
-    uint32_t sc = 0, oc = 0;
-    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
-      const Unit x = make_unit(p, u);
-      if (x.kt0[s] == x.kt1[s]) continue;  // no rows for this slot
-      const int32_t ts0 = x.t0 + s * kBM;
-      const int32_t tq = ts0 + (int32_t)row;
-      const bool valid_q = tq < p.T;
-      const int32_t seg_lo = valid_q ? (tq / p.m) * p.m : 0;
-      const int32_t seg_hi = valid_q ? min(seg_lo + p.m, p.T) : 0;
-      float mref = -INFINITY;
-      float l = 0.0f;
-      for (int32_t kt = x.kt0[s]; kt < x.kt1[s]; ++kt) {
-        ptx::mbar_wait(&sm.s_full[s], sc & 1);
-        ++sc;
-        ptx::tc_fence_after();
-        uint32_t sr[4][32];
+    uint32_t use_par = 0;                  // bit b: parity of the next s_full[s][b] phase
+    uint32_t oc = 0;                       // units completed
+    uint32_t pvc = 0;                      // pv_done phases consumed
+    uint32_t steps = 0;                    // steps of this slot so far
+    float mref = -INFINITY, l = 0.0f;
+    int32_t tq = 0, seg_lo = 0, seg_hi = 0, ts0 = 0;
+    bool valid_q = false;
+    Step st;
+    st.start(p);
+    for (; st.valid; st.next(p)) {
+      if (st.s != s) continue;
+      const Unit& x = st.x;
+      if (st.first_of_slot()) {
+        ts0 = x.t0 + s * kBM;
+        tq = ts0 + (int32_t)row;
+        valid_q = tq < p.T;
+        seg_lo = valid_q ? (tq / p.m) * p.m : 0;
+        seg_hi = valid_q ? min(seg_lo + p.m, p.T) : 0;
+        mref = -INFINITY;
+        l = 0.0f;
+      }
+      const uint32_t b = st.k % kSBufs;
+      ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
+      use_par ^= 1u << b;
+      ptx::tc_fence_after();
+      const uint32_t tS = tbase + lane_base + col_s(b);
+      uint32_t sr[4][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + 32 * c, sr[c]);
-        ptx::tmem_ld_wait();
-        const int32_t k0 = x.kv_lo + kt * kBN;
-        const int32_t lo = min(max(seg_lo - k0, 0), kBN);
-        const int32_t hi = min(max(seg_hi - k0, 0), kBN);
-        float tmax = -INFINITY;
-        if (lo == 0 && hi == kBN) {
+      for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + 32 * c, sr[c]);
+      ptx::tmem_ld_wait();
+      const int32_t k0 = x.kv_lo + st.kt * kBN;
+      const int32_t lo = min(max(seg_lo - k0, 0), kBN);
+      const int32_t hi = min(max(seg_hi - k0, 0), kBN);
+      if (!(lo == 0 && hi == kBN)) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-            for (int e = 0; e < 32; ++e) tmax = fmaxf(tmax, __uint_as_float(sr[c][e]));
-        } else {
+          for (int e = 0; e < 32; ++e) {
+            const int col = 32 * c + e;
+            if (col < lo || col >= hi) sr[c][e] = __float_as_uint(-INFINITY);
+          }
+      }
+      float mx[8];
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
+      for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int col = 32 * c + e;
-              const float v = (col >= lo && col < hi) ? __uint_as_float(sr[c][e]) : -INFINITY;
-              sr[c][e] = __float_as_uint(v);
-              tmax = fmaxf(tmax, v);
-            }
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(sr[c][e]));
+      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      // Lazy rescale (warp-uniform: tcgen05.ld/st are warp collectives).  O_s
+      // must hold every earlier P V of this slot: wait for the slot's previous
+      // P V (pv_done phases are consumed exactly once per step, in order).
+      const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
+      const bool fix_o = move && mref != -INFINITY;
+      bool waited = false;
+      if (__any_sync(0xffffffffu, fix_o)) {
+        if (steps > 0) {
+          ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
+          ++pvc;
+          waited = true;
         }
-        // Lazy rescale (warp-uniform: tcgen05.ld/st are warp collectives).
-        const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
-        const bool fix_o = move && mref != -INFINITY;
-        if (__any_sync(0xffffffffu, fix_o)) {
-          const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
-          l *= corr;
-          uint32_t orow[2][32];
-          ptx::tmem_ld32(tO, orow[0]);
-          ptx::tmem_ld32(tO + 32, orow[1]);
+        ptx::tc_fence_after();
+        const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
+        l *= corr;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t orow[32];
+          ptx::tmem_ld32(tO + 32 * c, orow);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int e = 0; e < 32; ++e) orow[c][e] = __float_as_uint(__uint_as_float(orow[c][e]) * corr);
-          ptx::tmem_st32(tO, orow[0]);
-          ptx::tmem_st32(tO + 32, orow[1]);
+          for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * corr);
+          ptx::tmem_st32(tO + 32 * c, orow);
         }
-        if (move) mref = tmax;
-        const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
-        float ls0 = 0.0f, ls1 = 0.0f;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[c][e]), p.c, neg));
-            const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[c][e + 1]), p.c, neg));
-            ls0 += p0;
-            ls1 += p1;
-            pk[e / 2] = ptx::pack_bf16x2(p0, p1);
-          }
-          ptx::tmem_st16(tS + 16 * c, pk);
-        }
-        l += ls0 + ls1;
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&sm.p_full[s]);
       }
+      if (move) mref = tmax;
+      const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
+      float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[c][e]), p.c, neg));
+          const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[c][e + 1]), p.c, neg));
+          ls[(e >> 1) & 3] += p0 + p1;
+          pk[e / 2] = ptx::pack_bf16x2(p0, p1);
+        }
+        ptx::tmem_st16(tS + 16 * c, pk);
+      }
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      // keep the pv_done phases in lockstep with the steps
+      if (!waited && steps > 0) {
+        ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
+        ++pvc;
+      }
+      ++steps;
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&sm.p_full[b]);
 
+      if (!st.last_of_slot()) continue;
       // ------------------------------------------------------- epilogue
       ptx::mbar_wait(&sm.o_full[s], oc & 1);
       ++oc;
@@ -465,7 +526,7 @@ bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t 
   cuuint32_t box[5] = {kD, 1, 1, 128, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS;
 }
