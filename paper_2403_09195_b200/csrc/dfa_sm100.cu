@@ -60,7 +60,7 @@ constexpr int kUnitRows = 2 * kBM;     // t'-rows per work unit
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 bf16), SW128
 constexpr int kQStages = 2;
 constexpr int kKVStages = 3;
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSBufs = 3;                                  // rotating S/P buffers
 __host__ __device__ constexpr uint32_t col_s(int buf) { return 128u * buf; }          // S_0..S_2 (P aliases)
@@ -80,8 +80,31 @@ struct __align__(1024) SmemLayout {
   uint64_t p_full[kSBufs];     // slot -> MMA: P written in buffer b (128 arrivals)
   uint64_t pv_done[2];         // MMA -> slot s: its latest P V completed
   uint64_t o_full[2], o_empty[2];
+  uint64_t stat_full[2];       // slot -> epilogue: row stats of the finished unit written
+  float stat_l[2][2][kBM];     // [unit parity][slot][row] normaliser l
+  float stat_m[2][2][kBM];     // [unit parity][slot][row] reference max (raw score units), for lse
   uint32_t tmem_base;
 };
+
+// n / d for 0 <= n < 2^31 by multiply-high (magic numbers from the host).
+struct FastDiv {
+  uint32_t d, mul, shift;
+  __device__ __forceinline__ int32_t div(int32_t n) const {
+    return (int32_t)((__umulhi((uint32_t)n, mul) + (uint32_t)n) >> shift);
+  }
+  __device__ __forceinline__ int32_t mod(int32_t n) const { return n - div(n) * (int32_t)d; }
+};
+
+FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t shift = 0;
+  while ((1ull << shift) < d) ++shift;
+  f.shift = shift;
+  f.mul = (uint32_t)((((1ull << 32) * ((1ull << shift) - d)) / d) + 1);
+  if (d == 1) f.mul = 0;
+  return f;
+}
 
 struct Sm100Params {
   int32_t N, T;      // T = N / r (t'-stream length per (b, j))
@@ -91,6 +114,7 @@ struct Sm100Params {
   int32_t n_units;   // B * h * n_pairs
   float c;           // scale * log2(e)
   float scale;
+  FastDiv div_pairs, div_h, div_m;
   int32_t offsets[kMaxHeads];
 };
 
@@ -107,10 +131,10 @@ struct Unit {
 
 __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
   Unit x;
-  const int32_t pair = u % p.n_pairs;
-  const int32_t bj = u / p.n_pairs;
-  x.j = bj % p.h;
-  x.b = bj / p.h;
+  const int32_t bj = p.div_pairs.div(u);
+  const int32_t pair = u - bj * p.n_pairs;
+  x.b = p.div_h.div(bj);
+  x.j = bj - x.b * p.h;
   x.gamma = p.offsets[x.j];
   x.t0 = pair * kUnitRows;
   int32_t lo[2], hi[2];
@@ -119,8 +143,8 @@ __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
     const int32_t r0 = x.t0 + s * kBM;
     const int32_t r1 = min(r0 + kBM, p.T);
     if (r0 < r1) {
-      lo[s] = (r0 / p.m) * p.m;
-      hi[s] = min(((r1 - 1) / p.m + 1) * p.m, p.T);
+      lo[s] = p.div_m.div(r0) * p.m;
+      hi[s] = min((p.div_m.div(r1 - 1) + 1) * p.m, p.T);
     } else {
       lo[s] = hi[s] = -1;
     }
@@ -234,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.pv_done[s], 1);
       ptx::mbar_init(&sm.o_full[s], 1);
       ptx::mbar_init(&sm.o_empty[s], kBM);
+      ptx::mbar_init(&sm.stat_full[s], kBM);
     }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tm_q);
@@ -248,9 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = sm.tmem_base;
 
-  // Registers: 384 x 168 at launch; the producer/MMA warpgroup gives most of
-  // its share to the two softmax warpgroups (128 x 64 + 256 x 216 <= 64512).
-  if (warp < 4) ptx::setmaxnreg_dec<64>();
+  // Registers: 512 x 128 at launch; rebalanced per warpgroup to
+  // producer/MMA 56, softmax 2 x 184, epilogue 88 (sum = 65536).
+  if (warp < 4) ptx::setmaxnreg_dec<56>();
   if (warp == 0) {
     // ============================================================ producer
     if (ptx::elect_one()) {
@@ -338,32 +363,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         pv.next(p);
       }
     }
-  } else if (warp >= 4) {
-    // ============================================= softmax + epilogue slots
-    ptx::setmaxnreg_inc<216>();
+  } else if (warp >= 4 && warp < 12) {
+    // ====================================================== softmax slots
+    ptx::setmaxnreg_inc<184>();
     const int s = (warp - 4) / 4;                 // slot
     const uint32_t row = (warp % 4) * 32 + lane;  // query row in tile == TMEM lane
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const uint32_t tO = tbase + lane_base + col_o(s);
-    const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
-    const bool leader = (warp % 4) == 0 && lane == 0;
-    uint32_t use_par = 0;                  // bit b: parity of the next s_full[s][b] phase
-    uint32_t oc = 0;                       // units completed
-    uint32_t pvc = 0;                      // pv_done phases consumed
-    uint32_t steps = 0;                    // steps of this slot so far
+    uint32_t use_par = 0;  // bit b: parity of the next s_full[s][b] phase
+    uint32_t pvc = 0;      // pv_done phases consumed
+    uint32_t steps = 0;    // steps of this slot so far
     float mref = -INFINITY, l = 0.0f;
-    int32_t tq = 0, seg_lo = 0, seg_hi = 0, ts0 = 0;
-    bool valid_q = false;
+    int32_t seg_lo = 0, seg_hi = 0;
     Step st;
     st.start(p);
     for (; st.valid; st.next(p)) {
       if (st.s != s) continue;
       const Unit& x = st.x;
       if (st.first_of_slot()) {
-        ts0 = x.t0 + s * kBM;
-        tq = ts0 + (int32_t)row;
-        valid_q = tq < p.T;
-        seg_lo = valid_q ? (tq / p.m) * p.m : 0;
+        const int32_t tq = x.t0 + s * kBM + (int32_t)row;
+        const bool valid_q = tq < p.T;
+        seg_lo = valid_q ? p.div_m.div(tq) * p.m : 0;
         seg_hi = valid_q ? min(seg_lo + p.m, p.T) : 0;
         mref = -INFINITY;
         l = 0.0f;
@@ -448,41 +468,71 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&sm.p_full[b]);
-
-      if (!st.last_of_slot()) continue;
-      // ------------------------------------------------------- epilogue
-      ptx::mbar_wait(&sm.o_full[s], oc & 1);
-      ++oc;
-      ptx::tc_fence_after();
-      uint32_t orow[2][32];
-      ptx::tmem_ld32(tO, orow[0]);
-      ptx::tmem_ld32(tO + 32, orow[1]);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&sm.o_empty[s]);  // O_s may be overwritten by the next unit
-      const float inv = valid_q ? 1.0f / l : 0.0f;
-      // the previous unit's TMA store must have finished reading the staging tile
-      if (leader) ptx::tma_store_wait_read<0>();
-      ptx::named_bar_sync(1 + s, kBM);
-      // 128B-swizzled staging row: 16B chunk c of row r at ((c ^ (r & 7)) * 16)
+      if (st.last_of_slot()) {
+        // Hand the row statistics to the epilogue warpgroup (double-buffered
+        // by unit parity; the pv_done wait above orders this write after the
+        // epilogue's read of the same buffer two units ago).
+        sm.stat_l[st.i & 1][s][row] = l;
+        sm.stat_m[st.i & 1][s][row] = mref;
+        ptx::mbar_arrive(&sm.stat_full[s]);
+      }
+    }
+  } else if (warp >= 12) {
+    // ============================================================ epilogue
+    ptx::setmaxnreg_dec<88>();
+    const uint32_t row = (warp % 4) * 32 + lane;
+    const uint32_t lane_base = ((warp % 4) * 32) << 16;
+    const bool leader = warp == 12 && lane == 0;
+    uint32_t par = 0;  // bit s: parity of slot s's completed-unit count
+    int32_t i = 0;
+    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
+      const Unit x = make_unit(p, u);
+#pragma unroll 1
+      for (int s = 0; s < 2; ++s) {
+        if (x.kt0(s) == x.kt1(s)) continue;  // slot has no rows in this unit
+        const int32_t ts0 = x.t0 + s * kBM;
+        const int32_t tq = ts0 + (int32_t)row;
+        const bool valid_q = tq < p.T;
+        const uint32_t ph = (par >> s) & 1u;
+        par ^= 1u << s;
+        ptx::mbar_wait(&sm.o_full[s], ph);
+        ptx::mbar_wait(&sm.stat_full[s], ph);
+        ptx::tc_fence_after();
+        const float l = sm.stat_l[i & 1][s][row];
+        const float mref = sm.stat_m[i & 1][s][row];
+        const uint32_t tO = tbase + lane_base + col_o(s);
+        uint32_t orow[2][32];
+        ptx::tmem_ld32(tO, orow[0]);
+        ptx::tmem_ld32(tO + 32, orow[1]);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.o_empty[s]);  // O_s (and this stats buffer) may be reused
+        const float inv = valid_q ? 1.0f / l : 0.0f;
+        // the previous TMA store from this staging tile must have finished reading it
+        if (leader) ptx::tma_store_wait_read<0>();
+        ptx::named_bar_sync(1, kBM);
+        const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
+        // 128B-swizzled staging row: 16B chunk c of row r at ((c ^ (r & 7)) * 16)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const float* f = reinterpret_cast<const float*>(&orow[c >> 2][(c & 3) * 8]);
-        const uint32_t addr = stage_addr + row * 128 + ((c ^ (row & 7)) * 16);
-        ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0] * inv, f[1] * inv), ptx::pack_bf16x2(f[2] * inv, f[3] * inv),
-                          ptx::pack_bf16x2(f[4] * inv, f[5] * inv), ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
-      }
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1 + s, kBM);
-      if (leader) {
-        ptx::tma_store_5d(&tm_o, sm.ostage[s], 0, x.j, x.gamma, ts0, x.b);
-        for (int32_t gz = 0; gz < p.r; ++gz)
-          if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
-        ptx::tma_store_commit();
-      }
-      if (lse && valid_q) {
-        float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N + (int64_t)tq * p.r;
-        for (int32_t gz = 0; gz < p.r; ++gz) lb[gz] = (gz == x.gamma) ? mref * p.scale + logf(l) : -INFINITY;
+        for (int c = 0; c < 8; ++c) {
+          const float* f = reinterpret_cast<const float*>(&orow[c >> 2][(c & 3) * 8]);
+          const uint32_t addr = stage_addr + row * 128 + ((c ^ (row & 7)) * 16);
+          ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0] * inv, f[1] * inv),
+                            ptx::pack_bf16x2(f[2] * inv, f[3] * inv), ptx::pack_bf16x2(f[4] * inv, f[5] * inv),
+                            ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, kBM);
+        if (leader) {
+          ptx::tma_store_5d(&tm_o, sm.ostage[s], 0, x.j, x.gamma, ts0, x.b);
+          for (int32_t gz = 0; gz < p.r; ++gz)
+            if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
+          ptx::tma_store_commit();
+        }
+        if (lse && valid_q) {
+          float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N + (int64_t)tq * p.r;
+          for (int32_t gz = 0; gz < p.r; ++gz) lb[gz] = (gz == x.gamma) ? mref * p.scale + logf(l) : -INFINITY;
+        }
       }
     }
     if (leader) ptx::tma_store_wait_all<0>();
@@ -578,6 +628,9 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.n_units = (int32_t)(g.B * g.h * p.n_pairs);
   p.scale = g.scale;
   p.c = g.scale * kLog2e;
+  p.div_pairs = make_fastdiv((uint32_t)p.n_pairs);
+  p.div_h = make_fastdiv((uint32_t)p.h);
+  p.div_m = make_fastdiv((uint32_t)p.m);
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
   const size_t smem = sizeof(SmemLayout) + 1024;
   static std::once_flag once;
