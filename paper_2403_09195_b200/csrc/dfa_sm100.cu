@@ -67,6 +67,7 @@ __host__ __device__ constexpr uint32_t col_s(int buf) { return 128u * buf; }    
 __host__ __device__ constexpr uint32_t col_o(int slot) { return 384u + 64u * slot; }  // O_A, O_B
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: p <= 2^8 between rescales
+constexpr int kPolyFrom = 6;               // elements e % 8 >= 6 use the FMA-pipe exp2
 
 struct __align__(1024) SmemLayout {
   uint8_t q[kQStages][2][kTileBytes];
@@ -448,13 +449,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
+        // three independent phases per 32-column chunk: scale, exponentiate
+        // (3 of 4 on MUFU, 1 of 4 as an FMA-pipe polynomial), sum + pack
+        float xv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) xv[e] = fmaf(__uint_as_float(sr[c][e]), p.c, neg);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) xv[e] = (e % 8 >= kPolyFrom) ? ptx::ex2_poly(xv[e]) : ptx::ex2(xv[e]);
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float p0 = ptx::ex2(fmaf(__uint_as_float(sr[c][e]), p.c, neg));
-          const float p1 = ptx::ex2(fmaf(__uint_as_float(sr[c][e + 1]), p.c, neg));
-          ls[(e >> 1) & 3] += p0 + p1;
-          pk[e / 2] = ptx::pack_bf16x2(p0, p1);
+          ls[(e >> 1) & 3] += xv[e] + xv[e + 1];
+          pk[e / 2] = ptx::pack_bf16x2(xv[e], xv[e + 1]);
         }
         ptx::tmem_st16(tS + 16 * c, pk);
       }

@@ -43,13 +43,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Blocking wait on phase `parity`.  The suspend-time hint lets the waiting
+// warp sleep in hardware until the phase flips instead of re-polling (each
+// poll costs an issue slot on the SMSP shared with the softmax warps).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 
@@ -234,6 +237,22 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = j + f,
+// f in [-1/2, 1/2], degree-3 polynomial for 2^f fitted for relative error
+// with p(0) = 1 exactly (max rel. err 1.2e-4, well under bf16 P's 2^-9),
+// exponent added as integer bits.  x is clamped at -125 so 2^x stays normal
+// (masked -inf scores give 2^-125 ~ 0).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.0f);
+  const float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
+  const float t = x + kMagic;
+  const float f = x - (t - kMagic);
+  float p = fmaf(5.459282631e-2f, f, 2.422181094e-1f);
+  p = fmaf(p, f, 6.933686450e-1f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 __device__ __forceinline__ float ex2(float x) {
