@@ -134,6 +134,13 @@ dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int
  * not cover fail with DFA_ERR_UNSUPPORTED).  Process-wide. */
 void dfa_set_path_override(int32_t path);
 
+/* Profiling hook: dfa_forward (bf16, tcgen05 path only) of a build of the
+ * kernel that records a timeline of CTA 0 into `trace` (5 x 4096 uint64:
+ * per role producer / MMA / softmax A / softmax B / epilogue, entries
+ * (event << 56) | clock64).  scripts/trace_timeline.py decodes it. */
+dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
+                                void* o, uint64_t* trace, void* stream);
+
 /* Number of device kernels the last dfa_forward on this thread launched
  * (evidence for bench.py's gpu_launches). */
 int32_t dfa_last_launch_count(void);

@@ -41,6 +41,7 @@ EXPORTED = (
     "dfa_get_fault_perturb",
     "dfa_workspace_bytes",
     "dfa_set_path_override",
+    "dfa_forward_traced",
     "dfa_last_launch_count",
     "dfa_version",
 )
@@ -91,6 +92,7 @@ def _load() -> ctypes.CDLL:
         "dfa_get_fault_perturb": (c_i32, []),
         "dfa_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_i32, ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_set_path_override": (None, [c_i32]),
+        "dfa_forward_traced": (c_i32, [p_cfg, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
         "dfa_last_launch_count": (c_i32, []),
         "dfa_version": (c_i32, []),
     }

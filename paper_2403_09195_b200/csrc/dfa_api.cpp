@@ -169,8 +169,22 @@ dfa_status_t dfa_query_path(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t 
   return DFA_OK;
 }
 
+static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                                 const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace);
+
 dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
                          const void* v, void* o, float* lse, void* stream) {
+  return forward_impl(cfg, dtype, batch, q, k, v, o, lse, stream, nullptr);
+}
+
+dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
+                                void* o, uint64_t* trace, void* stream) {
+  if (!trace) return fail(DFA_ERR_DIMENSION, "dfa_forward_traced: null trace buffer");
+  return forward_impl(cfg, DFA_BF16, batch, q, k, v, o, nullptr, stream, trace);
+}
+
+static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                                 const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace) {
   g_launches = 0;
   dfa_impl::Geometry g;
   dfa_status_t st = resolve(cfg, batch, &g);
@@ -184,9 +198,11 @@ dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t bat
   int launches = 0;
   if (path == DFA_PATH_SM100_TCGEN05) {
     const char* why = "";
-    launches = dfa_impl::launch_sm100(g, q, k, v, o, lse, s, &err, &why);
+    launches = dfa_impl::launch_sm100(g, q, k, v, o, lse, s, &err, &why, trace);
     if (launches == 0 && err != cudaSuccess)
       return fail(DFA_ERR_CUDA, "dfa_forward: sm100 path: %s (%s)", why, cudaGetErrorString(err));
+  } else if (trace) {
+    return fail(DFA_ERR_UNSUPPORTED, "dfa_forward_traced: only the tcgen05 path is instrumented");
   } else if (path == DFA_PATH_SIMT) {
     launches = dfa_impl::launch_simt(g, dtype, q, k, v, o, lse, s, &err);
   } else {

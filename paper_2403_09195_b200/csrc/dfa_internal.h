@@ -27,8 +27,9 @@ int launch_simt(const Geometry& g, int dtype, const void* q, const void* k, cons
 bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o);
 
 // tcgen05/TMEM/TMA kernel (bf16 in/out, fp32 accumulate).  Returns launches.
+// trace: optional profiling buffer (5 x 4096 uint64 timeline events of CTA 0).
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
-                 cudaStream_t stream, cudaError_t* err, const char** why);
+                 cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr);
 
 // Fault hook (attention.hpp:272): out[0] += 1e-3.
 int launch_perturb(int dtype, void* o, cudaStream_t stream);

@@ -225,10 +225,28 @@ struct Step {
   }
 };
 
+// Optional timeline trace (profiling builds of the same kernel, kTrace=true):
+// CTA 0 records (event << 56 | clock64) per role into trace[seg * kTraceCap].
+constexpr int kTraceCap = 4096;
+enum TraceEvent : uint64_t {
+  TR_Q_ISSUE = 1, TR_KV_WAIT, TR_KV_ISSUE,                          // producer  (seg 0)
+  TR_P_WAIT, TR_P_READY, TR_PV_ISSUED, TR_QK_WAIT, TR_QK_ISSUED,    // MMA       (seg 1)
+  TR_S_WAIT, TR_S_READY, TR_MAX_DONE, TR_EXP_DONE, TR_P_ARRIVE,     // softmax   (seg 2 = A, 3 = B)
+  TR_O_WAIT, TR_O_READY, TR_STORE_ISSUED                            // epilogue  (seg 4)
+};
+#define DFA_TRACE(seg, ev)                                                                        \
+  do {                                                                                            \
+    if constexpr (kTrace) {                                                                       \
+      if (tr_on && tr_n < kTraceCap) trace[(seg) * kTraceCap + tr_n++] = ((uint64_t)(ev) << 56) | \
+                                                                          (clock64() & 0xFFFFFFFFFFFFFFull); \
+    }                                                                                             \
+  } while (0)
+
+template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-                     float* __restrict__ lse, const __grid_constant__ Sm100Params p) {
+                     float* __restrict__ lse, const __grid_constant__ Sm100Params p, uint64_t* __restrict__ trace) {
   extern __shared__ uint8_t smem_raw[];
   SmemLayout& sm =
       *reinterpret_cast<SmemLayout*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -280,18 +298,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ============================================================ producer
     if (ptx::elect_one()) {
+      const bool tr_on = blockIdx.x == 0;
+      uint32_t tr_n = 0;
       const uint64_t pol = ptx::policy_evict_first();  // every byte is read once
       uint32_t i = 0, g = 0;
       for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
         const Unit x = make_unit(p, u);
         const uint32_t qs = i % kQStages;
         ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
+        DFA_TRACE(0, TR_Q_ISSUE);
         ptx::mbar_arrive_expect_tx(&sm.q_full[qs], 2 * kTileBytes);
         ptx::tma_load_5d(sm.q[qs][0], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0, x.b, pol);
         ptx::tma_load_5d(sm.q[qs][1], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0 + kBM, x.b, pol);
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
           const uint32_t st = g % kKVStages;
+          DFA_TRACE(0, TR_KV_WAIT);
           ptx::mbar_wait(&sm.kv_empty[st], ((g / kKVStages) & 1) ^ 1);
+          DFA_TRACE(0, TR_KV_ISSUE);
           ptx::mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
           const int32_t kr = x.kv_lo + kt * kBN;
           ptx::tma_load_5d(sm.k[st], &tm_k, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol);
@@ -302,6 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ========================================================== MMA issuer
     if (ptx::elect_one()) {
+      const bool tr_on = blockIdx.x == 0;
+      uint32_t tr_n = 0;
       constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);  // K-major Q and K
       constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, kD, 0, 1);   // P from TMEM, V MN-major
       // Q-stage bookkeeping: unit index owning each stage and QKs left on it.
@@ -310,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       auto issue_qk = [&](const Step& st) {
         const uint32_t qs = st.i % kQStages;
+        DFA_TRACE(1, TR_QK_WAIT);
         ptx::mbar_wait(&sm.q_full[qs], (st.i / kQStages) & 1);
         const uint32_t ks = st.g % kKVStages;
         ptx::mbar_wait(&sm.kv_full[ks], (st.g / kKVStages) & 1);
@@ -322,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mma_ss(tbase + col_s(b), ptx::sdesc_sw128(qa + kk * 32), ptx::sdesc_sw128(ka + kk * 32), idesc_qk,
                       kk > 0);
         ptx::tc_commit(&sm.s_full[st.s][b]);
+        DFA_TRACE(1, TR_QK_ISSUED);
         int32_t& unit_ref = qs ? qk_unit1 : qk_unit0;
         int32_t& left_ref = qs ? qk_left1 : qk_left0;
         if (unit_ref != st.i) {
@@ -341,7 +368,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (pv.valid) {
         const uint32_t b = pv.k % kSBufs;
         const int s = pv.s;
+        DFA_TRACE(1, TR_P_WAIT);
         ptx::mbar_wait(&sm.p_full[b], (pv.k / kSBufs) & 1);
+        DFA_TRACE(1, TR_P_READY);
         if (pv.first_of_slot()) ptx::mbar_wait(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u);
         ptx::tc_fence_after();
         const uint32_t va = ptx::smem_u32(sm.v[pv.g % kKVStages]);
@@ -351,6 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mma_ts(tbase + col_o(s), tbase + col_s(b) + kk * 8, ptx::sdesc_sw128(va + kk * 2048), idesc_pv,
                       (!first || kk > 0) ? 1u : 0u);
         ptx::tc_commit(&sm.pv_done[s]);
+        DFA_TRACE(1, TR_PV_ISSUED);
         if (pv.last_of_slot()) {
           ptx::tc_commit(&sm.o_full[s]);
           oc_par ^= 1u << s;
@@ -371,6 +401,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = (warp % 4) * 32 + lane;  // query row in tile == TMEM lane
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const uint32_t tO = tbase + lane_base + col_o(s);
+    const bool tr_on = blockIdx.x == 0 && row == 0;
+    uint32_t tr_n = 0;
     uint32_t use_par = 0;  // bit b: parity of the next s_full[s][b] phase
     uint32_t pvc = 0;      // pv_done phases consumed
     uint32_t steps = 0;    // steps of this slot so far
@@ -390,7 +422,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         l = 0.0f;
       }
       const uint32_t b = st.k % kSBufs;
+      DFA_TRACE(2 + s, TR_S_WAIT);
       ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
+      DFA_TRACE(2 + s, TR_S_READY);
       use_par ^= 1u << b;
       ptx::tc_fence_after();
       const uint32_t tS = tbase + lane_base + col_s(b);
@@ -419,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < 32; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(sr[c][e]));
       const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      DFA_TRACE(2 + s, TR_MAX_DONE);
       // Lazy rescale (warp-uniform: tcgen05.ld/st are warp collectives).  O_s
       // must hold every earlier P V of this slot: wait for the slot's previous
       // P V (pv_done phases are consumed exactly once per step, in order).
@@ -465,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_st16(tS + 16 * c, pk);
       }
       l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      DFA_TRACE(2 + s, TR_EXP_DONE);
       // keep the pv_done phases in lockstep with the steps
       if (!waited && steps > 0) {
         ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
@@ -474,6 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&sm.p_full[b]);
+      DFA_TRACE(2 + s, TR_P_ARRIVE);
       if (st.last_of_slot()) {
         // Hand the row statistics to the epilogue warpgroup (double-buffered
         // by unit parity; the pv_done wait above orders this write after the
@@ -489,6 +526,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t row = (warp % 4) * 32 + lane;
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const bool leader = warp == 12 && lane == 0;
+    const bool tr_on = blockIdx.x == 0 && leader;
+    uint32_t tr_n = 0;
     uint32_t par = 0;  // bit s: parity of slot s's completed-unit count
     int32_t i = 0;
     for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
@@ -501,7 +540,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool valid_q = tq < p.T;
         const uint32_t ph = (par >> s) & 1u;
         par ^= 1u << s;
+        DFA_TRACE(4, TR_O_WAIT);
         ptx::mbar_wait(&sm.o_full[s], ph);
+        DFA_TRACE(4, TR_O_READY);
         ptx::mbar_wait(&sm.stat_full[s], ph);
         ptx::tc_fence_after();
         const float l = sm.stat_l[i & 1][s][row];
@@ -535,6 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
           ptx::tma_store_commit();
         }
+        DFA_TRACE(4, TR_STORE_ISSUED);
         if (lse && valid_q) {
           float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N + (int64_t)tq * p.r;
           for (int32_t gz = 0; gz < p.r; ++gz) lb[gz] = (gz == x.gamma) ? mref * p.scale + logf(l) : -INFINITY;
@@ -616,7 +658,7 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 }
 
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
-                 cudaStream_t stream, cudaError_t* err, const char** why) {
+                 cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace) {
   CUtensorMap mq, mk, mv, mo;
   if (!make_map(&mq, q, g.B, g.N, g.r, g.h) || !make_map(&mk, k, g.B, g.N, g.r, g.h) ||
       !make_map(&mv, v, g.B, g.N, g.r, g.h) || !make_map(&mo, o, g.B, g.N, g.r, g.h)) {
@@ -642,7 +684,9 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(dfa_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_err = cudaFuncSetAttribute(dfa_sm100_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(dfa_sm100_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   if (attr_err != cudaSuccess) {
     *err = attr_err;
@@ -650,7 +694,10 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
     return 0;
   }
   const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
-  dfa_sm100_kernel<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p);
+  if (trace)
+    dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, trace);
+  else
+    dfa_sm100_kernel<false><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, nullptr);
   *err = cudaGetLastError();
   return 1;
 }

@@ -1,0 +1,111 @@
+#!/usr/bin/env python3
+"""Record and decode the CTA-0 timeline of the tcgen05 kernel (dfa_forward_traced).
+
+On the GPU box:  python scripts/trace_timeline.py run  [--w 512 --r 2 --batch 64]
+Here:            python scripts/trace_timeline.py show gpurun_out/trace.npy
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+CAP = 4096
+NAMES = {1: "Q_ISSUE", 2: "KV_WAIT", 3: "KV_ISSUE", 4: "P_WAIT", 5: "P_READY", 6: "PV_ISSUED", 7: "QK_WAIT",
+         8: "QK_ISSUED", 9: "S_WAIT", 10: "S_READY", 11: "MAX_DONE", 12: "EXP_DONE", 13: "P_ARRIVE", 14: "O_WAIT",
+         15: "O_READY", 16: "STORE_ISSUED"}
+ROLES = ["producer", "mma", "softmax_A", "softmax_B", "epilogue"]
+
+
+def run(args):
+    import torch
+
+    import paper_2403_09195_b200 as dfa
+    from paper_2403_09195_b200 import _lib
+
+    h = 6
+    offs = [j % args.r for j in range(h)]
+    cfg = dfa.AttentionConfig(4096, args.w, args.r, h, 64, offs)
+    q, k, v = (torch.randn((args.batch, 4096, h, 64), device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    o = torch.empty_like(q)
+    tr = torch.zeros(5 * CAP, dtype=torch.int64, device="cuda")
+    c = cfg._c()
+    for _ in range(3):  # warm (clocks, L2 state)
+        dfa.dfa_forward(q, k, v, cfg, out=o)
+    dfa._check(dfa.lib.dfa_forward_traced(ctypes.byref(c), args.batch, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                          o.data_ptr(), tr.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    out = os.path.join(ROOT, "gpurun_out", f"trace_w{args.w}_r{args.r}.npy")
+    np.save(out, tr.cpu().numpy().astype(np.uint64))
+    show(out)
+
+
+def decode(path):
+    raw = np.load(path).astype(np.uint64)
+    ev = {}
+    for s, role in enumerate(ROLES):
+        seg = raw[s * CAP:(s + 1) * CAP]
+        seg = seg[seg != 0]
+        ev[role] = [(int(x >> np.uint64(56)), int(x & np.uint64(0xFFFFFFFFFFFFFF))) for x in seg]
+    t0 = min(e[0][1] for e in ev.values() if e)
+    return {r: [(NAMES[c], t - t0) for c, t in e] for r, e in ev.items()}, t0
+
+
+def spans(events, a, b):
+    """durations from each event a to the next event b."""
+    out, start = [], None
+    for name, t in events:
+        if name == a:
+            start = t
+        elif name == b and start is not None:
+            out.append(t - start)
+            start = None
+    return np.array(out) if out else np.array([0])
+
+
+def show(path):
+    ev, _ = decode(path)
+    end = max(t for e in ev.values() for _, t in e)
+    print(f"CTA 0 timeline: {end} cycles total")
+    for role in ("softmax_A", "softmax_B"):
+        e = ev[role]
+        n = sum(1 for x, _ in e if x == "S_READY")
+        sw = spans(e, "S_WAIT", "S_READY")
+        mx = spans(e, "S_READY", "MAX_DONE")
+        ex = spans(e, "MAX_DONE", "EXP_DONE")
+        pa = spans(e, "EXP_DONE", "P_ARRIVE")
+        gap = spans(e, "P_ARRIVE", "S_WAIT")
+        busy = mx.sum() + ex.sum() + pa.sum()
+        print(f"{role}: {n} steps; per step mean: wait-S {sw.mean():.0f}, ld+max {mx.mean():.0f}, "
+              f"exp {ex.mean():.0f}, tail {pa.mean():.0f}, between {gap.mean():.0f}; busy {busy / end:.1%} "
+              f"(wait-S total {sw.sum() / end:.1%})")
+    m = ev["mma"]
+    pw = spans(m, "P_WAIT", "P_READY")
+    qw = spans(m, "QK_WAIT", "QK_ISSUED")
+    print(f"mma: p-wait mean {pw.mean():.0f} (total {pw.sum() / end:.1%}), qk wait+issue mean {qw.mean():.0f} "
+          f"(total {qw.sum() / end:.1%})")
+    pr = ev["producer"]
+    kw = spans(pr, "KV_WAIT", "KV_ISSUE")
+    print(f"producer: kv-empty wait mean {kw.mean():.0f} (total {kw.sum() / end:.1%})")
+    ep = ev["epilogue"]
+    ow = spans(ep, "O_WAIT", "O_READY")
+    st = spans(ep, "O_READY", "STORE_ISSUED")
+    print(f"epilogue: o-full wait mean {ow.mean():.0f} (total {ow.sum() / end:.1%}), "
+          f"readout+store mean {st.mean():.0f}")
+    # first few steps in detail
+    for role in ("mma", "softmax_A", "softmax_B"):
+        print(role, " ".join(f"{n}@{t}" for n, t in ev[role][:24]))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cmd", choices=["run", "show"])
+    ap.add_argument("path", nargs="?")
+    ap.add_argument("--w", type=int, default=512)
+    ap.add_argument("--r", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=64)
+    a = ap.parse_args()
+    run(a) if a.cmd == "run" else show(a.path)
