@@ -69,8 +69,19 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: p <= 2^8 between rescales
 constexpr int kPolyFrom = 6;               // elements e % 8 >= 6 use the FMA-pipe exp2
 
+// Geometry of one work unit, identical in every role.
+struct Unit {
+  int32_t b, j, gamma;
+  int32_t t0;              // first t' of slot A
+  int32_t kv_lo;           // first key t' (a segment start)
+  int32_t n_kv;            // key tiles in the unit
+  int32_t kt0a, kt1a, kt0b, kt1b;  // key-tile range [kt0, kt1) of slot A / B (empty if equal)
+  __device__ __forceinline__ int32_t kt0(int s) const { return s ? kt0b : kt0a; }
+  __device__ __forceinline__ int32_t kt1(int s) const { return s ? kt1b : kt1a; }
+};
+
 struct __align__(1024) SmemLayout {
-  uint8_t q[kQStages][2][kTileBytes];
+  uint8_t q[kQStages][2][kTileBytes];  // contiguous: tile (stage, slot) at index stage * 2 + slot
   uint8_t k[kKVStages][kTileBytes];
   uint8_t v[kKVStages][kTileBytes];
   uint8_t ostage[2][kTileBytes];
@@ -84,6 +95,7 @@ struct __align__(1024) SmemLayout {
   uint64_t stat_full[2];       // slot -> epilogue: row stats of the finished unit written
   float stat_l[2][2][kBM];     // [unit parity][slot][row] normaliser l
   float stat_m[2][2][kBM];     // [unit parity][slot][row] reference max (raw score units), for lse
+  Unit unit_ring[4];           // MMA issuer: geometry of the units its two cursors are in
   uint32_t tmem_base;
 };
 
@@ -117,17 +129,6 @@ struct Sm100Params {
   float scale;
   FastDiv div_pairs, div_h, div_m;
   int32_t offsets[kMaxHeads];
-};
-
-// Geometry of one work unit, identical in every role.
-struct Unit {
-  int32_t b, j, gamma;
-  int32_t t0;              // first t' of slot A
-  int32_t kv_lo;           // first key t' (a segment start)
-  int32_t n_kv;            // key tiles in the unit
-  int32_t kt0a, kt1a, kt0b, kt1b;  // key-tile range [kt0, kt1) of slot A / B (empty if equal)
-  __device__ __forceinline__ int32_t kt0(int s) const { return s ? kt0b : kt0a; }
-  __device__ __forceinline__ int32_t kt1(int s) const { return s ? kt1b : kt1a; }
 };
 
 __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
@@ -164,64 +165,63 @@ __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
   return x;
 }
 
-// The CTA's step sequence, identical in every role: units u = blockIdx.x +
-// i*gridDim.x, key tiles kt of the unit, slots s (A then B) that use kt.
-// Step k uses S buffer k % 3.
-struct Step {
-  Unit x;
-  int32_t u, i, kt, g, k, s;  // unit, local unit index, key tile, CTA-global key tile, step, slot
+// Per-unit step order (identical in every role): key tiles kt ascending, and
+// for each kt slot A then slot B if the slot uses kt.  The CTA-global step
+// index k selects S buffer k % 3.
+__device__ __forceinline__ bool uses(const Unit& x, int slot, int32_t kt) {
+  return kt >= x.kt0(slot) && kt < x.kt1(slot);
+}
+__device__ __forceinline__ int32_t clamp_count(int32_t kt, int32_t lo, int32_t hi) {
+  return min(max(kt, lo), hi) - lo;  // tiles of [lo, hi) before kt
+}
+// index of step (kt, slot) within its unit
+__device__ __forceinline__ int32_t step_in_unit(const Unit& x, int32_t kt, int slot) {
+  return clamp_count(kt, x.kt0a, x.kt1a) + clamp_count(kt, x.kt0b, x.kt1b) + (slot == 1 && uses(x, 0, kt) ? 1 : 0);
+}
+__device__ __forceinline__ int32_t steps_of_unit(const Unit& x) { return (x.kt1a - x.kt0a) + (x.kt1b - x.kt0b); }
+
+// Cursor over the step sequence for the single-thread MMA issuer.  Unit
+// geometry lives in a 4-entry smem ring written by the look-ahead cursor.
+struct Cursor {
+  int32_t u, i, kt, s, g;
+  uint32_t b;      // S buffer = step % 3
+  uint32_t gs;     // K/V stage = g % 3
+  uint32_t gpar;   // K/V full-barrier parity = (g / 3) & 1
   bool valid;
-
-  __device__ __forceinline__ bool uses(int32_t slot, int32_t tile) const {
-    return tile >= x.kt0(slot) && tile < x.kt1(slot);
-  }
-  __device__ __forceinline__ bool first_of_slot() const { return kt == x.kt0(s); }
-  __device__ __forceinline__ bool last_of_slot() const { return kt == x.kt1(s) - 1; }
-  __device__ __forceinline__ bool last_use_of_tile() const { return s == 1 || !uses(1, kt); }
-
-  __device__ __forceinline__ void next(const Sm100Params& p) {
-    while (true) {
-      if (++s == 2) {
-        s = 0;
-        ++g;
-        if (++kt >= x.n_kv) {
-          u += gridDim.x;
-          ++i;
-          if (u >= p.n_units) {
-            valid = false;
-            return;
-          }
-          x = make_unit(p, u);
-          kt = 0;
-        }
-      }
-      if (uses(s, kt)) {
-        ++k;
-        return;
+  __device__ __forceinline__ void step_counters(bool new_tile) {
+    b = (b == kSBufs - 1) ? 0 : b + 1;
+    if (new_tile) {
+      ++g;
+      if (++gs == kKVStages) {
+        gs = 0;
+        gpar ^= 1u;
       }
     }
   }
-  __device__ __forceinline__ void start(const Sm100Params& p) {
-    u = blockIdx.x;
-    i = 0;
+  // advance to the next step; `writer` computes the next unit into the ring
+  __device__ __forceinline__ void advance(const Sm100Params& p, Unit* ring, bool writer) {
+    const Unit& x = ring[i & 3];
+    if (s == 0 && uses(x, 1, kt)) {
+      s = 1;
+      step_counters(false);
+      return;
+    }
+    ++kt;
+    if (kt < x.n_kv) {
+      s = uses(x, 0, kt) ? 0 : 1;
+      step_counters(true);
+      return;
+    }
+    u += gridDim.x;
+    ++i;
+    if (u >= p.n_units) {
+      valid = false;
+      return;
+    }
+    if (writer) ring[i & 3] = make_unit(p, u);
     kt = 0;
-    g = 0;
-    k = -1;
-    s = -1;
-    valid = u < p.n_units;
-    if (!valid) return;
-    x = make_unit(p, u);
-    while (true) {
-      if (++s == 2) {  // (only reached if slot A does not use tile 0: impossible)
-        s = 0;
-        ++g;
-        ++kt;
-      }
-      if (uses(s, kt)) {
-        ++k;
-        return;
-      }
-    }
+    s = 0;  // slot A always starts at key tile 0 of its unit
+    step_counters(true);
   }
 };
 
@@ -293,8 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tbase = sm.tmem_base;
 
   // Registers: 512 x 128 at launch; rebalanced per warpgroup to
-  // producer/MMA 56, softmax 2 x 184, epilogue 88 (sum = 65536).
-  if (warp < 4) ptx::setmaxnreg_dec<56>();
+  // producer/MMA 80, softmax 2 x 176, epilogue 72 (sum 64512 <= 65536).
+  if (warp < 4) ptx::setmaxnreg_dec<80>();
   if (warp == 0) {
     // ============================================================ producer
     if (ptx::elect_one()) {
@@ -333,70 +333,86 @@ __global__ void __launch_bounds__(kThreads, 1)
       int32_t qk_left0 = 0, qk_left1 = 0, qk_unit0 = -1, qk_unit1 = -1;
       uint32_t oc_par = 0;  // bit s: parity of slot s's completed-unit count
 
-      auto issue_qk = [&](const Step& st) {
-        const uint32_t qs = st.i % kQStages;
+      // Shared-memory descriptors of every operand tile, built once; a K step
+      // of 16 bf16 (32 B) advances the start-address field by 2, a 16-key
+      // step of V (16 rows x 128 B) by 128.
+      const uint64_t qdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.q[0][0]));
+      const uint64_t kdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.k[0]));
+      const uint64_t vdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.v[0]));
+      auto issue_qk = [&](const Cursor& c) {
+        const Unit& x = sm.unit_ring[c.i & 3];
+        const uint32_t qs = c.i & 1;
         DFA_TRACE(1, TR_QK_WAIT);
-        ptx::mbar_wait(&sm.q_full[qs], (st.i / kQStages) & 1);
-        const uint32_t ks = st.g % kKVStages;
-        ptx::mbar_wait(&sm.kv_full[ks], (st.g / kKVStages) & 1);
+        ptx::mbar_wait(&sm.q_full[qs], (c.i >> 1) & 1);
+        ptx::mbar_wait(&sm.kv_full[c.gs], c.gpar);
         ptx::tc_fence_after();
-        const uint32_t qa = ptx::smem_u32(sm.q[qs][st.s]);
-        const uint32_t ka = ptx::smem_u32(sm.k[ks]);
-        const uint32_t b = st.k % kSBufs;
+        const uint64_t qd = qdesc0 + (uint64_t)((qs * 2 + c.s) * (kTileBytes >> 4));
+        const uint64_t kd = kdesc0 + (uint64_t)(c.gs * (kTileBytes >> 4));
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
-          ptx::mma_ss(tbase + col_s(b), ptx::sdesc_sw128(qa + kk * 32), ptx::sdesc_sw128(ka + kk * 32), idesc_qk,
-                      kk > 0);
-        ptx::tc_commit(&sm.s_full[st.s][b]);
+          ptx::mma_ss(tbase + col_s(c.b), qd + (uint64_t)(2 * kk), kd + (uint64_t)(2 * kk), idesc_qk, kk > 0);
+        ptx::tc_commit(&sm.s_full[c.s][c.b]);
         DFA_TRACE(1, TR_QK_ISSUED);
         int32_t& unit_ref = qs ? qk_unit1 : qk_unit0;
         int32_t& left_ref = qs ? qk_left1 : qk_left0;
-        if (unit_ref != st.i) {
-          unit_ref = st.i;
-          left_ref = (st.x.kt1a - st.x.kt0a) + (st.x.kt1b - st.x.kt0b);
+        if (unit_ref != c.i) {
+          unit_ref = c.i;
+          left_ref = steps_of_unit(x);
         }
         if (--left_ref == 0) ptx::tc_commit(&sm.q_empty[qs]);  // both Q tiles of the unit consumed
       };
 
-      Step pv, qk;
-      pv.start(p);
-      qk.start(p);
+      Cursor qk, pv;
+      qk.u = blockIdx.x;
+      qk.i = 0;
+      qk.kt = 0;
+      qk.s = 0;
+      qk.g = 0;
+      qk.b = 0;
+      qk.gs = 0;
+      qk.gpar = 0;
+      qk.valid = qk.u < p.n_units;
+      if (qk.valid) sm.unit_ring[0] = make_unit(p, qk.u);
+      pv = qk;
+      uint32_t p_par = 0;  // bit b: parity of the next p_full[b] phase
       for (int n = 0; n < kSBufs && qk.valid; ++n) {
         issue_qk(qk);
-        qk.next(p);
+        qk.advance(p, sm.unit_ring, true);
       }
       while (pv.valid) {
-        const uint32_t b = pv.k % kSBufs;
+        const Unit& x = sm.unit_ring[pv.i & 3];
+        const uint32_t b = pv.b;
         const int s = pv.s;
+        const bool first = pv.kt == x.kt0(s);
         DFA_TRACE(1, TR_P_WAIT);
-        ptx::mbar_wait(&sm.p_full[b], (pv.k / kSBufs) & 1);
+        ptx::mbar_wait(&sm.p_full[b], (p_par >> b) & 1u);
+        p_par ^= 1u << b;
         DFA_TRACE(1, TR_P_READY);
-        if (pv.first_of_slot()) ptx::mbar_wait(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u);
+        if (first) ptx::mbar_wait(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u);
         ptx::tc_fence_after();
-        const uint32_t va = ptx::smem_u32(sm.v[pv.g % kKVStages]);
-        const bool first = pv.first_of_slot();
+        const uint64_t vdesc = vdesc0 + (uint64_t)(pv.gs * (kTileBytes >> 4));
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk)
-          ptx::mma_ts(tbase + col_o(s), tbase + col_s(b) + kk * 8, ptx::sdesc_sw128(va + kk * 2048), idesc_pv,
+          ptx::mma_ts(tbase + col_o(s), tbase + col_s(b) + kk * 8, vdesc + (uint64_t)(kk * (2048 >> 4)), idesc_pv,
                       (!first || kk > 0) ? 1u : 0u);
         ptx::tc_commit(&sm.pv_done[s]);
         DFA_TRACE(1, TR_PV_ISSUED);
-        if (pv.last_of_slot()) {
+        if (pv.kt == x.kt1(s) - 1) {
           ptx::tc_commit(&sm.o_full[s]);
           oc_par ^= 1u << s;
         }
-        if (pv.last_use_of_tile()) ptx::tc_commit(&sm.kv_empty[pv.g % kKVStages]);
+        if (s == 1 || !uses(x, 1, pv.kt)) ptx::tc_commit(&sm.kv_empty[pv.gs]);
         // S buffer b is free once this P V has read it (in-order execution).
         if (qk.valid) {
           issue_qk(qk);
-          qk.next(p);
+          qk.advance(p, sm.unit_ring, true);
         }
-        pv.next(p);
+        pv.advance(p, sm.unit_ring, false);
       }
     }
   } else if (warp >= 4 && warp < 12) {
     // ====================================================== softmax slots
-    ptx::setmaxnreg_inc<184>();
+    ptx::setmaxnreg_inc<176>();
     const int s = (warp - 4) / 4;                 // slot
     const uint32_t row = (warp % 4) * 32 + lane;  // query row in tile == TMEM lane
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
@@ -408,12 +424,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t steps = 0;    // steps of this slot so far
     float mref = -INFINITY, l = 0.0f;
     int32_t seg_lo = 0, seg_hi = 0;
-    Step st;
-    st.start(p);
-    for (; st.valid; st.next(p)) {
-      if (st.s != s) continue;
-      const Unit& x = st.x;
-      if (st.first_of_slot()) {
+    int32_t k_base = 0;  // CTA-global index of the unit's first step
+    int32_t i = 0;
+    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
+      const Unit x = make_unit(p, u);
+      const int32_t kt_lo = x.kt0(s), kt_hi = x.kt1(s);
+      const int32_t k_unit = k_base;
+      k_base += steps_of_unit(x);
+      if (kt_lo == kt_hi) continue;  // no rows for this slot in this unit
+      {
         const int32_t tq = x.t0 + s * kBM + (int32_t)row;
         const bool valid_q = tq < p.T;
         seg_lo = valid_q ? p.div_m.div(tq) * p.m : 0;
@@ -421,7 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mref = -INFINITY;
         l = 0.0f;
       }
-      const uint32_t b = st.k % kSBufs;
+      for (int32_t kt = kt_lo; kt < kt_hi; ++kt) {
+      const uint32_t b = (uint32_t)(k_unit + step_in_unit(x, kt, s)) % kSBufs;
       DFA_TRACE(2 + s, TR_S_WAIT);
       ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
       DFA_TRACE(2 + s, TR_S_READY);
@@ -432,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + 32 * c, sr[c]);
       ptx::tmem_ld_wait();
-      const int32_t k0 = x.kv_lo + st.kt * kBN;
+      const int32_t k0 = x.kv_lo + kt * kBN;
       const int32_t lo = min(max(seg_lo - k0, 0), kBN);
       const int32_t hi = min(max(seg_hi - k0, 0), kBN);
       if (!(lo == 0 && hi == kBN)) {
@@ -511,18 +531,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&sm.p_full[b]);
       DFA_TRACE(2 + s, TR_P_ARRIVE);
-      if (st.last_of_slot()) {
-        // Hand the row statistics to the epilogue warpgroup (double-buffered
-        // by unit parity; the pv_done wait above orders this write after the
-        // epilogue's read of the same buffer two units ago).
-        sm.stat_l[st.i & 1][s][row] = l;
-        sm.stat_m[st.i & 1][s][row] = mref;
-        ptx::mbar_arrive(&sm.stat_full[s]);
-      }
+      }  // key tiles of the unit
+      // Hand the row statistics to the epilogue warpgroup (double-buffered by
+      // unit parity; the pv_done waits order this write after the epilogue's
+      // read of the same buffer two units ago).
+      sm.stat_l[i & 1][s][row] = l;
+      sm.stat_m[i & 1][s][row] = mref;
+      ptx::mbar_arrive(&sm.stat_full[s]);
     }
   } else if (warp >= 12) {
     // ============================================================ epilogue
-    ptx::setmaxnreg_dec<88>();
+    ptx::setmaxnreg_dec<72>();
     const uint32_t row = (warp % 4) * 32 + lane;
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const bool leader = warp == 12 && lane == 0;
