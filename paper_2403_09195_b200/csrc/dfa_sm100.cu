@@ -180,9 +180,12 @@ __device__ __forceinline__ int32_t step_in_unit(const Unit& x, int32_t kt, int s
 }
 __device__ __forceinline__ int32_t steps_of_unit(const Unit& x) { return (x.kt1a - x.kt0a) + (x.kt1b - x.kt0b); }
 
-// Cursor over the step sequence for the single-thread MMA issuer.  Unit
-// geometry lives in a 4-entry smem ring written by the look-ahead cursor.
+// Cursor over the step sequence for the single-thread MMA issuer.  The
+// cursor keeps its unit's geometry in registers; the look-ahead cursor
+// publishes each new unit into a 4-entry smem ring from which the lagging
+// cursor copies it once per unit (same thread: no synchronisation needed).
 struct Cursor {
+  Unit x;
   int32_t u, i, kt, s, g;
   uint32_t b;      // S buffer = step % 3
   uint32_t gs;     // K/V stage = g % 3
@@ -198,9 +201,7 @@ struct Cursor {
       }
     }
   }
-  // advance to the next step; `writer` computes the next unit into the ring
   __device__ __forceinline__ void advance(const Sm100Params& p, Unit* ring, bool writer) {
-    const Unit& x = ring[i & 3];
     if (s == 0 && uses(x, 1, kt)) {
       s = 1;
       step_counters(false);
@@ -218,7 +219,12 @@ struct Cursor {
       valid = false;
       return;
     }
-    if (writer) ring[i & 3] = make_unit(p, u);
+    if (writer) {
+      x = make_unit(p, u);
+      ring[i & 3] = x;
+    } else {
+      x = ring[i & 3];
+    }
     kt = 0;
     s = 0;  // slot A always starts at key tile 0 of its unit
     step_counters(true);
@@ -340,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t kdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.k[0]));
       const uint64_t vdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.v[0]));
       auto issue_qk = [&](const Cursor& c) {
-        const Unit& x = sm.unit_ring[c.i & 3];
+        const Unit& x = c.x;
         const uint32_t qs = c.i & 1;
         DFA_TRACE(1, TR_QK_WAIT);
         ptx::mbar_wait(&sm.q_full[qs], (c.i >> 1) & 1);
@@ -372,7 +378,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       qk.gs = 0;
       qk.gpar = 0;
       qk.valid = qk.u < p.n_units;
-      if (qk.valid) sm.unit_ring[0] = make_unit(p, qk.u);
+      if (qk.valid) {
+        qk.x = make_unit(p, qk.u);
+        sm.unit_ring[0] = qk.x;
+      }
       pv = qk;
       uint32_t p_par = 0;  // bit b: parity of the next p_full[b] phase
       for (int n = 0; n < kSBufs && qk.valid; ++n) {
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         qk.advance(p, sm.unit_ring, true);
       }
       while (pv.valid) {
-        const Unit& x = sm.unit_ring[pv.i & 3];
+        const Unit& x = pv.x;
         const uint32_t b = pv.b;
         const int s = pv.s;
         const bool first = pv.kt == x.kt0(s);
