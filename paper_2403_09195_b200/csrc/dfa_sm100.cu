@@ -310,6 +310,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t i = 0, g = 0;
       for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
         const Unit x = make_unit(p, u);
+        // Pull the next unit's tiles into L2 now: DRAM latency then overlaps a
+        // whole unit of compute without holding shared-memory stages.
+        if (u + (int32_t)gridDim.x < p.n_units) {
+          const Unit y = make_unit(p, u + gridDim.x);
+          ptx::tma_prefetch_5d(&tm_q, 0, y.j, y.gamma, y.t0, y.b);
+          ptx::tma_prefetch_5d(&tm_q, 0, y.j, y.gamma, y.t0 + kBM, y.b);
+          for (int32_t kt = 0; kt < y.n_kv; ++kt) {
+            ptx::tma_prefetch_5d(&tm_k, 0, y.j, y.gamma, y.kv_lo + kt * kBN, y.b);
+            ptx::tma_prefetch_5d(&tm_v, 0, y.j, y.gamma, y.kv_lo + kt * kBN, y.b);
+          }
+        }
         const uint32_t qs = i % kQStages;
         ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
         DFA_TRACE(0, TR_Q_ISSUE);
