@@ -26,7 +26,9 @@
 // own segment are masked (only when m is not a multiple of 128, or at tails).
 //
 // Warp roles (384 threads, one CTA per SM, persistent over units):
-//   warp 0      TMA producer: Q_A/Q_B (2-deep), K/V tiles (3-deep ring)
+//   warp 0      TMA producer: Q_A/Q_B (2-deep), K tiles (3-deep ring, a stage
+//               is freed as soon as its Q K^T completes)
+//   warp 3      TMA producer: V tiles (3-deep ring, freed after P V)
 //   warp 1      MMA issuer (one elected lane):
 //                 S_x = Q_x K^T   tcgen05.mma M=128 N=128 K=64 -> TMEM (fp32)
 //                 O_x += P_x V    tcgen05.mma A = P_x from TMEM, B = V (MN-major)
@@ -87,7 +89,8 @@ struct __align__(1024) SmemLayout {
   uint8_t ostage[2][kTileBytes];
   uint8_t zero[kTileBytes];
   uint64_t q_full[kQStages], q_empty[kQStages];
-  uint64_t kv_full[kKVStages], kv_empty[kKVStages];
+  uint64_t k_full[kKVStages], k_empty[kKVStages];  // K ring: freed when its last Q K^T completes
+  uint64_t v_full[kKVStages], v_empty[kKVStages];  // V ring: freed when its last P V completes
   uint64_t s_full[2][kSBufs];  // MMA -> slot s: S ready in buffer b
   uint64_t p_full[kSBufs];     // slot -> MMA: P written in buffer b (128 arrivals)
   uint64_t pv_done[2];         // MMA -> slot s: its latest P V completed
@@ -271,8 +274,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.q_empty[s], 1);
     }
     for (int s = 0; s < kKVStages; ++s) {
-      ptx::mbar_init(&sm.kv_full[s], 1);
-      ptx::mbar_init(&sm.kv_empty[s], 1);
+      ptx::mbar_init(&sm.k_full[s], 1);
+      ptx::mbar_init(&sm.k_empty[s], 1);
+      ptx::mbar_init(&sm.v_full[s], 1);
+      ptx::mbar_init(&sm.v_empty[s], 1);
     }
     for (int b = 0; b < kSBufs; ++b) {
       ptx::mbar_init(&sm.s_full[0][b], 1);
@@ -310,17 +315,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t i = 0, g = 0;
       for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
         const Unit x = make_unit(p, u);
-        // Pull the next unit's tiles into L2 now: DRAM latency then overlaps a
-        // whole unit of compute without holding shared-memory stages.
-        if (u + (int32_t)gridDim.x < p.n_units) {
-          const Unit y = make_unit(p, u + gridDim.x);
-          ptx::tma_prefetch_5d(&tm_q, 0, y.j, y.gamma, y.t0, y.b);
-          ptx::tma_prefetch_5d(&tm_q, 0, y.j, y.gamma, y.t0 + kBM, y.b);
-          for (int32_t kt = 0; kt < y.n_kv; ++kt) {
-            ptx::tma_prefetch_5d(&tm_k, 0, y.j, y.gamma, y.kv_lo + kt * kBN, y.b);
-            ptx::tma_prefetch_5d(&tm_v, 0, y.j, y.gamma, y.kv_lo + kt * kBN, y.b);
-          }
-        }
         const uint32_t qs = i % kQStages;
         ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
         DFA_TRACE(0, TR_Q_ISSUE);
@@ -330,12 +324,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
           const uint32_t st = g % kKVStages;
           DFA_TRACE(0, TR_KV_WAIT);
-          ptx::mbar_wait(&sm.kv_empty[st], ((g / kKVStages) & 1) ^ 1);
+          ptx::mbar_wait(&sm.k_empty[st], ((g / kKVStages) & 1) ^ 1);
           DFA_TRACE(0, TR_KV_ISSUE);
-          ptx::mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
-          const int32_t kr = x.kv_lo + kt * kBN;
-          ptx::tma_load_5d(sm.k[st], &tm_k, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol);
-          ptx::tma_load_5d(sm.v[st], &tm_v, &sm.kv_full[st], 0, x.j, x.gamma, kr, x.b, pol);
+          ptx::mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
+          ptx::tma_load_5d(sm.k[st], &tm_k, &sm.k_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ========================================================== V producer
+    if (ptx::elect_one()) {
+      const uint64_t pol = ptx::policy_evict_first();
+      uint32_t g = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Unit x = make_unit(p, u);
+        for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
+          const uint32_t st = g % kKVStages;
+          ptx::mbar_wait(&sm.v_empty[st], ((g / kKVStages) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
+          ptx::tma_load_5d(sm.v[st], &tm_v, &sm.v_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
         }
       }
     }
@@ -361,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t qs = c.i & 1;
         DFA_TRACE(1, TR_QK_WAIT);
         ptx::mbar_wait(&sm.q_full[qs], (c.i >> 1) & 1);
-        ptx::mbar_wait(&sm.kv_full[c.gs], c.gpar);
+        ptx::mbar_wait(&sm.k_full[c.gs], c.gpar);
         ptx::tc_fence_after();
         const uint64_t qd = qdesc0 + (uint64_t)((qs * 2 + c.s) * (kTileBytes >> 4));
         const uint64_t kd = kdesc0 + (uint64_t)(c.gs * (kTileBytes >> 4));
@@ -369,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kk = 0; kk < kD / 16; ++kk)
           ptx::mma_ss(tbase + col_s(c.b), qd + (uint64_t)(2 * kk), kd + (uint64_t)(2 * kk), idesc_qk, kk > 0);
         ptx::tc_commit(&sm.s_full[c.s][c.b]);
+        if (c.s == 1 || !uses(x, 1, c.kt)) ptx::tc_commit(&sm.k_empty[c.gs]);  // last Q K^T of this K tile
         DFA_TRACE(1, TR_QK_ISSUED);
         int32_t& unit_ref = qs ? qk_unit1 : qk_unit0;
         int32_t& left_ref = qs ? qk_left1 : qk_left0;
@@ -409,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         p_par ^= 1u << b;
         DFA_TRACE(1, TR_P_READY);
         if (first) ptx::mbar_wait(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u);
+        ptx::mbar_wait(&sm.v_full[pv.gs], pv.gpar);
         ptx::tc_fence_after();
         const uint64_t vdesc = vdesc0 + (uint64_t)(pv.gs * (kTileBytes >> 4));
 #pragma unroll
@@ -421,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tc_commit(&sm.o_full[s]);
           oc_par ^= 1u << s;
         }
-        if (s == 1 || !uses(x, 1, pv.kt)) ptx::tc_commit(&sm.kv_empty[pv.gs]);
+        if (s == 1 || !uses(x, 1, pv.kt)) ptx::tc_commit(&sm.v_empty[pv.gs]);
         // S buffer b is free once this P V has read it (in-order execution).
         if (qk.valid) {
           issue_qk(qk);

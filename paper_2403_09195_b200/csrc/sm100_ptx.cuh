@@ -78,13 +78,6 @@ __device__ __forceinline__ void tma_load_5d(void* smem_dst, const void* tmap, ui
       "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(cache_hint)
       : "memory");
 }
-// 5-D tile prefetch into L2 (no shared memory, no completion tracking).
-__device__ __forceinline__ void tma_prefetch_5d(const void* tmap, int32_t c0, int32_t c1, int32_t c2, int32_t c3,
-                                                int32_t c4) {
-  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(tmap), "r"(c0),
-               "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-               : "memory");
-}
 // 5-D tile store from shared memory (bulk-group completion).
 __device__ __forceinline__ void tma_store_5d(const void* tmap, const void* smem_src, int32_t c0, int32_t c1,
                                              int32_t c2, int32_t c3, int32_t c4) {
