@@ -131,6 +131,7 @@ struct Sm100Params {
   float c;           // scale * log2(e)
   float scale;
   FastDiv div_pairs, div_h, div_m;
+  int32_t pingpong;  // 1: slots A and B take equal step counts in every unit -> alternate exp phases
   int32_t offsets[kMaxHeads];
 };
 
@@ -455,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t seg_lo = 0, seg_hi = 0;
     int32_t k_base = 0;  // CTA-global index of the unit's first step
     int32_t i = 0;
+    if (p.pingpong && s == 1) ptx::named_bar_arrive(2, 2 * kBM);  // slot A goes first
     for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
       const Unit x = make_unit(p, u);
       const int32_t kt_lo = x.kt0(s), kt_hi = x.kt1(s);
@@ -530,6 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (move) mref = tmax;
       const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
+      // Ping-pong: the two slots take turns on the exponential phase so one
+      // slot's MUFU work overlaps the other's loads, max and bookkeeping.
+      if (p.pingpong) ptx::named_bar_sync(2 + s, 2 * kBM);
       float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -549,6 +554,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_st16(tS + 16 * c, pk);
       }
       l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      if (p.pingpong) {
+        const bool last_step = kt == kt_hi - 1 && u + (int32_t)gridDim.x >= p.n_units;
+        if (!(s == 1 && last_step)) ptx::named_bar_arrive(2 + (1 - s), 2 * kBM);  // hand over to the other slot
+      }
       DFA_TRACE(2 + s, TR_EXP_DONE);
       // keep the pv_done phases in lockstep with the steps
       if (!waited && steps > 0) {
@@ -727,6 +736,11 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.div_pairs = make_fastdiv((uint32_t)p.n_pairs);
   p.div_h = make_fastdiv((uint32_t)p.h);
   p.div_m = make_fastdiv((uint32_t)p.m);
+  // Strict A/B alternation needs equal step counts per unit in both slots:
+  // slot B never empty (T % 256 == 0) and every 128-row query tile inside one
+  // segment with full-length segments (m % 128 == 0, T % m == 0), or whole
+  // segments packed in a tile (128 % m == 0).
+  p.pingpong = (p.T % kUnitRows == 0) && ((p.m % kBM == 0 && p.T % p.m == 0) || (kBM % p.m == 0)) ? 1 : 0;
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
   const size_t smem = sizeof(SmemLayout) + 1024;
   static std::once_flag once;
