@@ -99,6 +99,7 @@ struct __align__(1024) SmemLayout {
   float stat_l[2][2][kBM];     // [unit parity][slot][row] normaliser l
   float stat_m[2][2][kBM];     // [unit parity][slot][row] reference max (raw score units), for lse
   Unit unit_ring[4];           // MMA issuer: geometry of the units its two cursors are in
+  float exp_scale;             // p.c, re-read after the ping-pong barrier (orders the exps behind it)
   uint32_t tmem_base;
 };
 
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.stat_full[s], kBM);
     }
     ptx::fence_barrier_init();
+    sm.exp_scale = p.c;
     ptx::tma_prefetch_desc(&tm_q);
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
@@ -534,7 +536,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
       // Ping-pong: the two slots take turns on the exponential phase so one
       // slot's MUFU work overlaps the other's loads, max and bookkeeping.
-      if (p.pingpong) ptx::named_bar_sync(2 + s, 2 * kBM);
+      float cexp = p.c;
+      if (p.pingpong) {
+        ptx::named_bar_sync(2 + s, 2 * kBM);
+        // an smem load is ordered after bar.sync, so the exponentials (which
+        // depend on it) cannot be scheduled above the barrier
+        cexp = ptx::ld_shared_volatile_f32(&sm.exp_scale);
+      }
       float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -542,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // (3 of 4 on MUFU, 1 of 4 as an FMA-pipe polynomial), sum + pack
         float xv[32];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) xv[e] = fmaf(__uint_as_float(sr[c][e]), p.c, neg);
+        for (int e = 0; e < 32; ++e) xv[e] = fmaf(__uint_as_float(sr[c][e]), cexp, neg);
 #pragma unroll
         for (int e = 0; e < 32; ++e) xv[e] = (e % 8 >= kPolyFrom) ? ptx::ex2_poly(xv[e]) : ptx::ex2(xv[e]);
         uint32_t pk[16];

@@ -255,6 +255,22 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// Opaque copy: the result is only available where this volatile asm sits in
+// program order, so arithmetic depending on it cannot be hoisted above a
+// preceding barrier (registers are not ordered by "memory" clobbers).
+__device__ __forceinline__ float opaque(float x) {
+  float y;
+  asm volatile("mov.b32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Shared-memory load that cannot be hoisted above a preceding barrier.
+__device__ __forceinline__ float ld_shared_volatile_f32(const float* p) {
+  float v;
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
