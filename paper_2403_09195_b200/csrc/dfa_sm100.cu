@@ -35,9 +35,8 @@
 //               ping-ponging slot A and slot B so one softmax overlaps the
 //               other slot's MMAs
 //   warp 2      TMEM allocator (512 columns: S_A, S_B, O_A, O_B)
-//   warps 4-11  slot A softmax + epilogue: warps 4-7 keys 0-63, warps 8-11 keys
-//               64-127 of each tile (TMEM lanes 0-127, two threads per row)
-//   warps 12-19 slot B, same split
+//   warps 4-7   slot A softmax + epilogue (TMEM lanes 0-127, thread = row)
+//   warps 8-11  slot B softmax + epilogue
 // Softmax: tcgen05.ld of the 128-score row, exp2 with the 1/sqrt(d)*log2(e)
 // fold, lazy (2^8 threshold) rescale of O in TMEM, P packed to bf16 and
 // tcgen05.st over the consumed S columns.  Epilogue: O/l -> bf16 -> 128B-
@@ -63,7 +62,7 @@ constexpr int kUnitRows = 2 * kBM;     // t'-rows per work unit
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 bf16), SW128
 constexpr int kQStages = 2;
 constexpr int kKVStages = 3;
-constexpr int kThreads = 640;
+constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSBufs = 3;                                  // rotating S/P buffers
 __host__ __device__ constexpr uint32_t col_s(int buf) { return 128u * buf; }          // S_0..S_2 (P aliases)
@@ -96,8 +95,9 @@ struct __align__(1024) SmemLayout {
   uint64_t p_full[kSBufs];     // slot -> MMA: P written in buffer b (128 arrivals)
   uint64_t pv_done[2];         // MMA -> slot s: its latest P V completed
   uint64_t o_full[2], o_empty[2];
-  float xmax[2][2][2][kBM];    // [parity][slot][half][row] per-half row max exchange
-  float lx[2][2][kBM];         // [slot][half][row] per-half normaliser exchange (epilogue)
+  uint64_t stat_full[2];       // slot -> epilogue: row stats of the finished unit written
+  float stat_l[2][2][kBM];     // [unit parity][slot][row] normaliser l
+  float stat_m[2][2][kBM];     // [unit parity][slot][row] reference max (raw score units), for lse
   Unit unit_ring[4];           // MMA issuer: geometry of the units its two cursors are in
   uint32_t tmem_base;
 };
@@ -282,12 +282,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < kSBufs; ++b) {
       ptx::mbar_init(&sm.s_full[0][b], 1);
       ptx::mbar_init(&sm.s_full[1][b], 1);
-      ptx::mbar_init(&sm.p_full[b], 2 * kBM);
+      ptx::mbar_init(&sm.p_full[b], kBM);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&sm.pv_done[s], 1);
       ptx::mbar_init(&sm.o_full[s], 1);
-      ptx::mbar_init(&sm.o_empty[s], 2 * kBM);
+      ptx::mbar_init(&sm.o_empty[s], kBM);
+      ptx::mbar_init(&sm.stat_full[s], kBM);
     }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tm_q);
@@ -302,9 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = sm.tmem_base;
 
-  // Registers: 640 x 96 at launch; the producer/MMA warpgroup gives part of
-  // its share to the four softmax warpgroups (128 x 56 + 512 x 104 <= 61440).
-  if (warp < 4) ptx::setmaxnreg_dec<56>();
+  // Registers: 512 x 128 at launch; rebalanced per warpgroup to
+  // producer/MMA 80, softmax 2 x 176, epilogue 72 (sum 64512 <= 65536).
+  if (warp < 4) ptx::setmaxnreg_dec<80>();
   if (warp == 0) {
     // ============================================================ producer
     if (ptx::elect_one()) {
@@ -438,86 +439,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         pv.advance(p, sm.unit_ring, false);
       }
     }
-  } else if (warp >= 4) {
-    // ============================================= softmax + epilogue slots
-    // Slot s = (warp - 4) / 8 owns query tile s of the unit; its two
-    // warpgroups split every score row: half 0 keys 0-63, half 1 keys 64-127
-    // of each 128-key tile (same TMEM lanes, different columns).
-    ptx::setmaxnreg_inc<104>();
-    const int s = (warp - 4) / 8;
-    const int half = ((warp - 4) / 4) & 1;
+  } else if (warp >= 4 && warp < 12) {
+    // ====================================================== softmax slots
+    ptx::setmaxnreg_inc<176>();
+    const int s = (warp - 4) / 4;                 // slot
     const uint32_t row = (warp % 4) * 32 + lane;  // query row in tile == TMEM lane
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
-    const uint32_t tO = tbase + lane_base + col_o(s) + 32 * half;  // this half's 32 O columns
-    const uint32_t bar_id = 2 + s;                                 // named barrier of the slot's 256 threads
-    const bool leader = half == 0 && row == 0;
-    const bool tr_on = blockIdx.x == 0 && leader;
+    const uint32_t tO = tbase + lane_base + col_o(s);
+    const bool tr_on = blockIdx.x == 0 && row == 0;
     uint32_t tr_n = 0;
     uint32_t use_par = 0;  // bit b: parity of the next s_full[s][b] phase
     uint32_t pvc = 0;      // pv_done phases consumed
     uint32_t steps = 0;    // steps of this slot so far
-    uint32_t xpar = 0;     // max-exchange buffer parity
     float mref = -INFINITY, l = 0.0f;
     int32_t seg_lo = 0, seg_hi = 0;
-    // pending epilogue (unit finished, O not yet read): deferred to the start
-    // of the slot's next unit so the final P V completes behind other work
-    bool pend = false;
-    uint32_t oc = 0;
-    int32_t pend_j = 0, pend_gamma = 0, pend_ts0 = 0, pend_b = 0, pend_tq = 0;
-    float pend_l = 0.0f, pend_m = -INFINITY;
-
-    auto epilogue = [&]() {
-      ptx::mbar_wait(&sm.o_full[s], oc & 1);
-      ++oc;
-      ptx::tc_fence_after();
-      uint32_t orow[32];
-      ptx::tmem_ld32(tO, orow);
-      ptx::tmem_ld_wait();
-      // row normaliser = both halves' partial sums
-      sm.lx[s][half][row] = pend_l;
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&sm.o_empty[s]);  // O_s may be overwritten by the next unit
-      if (leader) ptx::tma_store_wait_read<0>();  // previous store done reading the staging tile
-      ptx::named_bar_sync(bar_id, 2 * kBM);
-      const float lt = pend_l + sm.lx[s][half ^ 1][row];
-      const bool valid_q = pend_tq < p.T;
-      const float inv = valid_q ? 1.0f / lt : 0.0f;
-      const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
-      // 128B-swizzled staging row: 16B chunk c of row r at ((c ^ (r & 7)) * 16)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float* f = reinterpret_cast<const float*>(&orow[c * 8]);
-        const int chunk = half * 4 + c;
-        const uint32_t addr = stage_addr + row * 128 + ((chunk ^ (row & 7)) * 16);
-        ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0] * inv, f[1] * inv), ptx::pack_bf16x2(f[2] * inv, f[3] * inv),
-                          ptx::pack_bf16x2(f[4] * inv, f[5] * inv), ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
-      }
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(bar_id, 2 * kBM);
-      if (leader) {
-        ptx::tma_store_5d(&tm_o, sm.ostage[s], 0, pend_j, pend_gamma, pend_ts0, pend_b);
-        for (int32_t gz = 0; gz < p.r; ++gz)
-          if (gz != pend_gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, pend_j, gz, pend_ts0, pend_b);
-        ptx::tma_store_commit();
-      }
-      DFA_TRACE(4, TR_STORE_ISSUED);
-      if (lse && valid_q && half == 0) {
-        float* lb = lse + ((int64_t)pend_b * p.h + pend_j) * p.N + (int64_t)pend_tq * p.r;
-        for (int32_t gz = 0; gz < p.r; ++gz)
-          lb[gz] = (gz == pend_gamma) ? pend_m * p.scale + logf(lt) : -INFINITY;
-      }
-      pend = false;
-    };
-
     int32_t k_base = 0;  // CTA-global index of the unit's first step
-    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    int32_t i = 0;
+    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
       const Unit x = make_unit(p, u);
       const int32_t kt_lo = x.kt0(s), kt_hi = x.kt1(s);
       const int32_t k_unit = k_base;
       k_base += steps_of_unit(x);
       if (kt_lo == kt_hi) continue;  // no rows for this slot in this unit
-      const int32_t tq = x.t0 + s * kBM + (int32_t)row;
       {
+        const int32_t tq = x.t0 + s * kBM + (int32_t)row;
         const bool valid_q = tq < p.T;
         seg_lo = valid_q ? p.div_m.div(tq) * p.m : 0;
         seg_hi = valid_q ? min(seg_lo + p.m, p.T) : 0;
@@ -525,110 +470,179 @@ __global__ void __launch_bounds__(kThreads, 1)
         l = 0.0f;
       }
       for (int32_t kt = kt_lo; kt < kt_hi; ++kt) {
-        if (pend) epilogue();  // previous unit's output, before this unit's first P V
-        const uint32_t b = (uint32_t)(k_unit + step_in_unit(x, kt, s)) % kSBufs;
-        DFA_TRACE(2 + s, TR_S_WAIT);
-        ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
-        DFA_TRACE(2 + s, TR_S_READY);
-        use_par ^= 1u << b;
-        ptx::tc_fence_after();
-        const uint32_t tS = tbase + lane_base + col_s(b);
-        uint32_t sr[2][32];
-        ptx::tmem_ld32(tS + 64 * half, sr[0]);
-        ptx::tmem_ld32(tS + 64 * half + 32, sr[1]);
-        ptx::tmem_ld_wait();
-        const int32_t k0 = x.kv_lo + kt * kBN + 64 * half;
-        const int32_t lo = min(max(seg_lo - k0, 0), 64);
-        const int32_t hi = min(max(seg_hi - k0, 0), 64);
-        if (!(lo == 0 && hi == 64)) {
+      const uint32_t b = (uint32_t)(k_unit + step_in_unit(x, kt, s)) % kSBufs;
+      DFA_TRACE(2 + s, TR_S_WAIT);
+      ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
+      DFA_TRACE(2 + s, TR_S_READY);
+      use_par ^= 1u << b;
+      ptx::tc_fence_after();
+      const uint32_t tS = tbase + lane_base + col_s(b);
+      uint32_t sr[4][32];
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+      for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + 32 * c, sr[c]);
+      ptx::tmem_ld_wait();
+      const int32_t k0 = x.kv_lo + kt * kBN;
+      const int32_t lo = min(max(seg_lo - k0, 0), kBN);
+      const int32_t hi = min(max(seg_hi - k0, 0), kBN);
+      if (!(lo == 0 && hi == kBN)) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int col = 32 * c + e;
-              if (col < lo || col >= hi) sr[c][e] = __float_as_uint(-INFINITY);
-            }
-        }
-        float mx[8];
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(sr[c][e]));
-        // row max over both halves (double-buffered exchange through smem)
-        sm.xmax[xpar][s][half][row] = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                            fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        // Both halves have read their S columns past this barrier, so P (which
-        // aliases S columns 0-63) may now be written by either half.
-        ptx::named_bar_sync(bar_id, 2 * kBM);
-        const float tmax = fmaxf(sm.xmax[xpar][s][0][row], sm.xmax[xpar][s][1][row]);
-        xpar ^= 1u;
-        DFA_TRACE(2 + s, TR_MAX_DONE);
-        // Lazy rescale (identical decision in both halves; warp-uniform as
-        // tcgen05.ld/st are warp collectives).  O_s must hold every earlier
-        // P V of this slot: pv_done phases are consumed once per step, in order.
-        const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
-        const bool fix_o = move && mref != -INFINITY;
-        bool waited = false;
-        if (__any_sync(0xffffffffu, fix_o)) {
-          if (steps > 0) {
-            ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
-            ++pvc;
-            waited = true;
+          for (int e = 0; e < 32; ++e) {
+            const int col = 32 * c + e;
+            if (col < lo || col >= hi) sr[c][e] = __float_as_uint(-INFINITY);
           }
-          ptx::tc_fence_after();
-          const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
-          l *= corr;
+      }
+      float mx[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(sr[c][e]));
+      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      DFA_TRACE(2 + s, TR_MAX_DONE);
+      // Lazy rescale (warp-uniform: tcgen05.ld/st are warp collectives).  O_s
+      // must hold every earlier P V of this slot: wait for the slot's previous
+      // P V (pv_done phases are consumed exactly once per step, in order).
+      const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
+      const bool fix_o = move && mref != -INFINITY;
+      bool waited = false;
+      if (__any_sync(0xffffffffu, fix_o)) {
+        if (steps > 0) {
+          ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
+          ++pvc;
+          waited = true;
+        }
+        ptx::tc_fence_after();
+        const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
+        l *= corr;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
           uint32_t orow[32];
-          ptx::tmem_ld32(tO, orow);
+          ptx::tmem_ld32(tO + 32 * c, orow);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * corr);
-          ptx::tmem_st32(tO, orow);
+          ptx::tmem_st32(tO + 32 * c, orow);
         }
-        if (move) mref = tmax;
-        const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
-        float ls[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      }
+      if (move) mref = tmax;
+      const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
+      float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+      const float2 c2 = make_float2(p.c, p.c), n2 = make_float2(neg, neg);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          // scale, exponentiate (3 of 4 on MUFU, 1 of 4 as an FMA-pipe
-          // polynomial), then sum + pack
-          float xv[32];
+      for (int c = 0; c < 4; ++c) {
+        // per 32-column chunk: packed scale-subtract (FFMA2), exponentiate
+        // (3 of 4 pairs on MUFU, 1 of 4 as an FMA-pipe polynomial), packed
+        // sums (FADD2) and bf16 packing
+        float2 xv[16];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) xv[e] = fmaf(__uint_as_float(sr[c][e]), p.c, neg);
+        for (int e = 0; e < 16; ++e)
+          xv[e] = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * e]), __uint_as_float(sr[c][2 * e + 1])), c2, n2);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) xv[e] = (e % 8 >= kPolyFrom) ? ptx::ex2_poly(xv[e]) : ptx::ex2(xv[e]);
-          uint32_t pk[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            ls[(e >> 1) & 3] += xv[e] + xv[e + 1];
-            pk[e / 2] = ptx::pack_bf16x2(xv[e], xv[e + 1]);
+        for (int e = 0; e < 16; ++e) {
+          if (e % 4 == 3) {
+            xv[e] = ptx::ex2_poly2(xv[e]);
+          } else {
+            xv[e].x = ptx::ex2(xv[e].x);
+            xv[e].y = ptx::ex2(xv[e].y);
           }
-          ptx::tmem_st16(tS + 32 * half + 16 * c, pk);
         }
-        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-        DFA_TRACE(2 + s, TR_EXP_DONE);
-        if (!waited && steps > 0) {
-          ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
-          ++pvc;
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          ls2[e & 1] = ptx::fadd2(ls2[e & 1], xv[e]);
+          pk[e] = ptx::pack_bf16x2(xv[e].x, xv[e].y);
         }
-        ++steps;
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&sm.p_full[b]);
-        DFA_TRACE(2 + s, TR_P_ARRIVE);
+        ptx::tmem_st16(tS + 16 * c, pk);
+      }
+      const float2 lsum = ptx::fadd2(ls2[0], ls2[1]);
+      float ls[4] = {lsum.x, lsum.y, 0.0f, 0.0f};
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      DFA_TRACE(2 + s, TR_EXP_DONE);
+      // keep the pv_done phases in lockstep with the steps
+      if (!waited && steps > 0) {
+        ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
+        ++pvc;
+      }
+      ++steps;
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&sm.p_full[b]);
+      DFA_TRACE(2 + s, TR_P_ARRIVE);
       }  // key tiles of the unit
-      pend = true;
-      pend_j = x.j;
-      pend_gamma = x.gamma;
-      pend_ts0 = x.t0 + s * kBM;
-      pend_b = x.b;
-      pend_tq = tq;
-      pend_l = l;
-      pend_m = mref;
+      // Hand the row statistics to the epilogue warpgroup (double-buffered by
+      // unit parity; the pv_done waits order this write after the epilogue's
+      // read of the same buffer two units ago).
+      sm.stat_l[i & 1][s][row] = l;
+      sm.stat_m[i & 1][s][row] = mref;
+      ptx::mbar_arrive(&sm.stat_full[s]);
     }
-    if (pend) epilogue();
+  } else if (warp >= 12) {
+    // ============================================================ epilogue
+    ptx::setmaxnreg_dec<72>();
+    const uint32_t row = (warp % 4) * 32 + lane;
+    const uint32_t lane_base = ((warp % 4) * 32) << 16;
+    const bool leader = warp == 12 && lane == 0;
+    const bool tr_on = blockIdx.x == 0 && leader;
+    uint32_t tr_n = 0;
+    uint32_t par = 0;  // bit s: parity of slot s's completed-unit count
+    int32_t i = 0;
+    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
+      const Unit x = make_unit(p, u);
+#pragma unroll 1
+      for (int s = 0; s < 2; ++s) {
+        if (x.kt0(s) == x.kt1(s)) continue;  // slot has no rows in this unit
+        const int32_t ts0 = x.t0 + s * kBM;
+        const int32_t tq = ts0 + (int32_t)row;
+        const bool valid_q = tq < p.T;
+        const uint32_t ph = (par >> s) & 1u;
+        par ^= 1u << s;
+        DFA_TRACE(4, TR_O_WAIT);
+        ptx::mbar_wait(&sm.o_full[s], ph);
+        DFA_TRACE(4, TR_O_READY);
+        ptx::mbar_wait(&sm.stat_full[s], ph);
+        ptx::tc_fence_after();
+        const float l = sm.stat_l[i & 1][s][row];
+        const float mref = sm.stat_m[i & 1][s][row];
+        const uint32_t tO = tbase + lane_base + col_o(s);
+        uint32_t orow[2][32];
+        ptx::tmem_ld32(tO, orow[0]);
+        ptx::tmem_ld32(tO + 32, orow[1]);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.o_empty[s]);  // O_s (and this stats buffer) may be reused
+        const float inv = valid_q ? 1.0f / l : 0.0f;
+        // the previous TMA store from this staging tile must have finished reading it
+        if (leader) ptx::tma_store_wait_read<0>();
+        ptx::named_bar_sync(1, kBM);
+        const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
+        // 128B-swizzled staging row: 16B chunk c of row r at ((c ^ (r & 7)) * 16)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float* f = reinterpret_cast<const float*>(&orow[c >> 2][(c & 3) * 8]);
+          const uint32_t addr = stage_addr + row * 128 + ((c ^ (row & 7)) * 16);
+          ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0] * inv, f[1] * inv),
+                            ptx::pack_bf16x2(f[2] * inv, f[3] * inv), ptx::pack_bf16x2(f[4] * inv, f[5] * inv),
+                            ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, kBM);
+        if (leader) {
+          ptx::tma_store_5d(&tm_o, sm.ostage[s], 0, x.j, x.gamma, ts0, x.b);
+          for (int32_t gz = 0; gz < p.r; ++gz)
+            if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
+          ptx::tma_store_commit();
+        }
+        DFA_TRACE(4, TR_STORE_ISSUED);
+        if (lse && valid_q) {
+          float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N + (int64_t)tq * p.r;
+          for (int32_t gz = 0; gz < p.r; ++gz) lb[gz] = (gz == x.gamma) ? mref * p.scale + logf(l) : -INFINITY;
+        }
+      }
+    }
     if (leader) ptx::tma_store_wait_all<0>();
   }
 

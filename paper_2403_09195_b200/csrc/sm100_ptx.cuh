@@ -255,20 +255,38 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-// Opaque copy: the result is only available where this volatile asm sits in
-// program order, so arithmetic depending on it cannot be hoisted above a
-// preceding barrier (registers are not ordered by "memory" clobbers).
-__device__ __forceinline__ float opaque(float x) {
-  float y;
-  asm volatile("mov.b32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100a): two lanes per instruction.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
 }
 
-// Shared-memory load that cannot be hoisted above a preceding barrier.
-__device__ __forceinline__ float ld_shared_volatile_f32(const float* p) {
-  float v;
-  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
+// ex2_poly on a pair with packed FFMA2/FADD2 for the arithmetic.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float kMagic = 12582912.0f;
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 f = fadd2(x, fadd2(make_float2(kMagic, kMagic), make_float2(-t.x, -t.y)));
+  float2 p = ffma2(make_float2(5.459282631e-2f, 5.459282631e-2f), f, make_float2(2.422181094e-1f, 2.422181094e-1f));
+  p = ffma2(p, f, make_float2(6.933686450e-1f, 6.933686450e-1f));
+  p = ffma2(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 __device__ __forceinline__ float ex2(float x) {
