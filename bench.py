@@ -278,23 +278,21 @@ def run_b200(args):
     # ---- final gather of the shards to rank 0 (outside the hot path)
     gather = None
     if world > 1:
+        from paper_2403_09195_b200.dist import gather_to_rank0
+
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if rank == 0:
-            bufs = [torch.empty_like(o) for _ in range(world - 1)]
-            dist.batch_isend_irecv([dist.P2POp(dist.irecv, bufs[i], i + 1) for i in range(world - 1)])
-        else:
-            for req in dist.batch_isend_irecv([dist.P2POp(dist.isend, o, 0)]):
-                req.wait()
+        gathered = gather_to_rank0(o, B * world)
         e1.record(stream)
         torch.cuda.synchronize()
         gt = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
         dist.all_reduce(gt, op=dist.ReduceOp.MAX)
         gbytes = o.numel() * o.element_size() * (world - 1)
         gather = {"ms": gt.item(), "bytes_to_rank0": gbytes, "GBps": gbytes / (gt.item() / 1e3) / 1e9,
-                  "how": "grouped ncclSend/ncclRecv of each shard's output to rank 0"}
+                  "how": "grouped ncclSend/ncclRecv of each shard's output to rank 0 (paper_2403_09195_b200.dist)"}
+        del gathered
 
     # ---- end-to-end through the C-ABI host entry point (pinned host buffers)
     e2e = run_e2e(args, dfa, cfg, q, k, v, o, stream, world, dist, dev) if not args.quick else None

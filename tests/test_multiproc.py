@@ -1,0 +1,63 @@
+"""Batch sharding + final gather with world_size 2 on gloo (CPU)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2403_09195_b200.dist import gather_to_rank0, shard_range, shard_sizes
+
+
+def test_shard_ranges_cover_exactly():
+    for total in (0, 1, 7, 64, 8192, 8193):
+        for world in (1, 2, 3, 4, 8):
+            seen = []
+            for r in range(world):
+                a, b = shard_range(total, r, world)
+                seen.extend(range(a, b))
+            assert seen == list(range(total))
+            sizes = shard_sizes(total, world)
+            assert max(sizes) - min(sizes) <= 1
+    assert shard_sizes(8192, 8) == [1024] * 8
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, total, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, b = shard_range(total, rank, world)
+    # stand-in for each rank's dfa_forward output: image index in every element
+    shard = torch.arange(a, b, dtype=torch.float32).view(-1, 1, 1).expand(-1, 3, 2).contiguous()
+    out = gather_to_rank0(shard, total)
+    if rank == 0:
+        q.put(out.numpy().tolist())
+    else:
+        assert out is None
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [8, 9, 64])
+def test_gather_world2_gloo(total):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, total, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    t = torch.tensor(got)
+    assert t.shape == (total, 3, 2)
+    assert torch.equal(t[:, 0, 0], torch.arange(total, dtype=torch.float32))
