@@ -134,6 +134,24 @@ dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int
  * not cover fail with DFA_ERR_UNSUPPORTED).  Process-wide. */
 void dfa_set_path_override(int32_t path);
 
+/* EXTENSION (no reference analogue; SPEC.md:204 lists multi-(w, r) as a
+ * non-goal): several (w, r) branches over the same q, k, v, combined row by
+ * row with weights e^{lse_b} (each branch's log-sum-exp), i.e. one softmax over
+ * the union of the branches' key sets.  `base` supplies N, h, d, d_v,
+ * scale_scores; branch b supplies (w_b, r_b, head_offsets_b).  Rows no branch
+ * selects are 0.  With one branch the output equals dfa_forward bit for bit.
+ * `workspace` (device) must hold dfa_multibranch_workspace_bytes bytes. */
+typedef struct {
+  int64_t segment_len;          /* w_b */
+  int64_t interval;             /* r_b */
+  const int64_t* head_offsets;  /* h offsets in [0, r_b) */
+} dfa_branch_t;
+dfa_status_t dfa_multibranch_workspace_bytes(const dfa_config_t* base, int32_t n_branches, dfa_dtype_t dtype,
+                                             int64_t batch, size_t* bytes);
+dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t n_branches, const dfa_branch_t* branches,
+                                     dfa_dtype_t dtype, int64_t batch, const void* q, const void* k, const void* v,
+                                     void* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Profiling hook: dfa_forward (bf16, tcgen05 path only) of a build of the
  * kernel that records a timeline of CTA 0 into `trace` (5 x 4096 uint64:
  * per role producer / MMA / softmax A / softmax B / epilogue, entries

@@ -44,6 +44,7 @@ __all__ = [
     "dilated_attention",
     "dfa_forward",
     "dfa_forward_host",
+    "dfa_forward_multibranch",
     "query_path",
     "fault_perturb",
     "last_launch_count",
@@ -343,6 +344,37 @@ def dfa_forward_host(q, k, v, out, cfg: AttentionConfig, ws: Workspace, dtype: s
     sp = _stream_ptr(stream) if stream is not None else None
     _check(lib.dfa_forward_host(ctypes.byref(c), code, B, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                 lse.data_ptr() if lse is not None else None, ws.handle, sp))
+    return out
+
+
+def dfa_forward_multibranch(q, k, v, cfg: AttentionConfig, branches, out=None, lse=None, stream=None,
+                            workspace=None):
+    """EXTENSION: LSE-weighted combine of several (w, r) branches (include/dfa.h).
+    `branches`: list of (w, r) or (w, r, head_offsets); offsets default to
+    j mod r.  cfg supplies N, h, d, scale_scores.  Returns o [B, N, h, d_v]."""
+    torch = _torch()
+    B, N, h, d = q.shape
+    dv = v.shape[3]
+    bs, keep = [], []
+    for br in branches:
+        w, r = br[0], br[1]
+        offs = list(br[2]) if len(br) > 2 else AttentionConfig.spread_offsets(h, r)
+        arr = (ctypes.c_int64 * h)(*offs)
+        keep.append(arr)
+        bs.append(_lib.DfaBranch(w, r, ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))))
+    barr = (_lib.DfaBranch * len(bs))(*bs)
+    c = cfg._c()
+    c.value_dim = dv
+    code = _dtype_code(q)
+    need = ctypes.c_size_t(0)
+    _check(lib.dfa_multibranch_workspace_bytes(ctypes.byref(c), len(bs), code, B, ctypes.byref(need)))
+    if workspace is None or workspace.numel() < need.value:
+        workspace = torch.empty(need.value, dtype=torch.uint8, device=q.device)
+    if out is None:
+        out = torch.empty((B, N, h, dv), dtype=q.dtype, device=q.device)
+    _check(lib.dfa_forward_multibranch(ctypes.byref(c), len(bs), barr, code, B, q.data_ptr(), k.data_ptr(),
+                                       v.data_ptr(), out.data_ptr(), lse.data_ptr() if lse is not None else None,
+                                       workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
     return out
 
 

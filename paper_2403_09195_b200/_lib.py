@@ -42,6 +42,8 @@ EXPORTED = (
     "dfa_workspace_bytes",
     "dfa_set_path_override",
     "dfa_forward_traced",
+    "dfa_multibranch_workspace_bytes",
+    "dfa_forward_multibranch",
     "dfa_last_launch_count",
     "dfa_version",
 )
@@ -61,6 +63,16 @@ class DfaConfig(ctypes.Structure):
         ("kernel", ctypes.c_int32),
         ("tile_size", ctypes.c_int64),
         ("scale_scores", ctypes.c_int32),
+    ]
+
+
+class DfaBranch(ctypes.Structure):
+    """Mirror of dfa_branch_t (include/dfa.h)."""
+
+    _fields_ = [
+        ("segment_len", ctypes.c_int64),
+        ("interval", ctypes.c_int64),
+        ("head_offsets", ctypes.POINTER(ctypes.c_int64)),
     ]
 
 
@@ -93,6 +105,9 @@ def _load() -> ctypes.CDLL:
         "dfa_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_i32, ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_set_path_override": (None, [c_i32]),
         "dfa_forward_traced": (c_i32, [p_cfg, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+        "dfa_multibranch_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i32, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
+        "dfa_forward_multibranch": (c_i32, [p_cfg, c_i32, ctypes.POINTER(DfaBranch), c_i32, c_i64, c_vp, c_vp, c_vp,
+                                            c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]),
         "dfa_last_launch_count": (c_i32, []),
         "dfa_version": (c_i32, []),
     }

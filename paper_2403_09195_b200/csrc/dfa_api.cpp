@@ -278,6 +278,57 @@ dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_
   return DFA_OK;
 }
 
+static size_t up256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+dfa_status_t dfa_multibranch_workspace_bytes(const dfa_config_t* base, int32_t nb, dfa_dtype_t dtype, int64_t batch,
+                                             size_t* bytes) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(base, batch, &g);
+  if (st != DFA_OK) return st;
+  if (nb < 1 || nb > dfa_impl::kMaxBranches)
+    return fail(DFA_ERR_CONFIG, "multibranch: need 1..%d branches, got %d", dfa_impl::kMaxBranches, (int)nb);
+  const size_t es = elem_size(dtype);
+  *bytes = (size_t)nb * (up256((size_t)(g.B * g.N * g.h * g.dv) * es) + up256((size_t)(g.B * g.h * g.N) * 4));
+  return DFA_OK;
+}
+
+dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t nb, const dfa_branch_t* branches,
+                                     dfa_dtype_t dtype, int64_t batch, const void* q, const void* k, const void* v,
+                                     void* o, float* lse, void* workspace, size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  dfa_status_t st = dfa_multibranch_workspace_bytes(base, nb, dtype, batch, &need);
+  if (st != DFA_OK) return st;
+  if (!branches) return fail(DFA_ERR_CONFIG, "multibranch: null branch list");
+  if (ws_bytes < need || !workspace)
+    return fail(DFA_ERR_DIMENSION, "multibranch: workspace has %zu bytes, needs %zu", ws_bytes, need);
+  if (batch == 0) return DFA_OK;
+  dfa_impl::Geometry g;
+  resolve(base, batch, &g);
+  const size_t es = elem_size(dtype);
+  const size_t ob = up256((size_t)(g.B * g.N * g.h * g.dv) * es), lb = up256((size_t)(g.B * g.h * g.N) * 4);
+  const void* outs[dfa_impl::kMaxBranches];
+  const float* lses[dfa_impl::kMaxBranches];
+  int launches = 0;
+  for (int b = 0; b < nb; ++b) {
+    dfa_config_t c = *base;
+    c.segment_len = branches[b].segment_len;
+    c.interval = branches[b].interval;
+    c.head_offsets = branches[b].head_offsets;
+    char* base_ptr = static_cast<char*>(workspace) + (size_t)b * (ob + lb);
+    st = dfa_forward(&c, dtype, batch, q, k, v, base_ptr, reinterpret_cast<float*>(base_ptr + ob), stream);
+    if (st != DFA_OK) return st;
+    launches += g_launches;
+    outs[b] = base_ptr;
+    lses[b] = reinterpret_cast<const float*>(base_ptr + ob);
+  }
+  cudaError_t err = cudaSuccess;
+  launches += dfa_impl::launch_combine(dtype, g.B, g.N, g.h, g.dv, nb, outs, lses, o, lse,
+                                       reinterpret_cast<cudaStream_t>(stream), &err);
+  if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "multibranch combine: %s", cudaGetErrorString(err));
+  g_launches = launches;
+  return DFA_OK;
+}
+
 dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t with_lse,
                                  size_t* bytes) {
   dfa_impl::Geometry g;

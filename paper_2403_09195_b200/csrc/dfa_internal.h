@@ -31,6 +31,11 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr);
 
+// LSE-weighted combine of nb <= 8 branch outputs (dfa_combine.cu).
+int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int nb, const void* const* o,
+                   const float* const* lse, void* out, float* lse_out, cudaStream_t stream, cudaError_t* err);
+constexpr int kMaxBranches = 8;
+
 // Fault hook (attention.hpp:272): out[0] += 1e-3.
 int launch_perturb(int dtype, void* o, cudaStream_t stream);
 

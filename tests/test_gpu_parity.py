@@ -289,3 +289,45 @@ def test_single_query_passes_value_through(dfa, cuda):
     o = dfa.dilated_attention(q, k, v, cfg, 1)
     assert torch.equal(o[1], v[1])
     assert (o[[0, 2, 3]] == 0).all()
+
+
+# ------------------------------------------- multi-(w, r) LSE combine (ext.)
+def test_multibranch_single_branch_is_dfa_forward(dfa, cuda):
+    """One branch: weights e^0 = 1, so the combine returns dfa_forward bit for bit."""
+    torch = _torch()
+    for dt in (torch.bfloat16, torch.float32):
+        q, k, v = (torch.randn((2, 1024, 2, 64), device="cuda", dtype=dt) for _ in range(3))
+        cfg = make_cfg(dfa, 1024, 256, 2, 2, 64)
+        a = dfa.dfa_forward(q, k, v, cfg)
+        b = dfa.dfa_forward_multibranch(q, k, v, cfg, [(256, 2)])
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), dt
+
+
+@pytest.mark.parametrize("branches", [
+    [(512, 1), (1024, 2), (2048, 4), (4096, 8)],  # LongNet-style geometric set (SURVEY §8d)
+    [(256, 2), (512, 2), (1024, 4)],
+])
+def test_multibranch_vs_oracle(dfa, port, cuda, branches):
+    """LSE-weighted combine vs the extension oracle (one dense softmax over the
+    multiset of keys the covering branches select); bf16 tolerances."""
+    torch = _torch()
+    B, n, h = 1, 4096, 2
+    q, k, v = (bf16_round(rand((B, n, h, 64), 70 + s)) for s in range(3))
+    cfg = make_cfg(dfa, n, branches[0][0], branches[0][1], h, 64)
+    qd, kd, vd = (to_dev(x, torch.bfloat16) for x in (q, k, v))
+    L = torch.empty((B, h, n), dtype=torch.float32, device="cuda")
+    o = dfa.dfa_forward_multibranch(qd, kd, vd, cfg, branches, lse=L)
+    torch.cuda.synchronize()
+    got = o.double().cpu().numpy()
+    Lg = L.cpu().numpy()
+    want = np.zeros_like(got)
+    for j in range(h):
+        brs = [(w, r, j % r) for w, r in branches]
+        ob, lb = port.multibranch(q[0, :, j], k[0, :, j], v[0, :, j], brs)
+        want[0, :, j] = ob
+        fin = np.isfinite(lb)
+        assert np.array_equal(np.isfinite(Lg[0, j]), fin)
+        assert np.abs(Lg[0, j][fin] - lb[fin]).max() <= 2e-3
+    mx, rel = errors(got, want)
+    assert mx <= BF16_MAX_ABS and rel <= BF16_MEAN_REL, (mx, rel)
