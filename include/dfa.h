@@ -159,6 +159,12 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t n_branche
 dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
                                 void* o, uint64_t* trace, void* stream);
 
+/* Debug hook: as dfa_forward_traced, plus a deadlock watchdog -- a barrier
+ * wait lasting ~2 s writes {site, thread, parity, barrier word} per CTA into
+ * `watchdog` (2 x gridDim uint64, host-mapped memory) and traps. */
+dfa_status_t dfa_forward_debug(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
+                               void* o, uint64_t* trace, unsigned long long* watchdog, void* stream);
+
 /* Number of device kernels the last dfa_forward on this thread launched
  * (evidence for bench.py's gpu_launches). */
 int32_t dfa_last_launch_count(void);

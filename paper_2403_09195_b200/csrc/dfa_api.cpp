@@ -170,7 +170,8 @@ dfa_status_t dfa_query_path(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t 
 }
 
 static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
-                                 const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace);
+                                 const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace,
+                                 unsigned long long* watchdog = nullptr);
 
 dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
                          const void* v, void* o, float* lse, void* stream) {
@@ -183,8 +184,15 @@ dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const vo
   return forward_impl(cfg, DFA_BF16, batch, q, k, v, o, nullptr, stream, trace);
 }
 
+dfa_status_t dfa_forward_debug(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
+                               void* o, uint64_t* trace, unsigned long long* watchdog, void* stream) {
+  if (!trace) return fail(DFA_ERR_DIMENSION, "dfa_forward_debug: null trace buffer");
+  return forward_impl(cfg, DFA_BF16, batch, q, k, v, o, nullptr, stream, trace, watchdog);
+}
+
 static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
-                                 const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace) {
+                                 const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace,
+                                 unsigned long long* watchdog) {
   g_launches = 0;
   dfa_impl::Geometry g;
   dfa_status_t st = resolve(cfg, batch, &g);
@@ -198,7 +206,7 @@ static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int
   int launches = 0;
   if (path == DFA_PATH_SM100_TCGEN05) {
     const char* why = "";
-    launches = dfa_impl::launch_sm100(g, q, k, v, o, lse, s, &err, &why, trace);
+    launches = dfa_impl::launch_sm100(g, q, k, v, o, lse, s, &err, &why, trace, watchdog);
     if (launches == 0 && err != cudaSuccess)
       return fail(DFA_ERR_CUDA, "dfa_forward: sm100 path: %s (%s)", why, cudaGetErrorString(err));
   } else if (trace) {

@@ -29,7 +29,8 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 // tcgen05/TMEM/TMA kernel (bf16 in/out, fp32 accumulate).  Returns launches.
 // trace: optional profiling buffer (5 x 4096 uint64 timeline events of CTA 0).
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
-                 cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr);
+                 cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr,
+                 unsigned long long* watchdog = nullptr);
 
 // LSE-weighted combine of nb <= 8 branch outputs (dfa_combine.cu).
 int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int nb, const void* const* o,

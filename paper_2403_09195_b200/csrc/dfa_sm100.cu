@@ -251,11 +251,37 @@ enum TraceEvent : uint64_t {
     }                                                                                             \
   } while (0)
 
+// Barrier wait; in the instrumented build (kTrace) a wait that lasts ~2 s
+// writes {site, thread, parity, raw barrier word} to the mapped-host
+// watchdog buffer and traps, so a protocol deadlock is diagnosable from host.
+template <bool kDbg>
+__device__ __forceinline__ void wait_site(uint64_t* bar, uint32_t parity, uint32_t site,
+                                          unsigned long long* wd) {
+  if constexpr (!kDbg) {
+    ptx::mbar_wait(bar, parity);
+  } else {
+    const long long t0 = clock64();
+    while (!ptx::mbar_try(bar, parity)) {
+      if (wd && clock64() - t0 > 4000000000LL) {
+        const unsigned long long raw = *reinterpret_cast<volatile unsigned long long*>(bar);
+        wd[2 * blockIdx.x + 1] = raw;
+        wd[2 * blockIdx.x] = (1ull << 63) | ((unsigned long long)site << 40) |
+                             ((unsigned long long)threadIdx.x << 16) | ((unsigned long long)ptx::smem_u32(bar) << 1) |
+                             parity;
+        __threadfence_system();
+        asm volatile("trap;");
+      }
+    }
+  }
+}
+#define DFA_WAIT(bar, parity, site) wait_site<kTrace>((bar), (parity), (site), watchdog)
+
 template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-                     float* __restrict__ lse, const __grid_constant__ Sm100Params p, uint64_t* __restrict__ trace) {
+                     float* __restrict__ lse, const __grid_constant__ Sm100Params p, uint64_t* __restrict__ trace,
+                     unsigned long long* __restrict__ watchdog) {
   extern __shared__ uint8_t smem_raw[];
   SmemLayout& sm =
       *reinterpret_cast<SmemLayout*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -316,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
         const Unit x = make_unit(p, u);
         const uint32_t qs = i % kQStages;
-        ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
+        DFA_WAIT(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1, 2);
         DFA_TRACE(0, TR_Q_ISSUE);
         ptx::mbar_arrive_expect_tx(&sm.q_full[qs], 2 * kTileBytes);
         ptx::tma_load_5d(sm.q[qs][0], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0, x.b, pol);
@@ -324,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
           const uint32_t st = g % kKVStages;
           DFA_TRACE(0, TR_KV_WAIT);
-          ptx::mbar_wait(&sm.k_empty[st], ((g / kKVStages) & 1) ^ 1);
+          DFA_WAIT(&sm.k_empty[st], ((g / kKVStages) & 1) ^ 1, 3);
           DFA_TRACE(0, TR_KV_ISSUE);
           ptx::mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
           ptx::tma_load_5d(sm.k[st], &tm_k, &sm.k_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
@@ -340,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Unit x = make_unit(p, u);
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
           const uint32_t st = g % kKVStages;
-          ptx::mbar_wait(&sm.v_empty[st], ((g / kKVStages) & 1) ^ 1);
+          DFA_WAIT(&sm.v_empty[st], ((g / kKVStages) & 1) ^ 1, 4);
           ptx::mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
           ptx::tma_load_5d(sm.v[st], &tm_v, &sm.v_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
         }
@@ -367,8 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Unit& x = c.x;
         const uint32_t qs = c.i & 1;
         DFA_TRACE(1, TR_QK_WAIT);
-        ptx::mbar_wait(&sm.q_full[qs], (c.i >> 1) & 1);
-        ptx::mbar_wait(&sm.k_full[c.gs], c.gpar);
+        DFA_WAIT(&sm.q_full[qs], (c.i >> 1) & 1, 5);
+        DFA_WAIT(&sm.k_full[c.gs], c.gpar, 6);
         ptx::tc_fence_after();
         const uint64_t qd = qdesc0 + (uint64_t)((qs * 2 + c.s) * (kTileBytes >> 4));
         const uint64_t kd = kdesc0 + (uint64_t)(c.gs * (kTileBytes >> 4));
@@ -413,11 +439,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = pv.s;
         const bool first = pv.kt == x.kt0(s);
         DFA_TRACE(1, TR_P_WAIT);
-        ptx::mbar_wait(&sm.p_full[b], (p_par >> b) & 1u);
+        DFA_WAIT(&sm.p_full[b], (p_par >> b) & 1u, 7);
         p_par ^= 1u << b;
         DFA_TRACE(1, TR_P_READY);
-        if (first) ptx::mbar_wait(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u);
-        ptx::mbar_wait(&sm.v_full[pv.gs], pv.gpar);
+        if (first) DFA_WAIT(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u, 8);
+        DFA_WAIT(&sm.v_full[pv.gs], pv.gpar, 9);
         ptx::tc_fence_after();
         const uint64_t vdesc = vdesc0 + (uint64_t)(pv.gs * (kTileBytes >> 4));
 #pragma unroll
@@ -472,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int32_t kt = kt_lo; kt < kt_hi; ++kt) {
       const uint32_t b = (uint32_t)(k_unit + step_in_unit(x, kt, s)) % kSBufs;
       DFA_TRACE(2 + s, TR_S_WAIT);
-      ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
+      DFA_WAIT(&sm.s_full[s][b], (use_par >> b) & 1u, 10);
       DFA_TRACE(2 + s, TR_S_READY);
       use_par ^= 1u << b;
       ptx::tc_fence_after();
@@ -511,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       bool waited = false;
       if (__any_sync(0xffffffffu, fix_o)) {
         if (steps > 0) {
-          ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
+          DFA_WAIT(&sm.pv_done[s], pvc & 1, 11);
           ++pvc;
           waited = true;
         }
@@ -564,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       DFA_TRACE(2 + s, TR_EXP_DONE);
       // keep the pv_done phases in lockstep with the steps
       if (!waited && steps > 0) {
-        ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
+        DFA_WAIT(&sm.pv_done[s], pvc & 1, 12);
         ++pvc;
       }
       ++steps;
@@ -601,9 +627,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t ph = (par >> s) & 1u;
         par ^= 1u << s;
         DFA_TRACE(4, TR_O_WAIT);
-        ptx::mbar_wait(&sm.o_full[s], ph);
+        DFA_WAIT(&sm.o_full[s], ph, 13);
         DFA_TRACE(4, TR_O_READY);
-        ptx::mbar_wait(&sm.stat_full[s], ph);
+        DFA_WAIT(&sm.stat_full[s], ph, 14);
         ptx::tc_fence_after();
         const float l = sm.stat_l[i & 1][s][row];
         const float mref = sm.stat_m[i & 1][s][row];
@@ -718,7 +744,8 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 }
 
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
-                 cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace) {
+                 cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace,
+                 unsigned long long* watchdog) {
   CUtensorMap mq, mk, mv, mo;
   if (!make_map(&mq, q, g.B, g.N, g.r, g.h) || !make_map(&mk, k, g.B, g.N, g.r, g.h) ||
       !make_map(&mv, v, g.B, g.N, g.r, g.h) || !make_map(&mo, o, g.B, g.N, g.r, g.h)) {
@@ -755,9 +782,9 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   }
   const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
   if (trace)
-    dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, trace);
+    dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, trace, watchdog);
   else
-    dfa_sm100_kernel<false><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, nullptr);
+    dfa_sm100_kernel<false><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, nullptr, nullptr);
   *err = cudaGetLastError();
   return 1;
 }
