@@ -96,8 +96,9 @@ struct __align__(1024) SmemLayout {
   uint64_t pv_done[2];         // MMA -> slot s: its latest P V completed
   uint64_t o_full[2], o_empty[2];
   uint64_t stat_full[2];       // slot -> epilogue: row stats of the finished unit written
-  float stat_l[2][2][kBM];     // [unit parity][slot][row] normaliser l
-  float stat_m[2][2][kBM];     // [unit parity][slot][row] reference max (raw score units), for lse
+  uint64_t stat_empty[2];      // epilogue -> slot: stats read (keeps stat_full <= 1 phase ahead)
+  float stat_l[2][2][kBM];     // [published parity][slot][row] normaliser l
+  float stat_m[2][2][kBM];     // [published parity][slot][row] reference max (raw score units), for lse
   Unit unit_ring[4];           // MMA issuer: geometry of the units its two cursors are in
   uint32_t tmem_base;
 };
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.o_full[s], 1);
       ptx::mbar_init(&sm.o_empty[s], kBM);
       ptx::mbar_init(&sm.stat_full[s], kBM);
+      ptx::mbar_init(&sm.stat_empty[s], kBM);
     }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tm_q);
@@ -477,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t use_par = 0;  // bit b: parity of the next s_full[s][b] phase
     uint32_t pvc = 0;      // pv_done phases consumed
     uint32_t steps = 0;    // steps of this slot so far
+    uint32_t published = 0;  // units whose row stats went to the epilogue
     float mref = -INFINITY, l = 0.0f;
     int32_t seg_lo = 0, seg_hi = 0;
     int32_t k_base = 0;  // CTA-global index of the unit's first step
@@ -599,12 +602,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_arrive(&sm.p_full[b]);
       DFA_TRACE(2 + s, TR_P_ARRIVE);
       }  // key tiles of the unit
-      // Hand the row statistics to the epilogue warpgroup (double-buffered by
-      // unit parity; the pv_done waits order this write after the epilogue's
-      // read of the same buffer two units ago).
-      sm.stat_l[i & 1][s][row] = l;
-      sm.stat_m[i & 1][s][row] = mref;
+      // Hand the row statistics to the epilogue warpgroup: double-buffered by
+      // the slot's published-unit count; publish unit n only after the
+      // epilogue consumed unit n-1, so stat_full is never two phases ahead
+      // of its parity waits (slots with one step per unit would otherwise
+      // outrun the epilogue -- scripts/protocol_model.py).
+      sm.stat_l[published & 1][s][row] = l;
+      sm.stat_m[published & 1][s][row] = mref;
+      if (published > 0) DFA_WAIT(&sm.stat_empty[s], (published - 1) & 1, 15);
       ptx::mbar_arrive(&sm.stat_full[s]);
+      ++published;
     }
   } else if (warp >= 12) {
     // ============================================================ epilogue
@@ -631,15 +638,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         DFA_TRACE(4, TR_O_READY);
         DFA_WAIT(&sm.stat_full[s], ph, 14);
         ptx::tc_fence_after();
-        const float l = sm.stat_l[i & 1][s][row];
-        const float mref = sm.stat_m[i & 1][s][row];
+        const float l = sm.stat_l[ph][s][row];
+        const float mref = sm.stat_m[ph][s][row];
         const uint32_t tO = tbase + lane_base + col_o(s);
         uint32_t orow[2][32];
         ptx::tmem_ld32(tO, orow[0]);
         ptx::tmem_ld32(tO + 32, orow[1]);
         ptx::tmem_ld_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&sm.o_empty[s]);  // O_s (and this stats buffer) may be reused
+        ptx::mbar_arrive(&sm.stat_empty[s]);  // stats buffer `ph` may be reused
+        ptx::mbar_arrive(&sm.o_empty[s]);     // O_s may be overwritten by the next unit
         const float inv = valid_q ? 1.0f / l : 0.0f;
         // the previous TMA store from this staging tile must have finished reading it
         if (leader) ptx::tma_store_wait_read<0>();

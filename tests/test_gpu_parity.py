@@ -331,3 +331,23 @@ def test_multibranch_vs_oracle(dfa, port, cuda, branches):
         assert np.abs(Lg[0, j][fin] - lb[fin]).max() <= 2e-3
     mx, rel = errors(got, want)
     assert mx <= BF16_MAX_ABS and rel <= BF16_MEAN_REL, (mx, rel)
+
+
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("w,r", [(256, 2), (256, 4), (256, 8), (512, 4), (512, 8), (1024, 8), (512, 2), (4096, 1)])
+def test_tcgen05_many_units_per_cta(dfa, cuda, w, r):
+    """B=64, h=6: ~20 work units per persistent CTA (the protocol's steady
+    state, incl. one-step-per-slot units when m <= 128) vs the SIMT kernel."""
+    torch = _torch()
+    from paper_2403_09195_b200 import _lib, path_override
+
+    g = torch.Generator(device="cuda").manual_seed(w + r)
+    q, k, v = (torch.randn((64, 4096, 6, 64), device="cuda", generator=g, dtype=torch.bfloat16) for _ in range(3))
+    cfg = make_cfg(dfa, 4096, w, r, 6, 64)
+    a = dfa.dfa_forward(q, k, v, cfg)
+    with path_override(_lib.DFA_PATH_SIMT):
+        b = dfa.dfa_forward(q, k, v, cfg)
+    torch.cuda.synchronize()
+    err = (a.float() - b.float()).abs()
+    assert err.max().item() <= BF16_MAX_ABS
+    assert (err.sum() / b.float().abs().sum()).item() <= BF16_MEAN_REL
