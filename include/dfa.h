@@ -153,8 +153,8 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t n_branche
                                      void* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Profiling hook: dfa_forward (bf16, tcgen05 path only) of a build of the
- * kernel that records a timeline of CTA 0 into `trace` (5 x 4096 uint64:
- * per role producer / MMA / softmax A / softmax B / epilogue, entries
+ * kernel that records a timeline of CTA 0 into `trace` (6 x 4096 uint64:
+ * per role producer / QK issuer / softmax A / softmax B / epilogue / PV issuer, entries
  * (event << 56) | clock64).  scripts/trace_timeline.py decodes it. */
 dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
                                 void* o, uint64_t* trace, void* stream);

@@ -171,7 +171,7 @@ dfa_status_t dfa_query_path(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t 
 
 static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
                                  const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace,
-                                 unsigned long long* watchdog = nullptr);
+                                 unsigned long long* watchdog = nullptr, bool apply_fault = true);
 
 dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
                          const void* v, void* o, float* lse, void* stream) {
@@ -192,7 +192,7 @@ dfa_status_t dfa_forward_debug(const dfa_config_t* cfg, int64_t batch, const voi
 
 static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
                                  const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace,
-                                 unsigned long long* watchdog) {
+                                 unsigned long long* watchdog, bool apply_fault) {
   g_launches = 0;
   dfa_impl::Geometry g;
   dfa_status_t st = resolve(cfg, batch, &g);
@@ -217,7 +217,7 @@ static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int
     return fail(DFA_ERR_UNSUPPORTED, "dfa_forward: forced tcgen05 path does not cover this call");
   }
   if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "dfa_forward: launch failed: %s", cudaGetErrorString(err));
-  if (g_fault.load()) {
+  if (apply_fault && g_fault.load()) {
     launches += dfa_impl::launch_perturb(dtype, o, s);
     err = cudaGetLastError();
     if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "dfa_forward: fault hook: %s", cudaGetErrorString(err));
@@ -309,30 +309,62 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t nb, const
   if (!branches) return fail(DFA_ERR_CONFIG, "multibranch: null branch list");
   if (ws_bytes < need || !workspace)
     return fail(DFA_ERR_DIMENSION, "multibranch: workspace has %zu bytes, needs %zu", ws_bytes, need);
+  g_launches = 0;
+  // validate every branch before launching anything
+  dfa_config_t cfgs[dfa_impl::kMaxBranches];
+  dfa_impl::Geometry gb[dfa_impl::kMaxBranches];
+  bool fused = dtype == DFA_BF16 && g_path_override.load() != DFA_PATH_SIMT;
+  for (int b = 0; b < nb; ++b) {
+    cfgs[b] = *base;
+    cfgs[b].segment_len = branches[b].segment_len;
+    cfgs[b].interval = branches[b].interval;
+    cfgs[b].head_offsets = branches[b].head_offsets;
+    st = resolve(&cfgs[b], batch, &gb[b]);
+    if (st != DFA_OK) return st;
+    fused = fused && dfa_impl::sm100_supported(gb[b], dtype, q, k, v, o);
+  }
   if (batch == 0) return DFA_OK;
-  dfa_impl::Geometry g;
-  resolve(base, batch, &g);
+  if (!q || !k || !v || !o) return fail(DFA_ERR_DIMENSION, "multibranch: null tensor pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const dfa_impl::Geometry& g = gb[0];
   const size_t es = elem_size(dtype);
   const size_t ob = up256((size_t)(g.B * g.N * g.h * g.dv) * es), lb = up256((size_t)(g.B * g.h * g.N) * 4);
-  const void* outs[dfa_impl::kMaxBranches];
-  const float* lses[dfa_impl::kMaxBranches];
-  int launches = 0;
-  for (int b = 0; b < nb; ++b) {
-    dfa_config_t c = *base;
-    c.segment_len = branches[b].segment_len;
-    c.interval = branches[b].interval;
-    c.head_offsets = branches[b].head_offsets;
-    char* base_ptr = static_cast<char*>(workspace) + (size_t)b * (ob + lb);
-    st = dfa_forward(&c, dtype, batch, q, k, v, base_ptr, reinterpret_cast<float*>(base_ptr + ob), stream);
-    if (st != DFA_OK) return st;
-    launches += g_launches;
-    outs[b] = base_ptr;
-    lses[b] = reinterpret_cast<const float*>(base_ptr + ob);
-  }
   cudaError_t err = cudaSuccess;
-  launches += dfa_impl::launch_combine(dtype, g.B, g.N, g.h, g.dv, nb, outs, lses, o, lse,
-                                       reinterpret_cast<cudaStream_t>(stream), &err);
-  if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "multibranch combine: %s", cudaGetErrorString(err));
+  int launches = 0;
+  if (fused) {
+    // Fused epilogue combine: branch 0 writes o (zero rows included) and the
+    // running lse; every later branch LSE-merges its kept rows into them in
+    // its epilogue.  Stream order separates the branches.
+    float* run_lse = lse ? lse : static_cast<float*>(workspace);
+    for (int b = 0; b < nb; ++b) {
+      const char* why = "";
+      const int n = dfa_impl::launch_sm100(gb[b], q, k, v, o, run_lse, s, &err, &why, nullptr, nullptr, b > 0);
+      if (n == 0 || err != cudaSuccess)
+        return fail(DFA_ERR_CUDA, "multibranch: branch %d: %s (%s)", b, why, cudaGetErrorString(err));
+      launches += n;
+    }
+  } else {
+    // General path (fp32 validation mode, SIMT geometries): every branch
+    // writes o_b and lse_b to the workspace, then one combine kernel.
+    const void* outs[dfa_impl::kMaxBranches];
+    const float* lses[dfa_impl::kMaxBranches];
+    for (int b = 0; b < nb; ++b) {
+      char* base_ptr = static_cast<char*>(workspace) + (size_t)b * (ob + lb);
+      st = forward_impl(&cfgs[b], dtype, batch, q, k, v, base_ptr, reinterpret_cast<float*>(base_ptr + ob), stream,
+                        nullptr, nullptr, false);
+      if (st != DFA_OK) return st;
+      launches += g_launches;
+      outs[b] = base_ptr;
+      lses[b] = reinterpret_cast<const float*>(base_ptr + ob);
+    }
+    launches += dfa_impl::launch_combine(dtype, g.B, g.N, g.h, g.dv, nb, outs, lses, o, lse, s, &err);
+    if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "multibranch combine: %s", cudaGetErrorString(err));
+  }
+  if (g_fault.load()) {
+    launches += dfa_impl::launch_perturb(dtype, o, s);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "multibranch: fault hook: %s", cudaGetErrorString(err));
+  }
   g_launches = launches;
   return DFA_OK;
 }

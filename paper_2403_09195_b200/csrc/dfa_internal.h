@@ -27,10 +27,13 @@ int launch_simt(const Geometry& g, int dtype, const void* q, const void* k, cons
 bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o);
 
 // tcgen05/TMEM/TMA kernel (bf16 in/out, fp32 accumulate).  Returns launches.
-// trace: optional profiling buffer (5 x 4096 uint64 timeline events of CTA 0).
+// trace: optional profiling buffer (6 x 4096 uint64 timeline events of CTA 0).
+// merge: multi-(w, r) branch merge -- o and lse hold the running result of
+// the earlier branches; the kept rows of this branch are LSE-combined into
+// them in the epilogue (no zero boxes; lse required).
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr,
-                 unsigned long long* watchdog = nullptr);
+                 unsigned long long* watchdog = nullptr, bool merge = false);
 
 // LSE-weighted combine of nb <= 8 branch outputs (dfa_combine.cu).
 int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int nb, const void* const* o,

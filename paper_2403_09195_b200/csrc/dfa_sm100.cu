@@ -25,18 +25,22 @@
 // ONCE per unit (for m >= 256 both tiles share them).  Keys outside a query's
 // own segment are masked (only when m is not a multiple of 128, or at tails).
 //
-// Warp roles (384 threads, one CTA per SM, persistent over units):
+// Warp roles (512 threads, one CTA per SM, persistent over units):
 //   warp 0      TMA producer: Q_A/Q_B (2-deep), K tiles (3-deep ring, a stage
 //               is freed as soon as its Q K^T completes)
 //   warp 3      TMA producer: V tiles (3-deep ring, freed after P V)
-//   warp 1      MMA issuer (one elected lane):
+//   warp 1      Q K^T issuer (one elected lane):
 //                 S_x = Q_x K^T   tcgen05.mma M=128 N=128 K=64 -> TMEM (fp32)
+//               into three rotating S buffers, up to three steps ahead
+//   warp 2      TMEM allocator (512 columns), then P V issuer:
 //                 O_x += P_x V    tcgen05.mma A = P_x from TMEM, B = V (MN-major)
-//               ping-ponging slot A and slot B so one softmax overlaps the
-//               other slot's MMAs
-//   warp 2      TMEM allocator (512 columns: S_A, S_B, O_A, O_B)
-//   warps 4-7   slot A softmax + epilogue (TMEM lanes 0-127, thread = row)
-//   warps 8-11  slot B softmax + epilogue
+//               Two issuing threads on different SMSPs halve the serial
+//               barrier-wait + issue latency per step (the single-issuer
+//               timeline showed it on the critical path); s_free orders the
+//               reuse of an S buffer after the P V that read it.
+//   warps 4-7   slot A softmax (TMEM lanes 0-127, thread = row)
+//   warps 8-11  slot B softmax
+//   warps 12-15 epilogue (O / l -> bf16 -> TMA store, zero boxes, lse)
 // Softmax: tcgen05.ld of the 128-score row, exp2 with the 1/sqrt(d)*log2(e)
 // fold, lazy (2^8 threshold) rescale of O in TMEM, P packed to bf16 and
 // tcgen05.st over the consumed S columns.  Epilogue: O/l -> bf16 -> 128B-
@@ -92,14 +96,15 @@ struct __align__(1024) SmemLayout {
   uint64_t k_full[kKVStages], k_empty[kKVStages];  // K ring: freed when its last Q K^T completes
   uint64_t v_full[kKVStages], v_empty[kKVStages];  // V ring: freed when its last P V completes
   uint64_t s_full[2][kSBufs];  // MMA -> slot s: S ready in buffer b
-  uint64_t p_full[kSBufs];     // slot -> MMA: P written in buffer b (128 arrivals)
+  uint64_t p_full[kSBufs];     // slot -> P V issuer: P written in buffer b (128 arrivals)
+  uint64_t s_free[kSBufs];     // P V issuer -> Q K^T issuer: P V of buffer b completed
   uint64_t pv_done[2];         // MMA -> slot s: its latest P V completed
   uint64_t o_full[2], o_empty[2];
   uint64_t stat_full[2];       // slot -> epilogue: row stats of the finished unit written
   uint64_t stat_empty[2];      // epilogue -> slot: stats read (keeps stat_full <= 1 phase ahead)
+  uint64_t oload_full[2];      // merge mode: running output rows landed in ostage[slot]
   float stat_l[2][2][kBM];     // [published parity][slot][row] normaliser l
   float stat_m[2][2][kBM];     // [published parity][slot][row] reference max (raw score units), for lse
-  Unit unit_ring[4];           // MMA issuer: geometry of the units its two cursors are in
   uint32_t tmem_base;
 };
 
@@ -131,6 +136,7 @@ struct Sm100Params {
   int32_t n_units;   // B * h * n_pairs
   float c;           // scale * log2(e)
   float scale;
+  int32_t merge;     // 1: merge into the running (o, lse) of earlier branches (no zero boxes)
   FastDiv div_pairs, div_h, div_m;
   int32_t offsets[kMaxHeads];
 };
@@ -184,65 +190,16 @@ __device__ __forceinline__ int32_t step_in_unit(const Unit& x, int32_t kt, int s
 }
 __device__ __forceinline__ int32_t steps_of_unit(const Unit& x) { return (x.kt1a - x.kt0a) + (x.kt1b - x.kt0b); }
 
-// Cursor over the step sequence for the single-thread MMA issuer.  The
-// cursor keeps its unit's geometry in registers; the look-ahead cursor
-// publishes each new unit into a 4-entry smem ring from which the lagging
-// cursor copies it once per unit (same thread: no synchronisation needed).
-struct Cursor {
-  Unit x;
-  int32_t u, i, kt, s, g;
-  uint32_t b;      // S buffer = step % 3
-  uint32_t gs;     // K/V stage = g % 3
-  uint32_t gpar;   // K/V full-barrier parity = (g / 3) & 1
-  bool valid;
-  __device__ __forceinline__ void step_counters(bool new_tile) {
-    b = (b == kSBufs - 1) ? 0 : b + 1;
-    if (new_tile) {
-      ++g;
-      if (++gs == kKVStages) {
-        gs = 0;
-        gpar ^= 1u;
-      }
-    }
-  }
-  __device__ __forceinline__ void advance(const Sm100Params& p, Unit* ring, bool writer) {
-    if (s == 0 && uses(x, 1, kt)) {
-      s = 1;
-      step_counters(false);
-      return;
-    }
-    ++kt;
-    if (kt < x.n_kv) {
-      s = uses(x, 0, kt) ? 0 : 1;
-      step_counters(true);
-      return;
-    }
-    u += gridDim.x;
-    ++i;
-    if (u >= p.n_units) {
-      valid = false;
-      return;
-    }
-    if (writer) {
-      x = make_unit(p, u);
-      ring[i & 3] = x;
-    } else {
-      x = ring[i & 3];
-    }
-    kt = 0;
-    s = 0;  // slot A always starts at key tile 0 of its unit
-    step_counters(true);
-  }
-};
-
 // Optional timeline trace (profiling builds of the same kernel, kTrace=true):
-// CTA 0 records (event << 56 | clock64) per role into trace[seg * kTraceCap].
+// CTA 0 records (event << 56 | clock64) per role into trace[seg * kTraceCap]
+// (seg: 0 producer, 1 Q K^T issuer, 2/3 softmax A/B, 4 epilogue, 5 P V issuer).
 constexpr int kTraceCap = 4096;
 enum TraceEvent : uint64_t {
   TR_Q_ISSUE = 1, TR_KV_WAIT, TR_KV_ISSUE,                          // producer  (seg 0)
   TR_P_WAIT, TR_P_READY, TR_PV_ISSUED, TR_QK_WAIT, TR_QK_ISSUED,    // MMA       (seg 1)
   TR_S_WAIT, TR_S_READY, TR_MAX_DONE, TR_EXP_DONE, TR_P_ARRIVE,     // softmax   (seg 2 = A, 3 = B)
-  TR_O_WAIT, TR_O_READY, TR_STORE_ISSUED                            // epilogue  (seg 4)
+  TR_O_WAIT, TR_O_READY, TR_STORE_ISSUED,                           // epilogue  (seg 4)
+  TR_QK_GOT, TR_PV_GOT, TR_Q_GOT                                    // MMA issuers: operands ready
 };
 #define DFA_TRACE(seg, ev)                                                                        \
   do {                                                                                            \
@@ -310,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.s_full[0][b], 1);
       ptx::mbar_init(&sm.s_full[1][b], 1);
       ptx::mbar_init(&sm.p_full[b], kBM);
+      ptx::mbar_init(&sm.s_free[b], 1);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&sm.pv_done[s], 1);
@@ -317,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.o_empty[s], kBM);
       ptx::mbar_init(&sm.stat_full[s], kBM);
       ptx::mbar_init(&sm.stat_empty[s], kBM);
+      ptx::mbar_init(&sm.oload_full[s], 1);
     }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tm_q);
@@ -332,8 +291,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tbase = sm.tmem_base;
 
   // Registers: 512 x 128 at launch; rebalanced per warpgroup to
-  // producer/MMA 80, softmax 2 x 176, epilogue 72 (sum 64512 <= 65536).
-  if (warp < 4) ptx::setmaxnreg_dec<80>();
+  // producer/MMA 72, softmax 2 x 176, epilogue 80 (sum 64512 <= 65536).
+  if (warp < 4) ptx::setmaxnreg_dec<72>();
   if (warp == 0) {
     // ============================================================ producer
     if (ptx::elect_one()) {
@@ -375,96 +334,116 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ========================================================== MMA issuer
+    // ======================================================= Q K^T issuer
+    // One elected lane.  Step k (CTA-global, unit-major order: key tiles
+    // ascending, slot A then slot B) writes S buffer k % 3; the buffer is
+    // free once P V of step k - 3 completed (s_free, committed by the P V
+    // issuer).  Q and K are waited for once per unit / key tile.
     if (ptx::elect_one()) {
       const bool tr_on = blockIdx.x == 0;
       uint32_t tr_n = 0;
       constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);  // K-major Q and K
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, kD, 0, 1);   // P from TMEM, V MN-major
-      // Q-stage bookkeeping: unit index owning each stage and QKs left on it.
-      int32_t qk_left0 = 0, qk_left1 = 0, qk_unit0 = -1, qk_unit1 = -1;
-      uint32_t oc_par = 0;  // bit s: parity of slot s's completed-unit count
-
       // Shared-memory descriptors of every operand tile, built once; a K step
-      // of 16 bf16 (32 B) advances the start-address field by 2, a 16-key
-      // step of V (16 rows x 128 B) by 128.
+      // of 16 bf16 (32 B) advances the start-address field by 2.
       const uint64_t qdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.q[0][0]));
       const uint64_t kdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.k[0]));
-      const uint64_t vdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.v[0]));
-      auto issue_qk = [&](const Cursor& c) {
-        const Unit& x = c.x;
-        const uint32_t qs = c.i & 1;
+      uint32_t b = 0;          // S buffer of the next step (step % 3)
+      uint32_t steps = 0;      // steps issued so far
+      uint32_t sfree_par = 0;  // bit b: parity of the next s_free[b] completion
+      uint32_t gs = 0, gpar = 0;  // K stage / its full-barrier parity
+      int32_t i = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
+        const Unit x = make_unit(p, u);
+        const uint32_t qs = i & 1;
         DFA_TRACE(1, TR_QK_WAIT);
-        DFA_WAIT(&sm.q_full[qs], (c.i >> 1) & 1, 5);
-        DFA_WAIT(&sm.k_full[c.gs], c.gpar, 6);
-        ptx::tc_fence_after();
-        const uint64_t qd = qdesc0 + (uint64_t)((qs * 2 + c.s) * (kTileBytes >> 4));
-        const uint64_t kd = kdesc0 + (uint64_t)(c.gs * (kTileBytes >> 4));
+        DFA_WAIT(&sm.q_full[qs], (i >> 1) & 1, 5);
+        DFA_TRACE(1, TR_Q_GOT);
+        for (int32_t kt = 0; kt < x.n_kv; ++kt) {
+          DFA_WAIT(&sm.k_full[gs], gpar, 6);
+          ptx::tc_fence_after();
+          DFA_TRACE(1, TR_QK_GOT);
+          const uint64_t kd = kdesc0 + (uint64_t)(gs * (kTileBytes >> 4));
+#pragma unroll 1
+          for (int sl = 0; sl < 2; ++sl) {
+            if (!uses(x, sl, kt)) continue;
+            if (steps >= (uint32_t)kSBufs) {
+              DFA_WAIT(&sm.s_free[b], (sfree_par >> b) & 1u, 16);
+              ptx::tc_fence_after();
+            }
+            sfree_par ^= (steps >= (uint32_t)kSBufs ? 1u : 0u) << b;
+            const uint64_t qd = qdesc0 + (uint64_t)((qs * 2 + sl) * (kTileBytes >> 4));
 #pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk)
-          ptx::mma_ss(tbase + col_s(c.b), qd + (uint64_t)(2 * kk), kd + (uint64_t)(2 * kk), idesc_qk, kk > 0);
-        ptx::tc_commit(&sm.s_full[c.s][c.b]);
-        if (c.s == 1 || !uses(x, 1, c.kt)) ptx::tc_commit(&sm.k_empty[c.gs]);  // last Q K^T of this K tile
-        DFA_TRACE(1, TR_QK_ISSUED);
-        int32_t& unit_ref = qs ? qk_unit1 : qk_unit0;
-        int32_t& left_ref = qs ? qk_left1 : qk_left0;
-        if (unit_ref != c.i) {
-          unit_ref = c.i;
-          left_ref = steps_of_unit(x);
+            for (int kk = 0; kk < kD / 16; ++kk)
+              ptx::mma_ss(tbase + col_s(b), qd + (uint64_t)(2 * kk), kd + (uint64_t)(2 * kk), idesc_qk, kk > 0);
+            ptx::tc_commit(&sm.s_full[sl][b]);
+            DFA_TRACE(1, TR_QK_ISSUED);
+            b = (b == kSBufs - 1) ? 0 : b + 1;
+            ++steps;
+          }
+          ptx::tc_commit(&sm.k_empty[gs]);  // every Q K^T of this K tile issued
+          if (++gs == kKVStages) {
+            gs = 0;
+            gpar ^= 1u;
+          }
         }
-        if (--left_ref == 0) ptx::tc_commit(&sm.q_empty[qs]);  // both Q tiles of the unit consumed
-      };
-
-      Cursor qk, pv;
-      qk.u = blockIdx.x;
-      qk.i = 0;
-      qk.kt = 0;
-      qk.s = 0;
-      qk.g = 0;
-      qk.b = 0;
-      qk.gs = 0;
-      qk.gpar = 0;
-      qk.valid = qk.u < p.n_units;
-      if (qk.valid) {
-        qk.x = make_unit(p, qk.u);
-        sm.unit_ring[0] = qk.x;
+        ptx::tc_commit(&sm.q_empty[qs]);  // both Q tiles of the unit consumed
       }
-      pv = qk;
-      uint32_t p_par = 0;  // bit b: parity of the next p_full[b] phase
-      for (int n = 0; n < kSBufs && qk.valid; ++n) {
-        issue_qk(qk);
-        qk.advance(p, sm.unit_ring, true);
-      }
-      while (pv.valid) {
-        const Unit& x = pv.x;
-        const uint32_t b = pv.b;
-        const int s = pv.s;
-        const bool first = pv.kt == x.kt0(s);
-        DFA_TRACE(1, TR_P_WAIT);
-        DFA_WAIT(&sm.p_full[b], (p_par >> b) & 1u, 7);
-        p_par ^= 1u << b;
-        DFA_TRACE(1, TR_P_READY);
-        if (first) DFA_WAIT(&sm.o_empty[s], ((oc_par >> s) & 1u) ^ 1u, 8);
-        DFA_WAIT(&sm.v_full[pv.gs], pv.gpar, 9);
-        ptx::tc_fence_after();
-        const uint64_t vdesc = vdesc0 + (uint64_t)(pv.gs * (kTileBytes >> 4));
+    }
+  } else if (warp == 2) {
+    // ========================================================= P V issuer
+    // Same step order.  O_s += P_s V with A = P from TMEM (bf16 over the S
+    // columns) and B = V as an MN-major smem operand; completion frees the S
+    // buffer (s_free), the V stage after the tile's last P V, and hands O_s
+    // to the epilogue after the slot's last step of the unit.
+    if (ptx::elect_one()) {
+      const bool tr_on = blockIdx.x == 0;
+      uint32_t tr_n = 0;
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, kD, 0, 1);  // P from TMEM, V MN-major
+      // a 16-key step of V (16 rows x 128 B) advances the start address by 128
+      const uint64_t vdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.v[0]));
+      uint32_t b = 0;
+      uint32_t p_par = 0;   // bit b: parity of the next p_full[b] phase
+      uint32_t oc_par = 0;  // bit s: parity of slot s's completed-unit count
+      uint32_t gs = 0, gpar = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+        const Unit x = make_unit(p, u);
+        for (int32_t kt = 0; kt < x.n_kv; ++kt) {
+          bool have_v = false;
+          const uint64_t vdesc = vdesc0 + (uint64_t)(gs * (kTileBytes >> 4));
+#pragma unroll 1
+          for (int sl = 0; sl < 2; ++sl) {
+            if (!uses(x, sl, kt)) continue;
+            const bool first = kt == x.kt0(sl);
+            DFA_TRACE(5, TR_P_WAIT);
+            DFA_WAIT(&sm.p_full[b], (p_par >> b) & 1u, 7);
+            p_par ^= 1u << b;
+            DFA_TRACE(5, TR_P_READY);
+            if (first) DFA_WAIT(&sm.o_empty[sl], ((oc_par >> sl) & 1u) ^ 1u, 8);
+            if (!have_v) {
+              DFA_WAIT(&sm.v_full[gs], gpar, 9);
+              have_v = true;
+            }
+            ptx::tc_fence_after();
+            DFA_TRACE(5, TR_PV_GOT);
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
-          ptx::mma_ts(tbase + col_o(s), tbase + col_s(b) + kk * 8, vdesc + (uint64_t)(kk * (2048 >> 4)), idesc_pv,
-                      (!first || kk > 0) ? 1u : 0u);
-        ptx::tc_commit(&sm.pv_done[s]);
-        DFA_TRACE(1, TR_PV_ISSUED);
-        if (pv.kt == x.kt1(s) - 1) {
-          ptx::tc_commit(&sm.o_full[s]);
-          oc_par ^= 1u << s;
+            for (int kk = 0; kk < kBN / 16; ++kk)
+              ptx::mma_ts(tbase + col_o(sl), tbase + col_s(b) + kk * 8, vdesc + (uint64_t)(kk * (2048 >> 4)),
+                          idesc_pv, (!first || kk > 0) ? 1u : 0u);
+            ptx::tc_commit(&sm.pv_done[sl]);
+            ptx::tc_commit(&sm.s_free[b]);
+            DFA_TRACE(5, TR_PV_ISSUED);
+            if (kt == x.kt1(sl) - 1) {
+              ptx::tc_commit(&sm.o_full[sl]);
+              oc_par ^= 1u << sl;
+            }
+            b = (b == kSBufs - 1) ? 0 : b + 1;
+          }
+          ptx::tc_commit(&sm.v_empty[gs]);  // every P V of this V tile issued
+          if (++gs == kKVStages) {
+            gs = 0;
+            gpar ^= 1u;
+          }
         }
-        if (s == 1 || !uses(x, 1, pv.kt)) ptx::tc_commit(&sm.v_empty[pv.gs]);
-        // S buffer b is free once this P V has read it (in-order execution).
-        if (qk.valid) {
-          issue_qk(qk);
-          qk.advance(p, sm.unit_ring, true);
-        }
-        pv.advance(p, sm.unit_ring, false);
       }
     }
   } else if (warp >= 4 && warp < 12) {
@@ -615,13 +594,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 12) {
     // ============================================================ epilogue
-    ptx::setmaxnreg_dec<72>();
+    ptx::setmaxnreg_dec<80>();
     const uint32_t row = (warp % 4) * 32 + lane;
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const bool leader = warp == 12 && lane == 0;
     const bool tr_on = blockIdx.x == 0 && leader;
     uint32_t tr_n = 0;
-    uint32_t par = 0;  // bit s: parity of slot s's completed-unit count
+    uint32_t par = 0;     // bit s: parity of slot s's completed-unit count
+    uint32_t ld_par = 0;  // bit s: parity of oload_full[s] (merge mode)
+    const uint64_t pol_merge = ptx::policy_evict_first();
     int32_t i = 0;
     for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++i) {
       const Unit x = make_unit(p, u);
@@ -633,6 +614,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool valid_q = tq < p.T;
         const uint32_t ph = (par >> s) & 1u;
         par ^= 1u << s;
+        // Branch merge (multi-(w, r) LSE combine): fetch the running output
+        // rows (a TMA box of the previous branches' result) into this slot's
+        // staging tile and the running lse, both before the O wait so their
+        // latency hides behind it.
+        float lse_prev = -INFINITY;
+        float* lrow = nullptr;
+        if (lse && valid_q) lrow = lse + ((int64_t)x.b * p.h + x.j) * p.N + (int64_t)tq * p.r;
+        if (p.merge) {
+          if (leader) {
+            ptx::tma_store_wait_read<0>();  // staging no longer read by an earlier store
+            ptx::mbar_arrive_expect_tx(&sm.oload_full[s], kTileBytes);
+            ptx::tma_load_5d(sm.ostage[s], &tm_o, &sm.oload_full[s], 0, x.j, x.gamma, ts0, x.b, pol_merge);
+          }
+          if (lrow) lse_prev = lrow[x.gamma];
+        }
         DFA_TRACE(4, TR_O_WAIT);
         DFA_WAIT(&sm.o_full[s], ph, 13);
         DFA_TRACE(4, TR_O_READY);
@@ -648,33 +644,60 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&sm.stat_empty[s]);  // stats buffer `ph` may be reused
         ptx::mbar_arrive(&sm.o_empty[s]);     // O_s may be overwritten by the next unit
-        const float inv = valid_q ? 1.0f / l : 0.0f;
-        // the previous TMA store from this staging tile must have finished reading it
-        if (leader) ptx::tma_store_wait_read<0>();
-        ptx::named_bar_sync(1, kBM);
+        const float lse_new = mref * p.scale + __logf(l);
         const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
-        // 128B-swizzled staging row: 16B chunk c of row r at ((c ^ (r & 7)) * 16)
+        if (!p.merge) {
+          const float inv = valid_q ? 1.0f / l : 0.0f;
+          // the previous TMA store from this staging tile must have finished reading it
+          if (leader) ptx::tma_store_wait_read<0>();
+          ptx::named_bar_sync(1, kBM);
+          // 128B-swizzled staging row: 16B chunk c of row r at ((c ^ (r & 7)) * 16)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float* f = reinterpret_cast<const float*>(&orow[c >> 2][(c & 3) * 8]);
-          const uint32_t addr = stage_addr + row * 128 + ((c ^ (row & 7)) * 16);
-          ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0] * inv, f[1] * inv),
-                            ptx::pack_bf16x2(f[2] * inv, f[3] * inv), ptx::pack_bf16x2(f[4] * inv, f[5] * inv),
-                            ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
+          for (int c = 0; c < 8; ++c) {
+            const float* f = reinterpret_cast<const float*>(&orow[c >> 2][(c & 3) * 8]);
+            const uint32_t addr = stage_addr + row * 128 + ((c ^ (row & 7)) * 16);
+            ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0] * inv, f[1] * inv),
+                              ptx::pack_bf16x2(f[2] * inv, f[3] * inv), ptx::pack_bf16x2(f[4] * inv, f[5] * inv),
+                              ptx::pack_bf16x2(f[6] * inv, f[7] * inv));
+          }
+          if (lrow)
+            for (int32_t gz = 0; gz < p.r; ++gz) lrow[gz] = (gz == x.gamma) ? lse_new : -INFINITY;
+        } else {
+          // O = (e^{lse_prev} O_prev + e^{lse_new} O_new) / (e^{lse_prev} + e^{lse_new}), max-subtracted;
+          // rows outside the tensor (valid_q false) are dropped by the store.
+          const float mx = fmaxf(lse_prev, lse_new);
+          const float wp = __expf(lse_prev - mx), wn = __expf(lse_new - mx);
+          const float den = wp + wn;
+          const float a = valid_q ? wp / den : 0.0f;
+          const float cn = valid_q ? wn / (den * l) : 0.0f;
+          DFA_WAIT(&sm.oload_full[s], (ld_par >> s) & 1u, 17);
+          ld_par ^= 1u << s;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float* f = reinterpret_cast<const float*>(&orow[c >> 2][(c & 3) * 8]);
+            const uint32_t addr = stage_addr + row * 128 + ((c ^ (row & 7)) * 16);
+            uint32_t prev[4];
+            ptx::ld_shared_v4(addr, prev);
+            uint32_t outp[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 pv = ptx::unpack_bf16x2(prev[e]);
+              outp[e] = ptx::pack_bf16x2(fmaf(a, pv.x, cn * f[2 * e]), fmaf(a, pv.y, cn * f[2 * e + 1]));
+            }
+            ptx::st_shared_v4(addr, outp[0], outp[1], outp[2], outp[3]);
+          }
+          if (lrow) lrow[x.gamma] = mx + __logf(den);
         }
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, kBM);
         if (leader) {
           ptx::tma_store_5d(&tm_o, sm.ostage[s], 0, x.j, x.gamma, ts0, x.b);
-          for (int32_t gz = 0; gz < p.r; ++gz)
-            if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
+          if (!p.merge)
+            for (int32_t gz = 0; gz < p.r; ++gz)
+              if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
           ptx::tma_store_commit();
         }
         DFA_TRACE(4, TR_STORE_ISSUED);
-        if (lse && valid_q) {
-          float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N + (int64_t)tq * p.r;
-          for (int32_t gz = 0; gz < p.r; ++gz) lb[gz] = (gz == x.gamma) ? mref * p.scale + logf(l) : -INFINITY;
-        }
       }
     }
     if (leader) ptx::tma_store_wait_all<0>();
@@ -753,7 +776,12 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace,
-                 unsigned long long* watchdog) {
+                 unsigned long long* watchdog, bool merge) {
+  if (merge && !lse) {
+    *why = "merge mode needs the running lse buffer";
+    *err = cudaErrorInvalidValue;
+    return 0;
+  }
   CUtensorMap mq, mk, mv, mo;
   if (!make_map(&mq, q, g.B, g.N, g.r, g.h) || !make_map(&mk, k, g.B, g.N, g.r, g.h) ||
       !make_map(&mv, v, g.B, g.N, g.r, g.h) || !make_map(&mo, o, g.B, g.N, g.r, g.h)) {
@@ -771,6 +799,7 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.n_units = (int32_t)(g.B * g.h * p.n_pairs);
   p.scale = g.scale;
   p.c = g.scale * kLog2e;
+  p.merge = merge ? 1 : 0;
   p.div_pairs = make_fastdiv((uint32_t)p.n_pairs);
   p.div_h = make_fastdiv((uint32_t)p.h);
   p.div_m = make_fastdiv((uint32_t)p.m);

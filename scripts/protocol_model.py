@@ -123,44 +123,56 @@ def step_list(p, cta):
     return out
 
 
-def mma(p, B, cta):
-    steps = step_list(p, cta)
-    qk_left = {}
-    oc = [0, 0]
-
-    def issue_qk(k):
-        i, x, kt, s, g = steps[k]
+def qk_issuer(p, B, cta):
+    """warp 1: Q K^T for step k into S buffer k % 3 once P V of step k - 3 completed."""
+    steps = 0
+    g = 0
+    for i, u in enumerate(units(p, cta)):
+        x = make_unit(p, u)
         qs = i & 1
         yield ("wait", B["q_full"][qs], (i >> 1) + 1)
-        yield ("wait", B["k_full"][g % KKV], g // KKV + 1)
-        B["s_full"][s][k % KSB].arrive()
-        if s == 1 or not uses(x, 1, kt):
+        for kt in range(x["n_kv"]):
+            yield ("wait", B["k_full"][g % KKV], g // KKV + 1)
+            for s in range(2):
+                if not uses(x, s, kt):
+                    continue
+                b = steps % KSB
+                if steps >= KSB:
+                    yield ("wait", B["s_free"][b], steps // KSB)
+                B["s_full"][s][b].arrive()
+                steps += 1
             B["k_empty"][g % KKV].arrive()
-        if qk_left.get(qs, (None,))[0] != i:
-            qk_left[qs] = [i, steps_of(x)]
-        qk_left[qs][1] -= 1
-        if qk_left[qs][1] == 0:
-            B["q_empty"][qs].arrive()
+            g += 1
+        B["q_empty"][qs].arrive()
 
-    nq = 0
-    for _ in range(min(KSB, len(steps))):
-        yield from issue_qk(nq)
-        nq += 1
-    for k, (i, x, kt, s, g) in enumerate(steps):
-        yield ("wait", B["p_full"][k % KSB], k // KSB + 1)
-        first = kt == x["kt"][s][0]
-        if first:
-            yield ("wait", B["o_empty"][s], oc[s])
-        yield ("wait", B["v_full"][g % KKV], g // KKV + 1)
-        B["pv_done"][s].arrive()
-        if kt == x["kt"][s][1] - 1:
-            B["o_full"][s].arrive()
-            oc[s] += 1
-        if s == 1 or not uses(x, 1, kt):
+
+def pv_issuer(p, B, cta):
+    """warp 2: P V for step k after P(k); frees S buffer k % 3 (s_free)."""
+    steps = 0
+    g = 0
+    oc = [0, 0]
+    for i, u in enumerate(units(p, cta)):
+        x = make_unit(p, u)
+        for kt in range(x["n_kv"]):
+            have_v = False
+            for s in range(2):
+                if not uses(x, s, kt):
+                    continue
+                b = steps % KSB
+                yield ("wait", B["p_full"][b], steps // KSB + 1)
+                if kt == x["kt"][s][0]:
+                    yield ("wait", B["o_empty"][s], oc[s])
+                if not have_v:
+                    yield ("wait", B["v_full"][g % KKV], g // KKV + 1)
+                    have_v = True
+                B["pv_done"][s].arrive()
+                B["s_free"][b].arrive()
+                if kt == x["kt"][s][1] - 1:
+                    B["o_full"][s].arrive()
+                    oc[s] += 1
+                steps += 1
             B["v_empty"][g % KKV].arrive()
-        if nq < len(steps):
-            yield from issue_qk(nq)
-            nq += 1
+            g += 1
 
 
 def softmax(p, B, cta, s):
@@ -211,11 +223,12 @@ def run(p, cta, seed=0):
              k_full=[Bar(f"k_full{i}", 1) for i in range(KKV)], k_empty=[Bar(f"k_empty{i}", 1) for i in range(KKV)],
              v_full=[Bar(f"v_full{i}", 1) for i in range(KKV)], v_empty=[Bar(f"v_empty{i}", 1) for i in range(KKV)],
              s_full=[[Bar(f"s_full{s}{b}", 1) for b in range(KSB)] for s in range(2)],
-             p_full=[Bar(f"p_full{b}", KBM) for b in range(KSB)], pv_done=[Bar(f"pv_done{s}", 1) for s in range(2)],
+             p_full=[Bar(f"p_full{b}", KBM) for b in range(KSB)],
+             s_free=[Bar(f"s_free{b}", 1) for b in range(KSB)], pv_done=[Bar(f"pv_done{s}", 1) for s in range(2)],
              o_full=[Bar(f"o_full{s}", 1) for s in range(2)], o_empty=[Bar(f"o_empty{s}", KBM) for s in range(2)],
              stat_full=[Bar(f"stat_full{s}", KBM) for s in range(2)],
              stat_empty=[Bar(f"stat_empty{s}", KBM) for s in range(2)])
-    roles = {"producer_qk": producer_qk(p, B, cta), "producer_v": producer_v(p, B, cta), "mma": mma(p, B, cta),
+    roles = {"producer_qk": producer_qk(p, B, cta), "producer_v": producer_v(p, B, cta), "qk_issuer": qk_issuer(p, B, cta), "pv_issuer": pv_issuer(p, B, cta),
              "softmax_A": softmax(p, B, cta, 0), "softmax_B": softmax(p, B, cta, 1), "epilogue": epilogue(p, B, cta)}
     import random
 

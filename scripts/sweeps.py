@@ -125,19 +125,26 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweeps.json"))
     ap.add_argument("--ncu", action="store_true")
+    ap.add_argument("--only", choices=["config1", "config3", "config4"], default=None)
     a = ap.parse_args()
     if a.ncu:
         config4(ncu=True)
         return
-    res = {"gpu": torch.cuda.get_device_name(0), "config1": config1(), "config4": config4(), "config3": config3()}
+    fns = {"config1": config1, "config4": config4, "config3": config3}
+    res = {"gpu": torch.cuda.get_device_name(0)}
+    for name, fn in fns.items():
+        if a.only in (None, name):
+            res[name] = fn()
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     json.dump(res, open(a.out, "w"), indent=1)
-    print(json.dumps(res["config1"]))
-    for r in res["config4"]["rows"]:
+    if "config1" in res:
+        print(json.dumps(res["config1"]))
+    for r in res.get("config4", {}).get("rows", []):
         print(f"w={r['w']:5d} r={r['r']} {r['ms']:.3f} ms {r['tflops']:7.1f} TF {r['GBps']:7.0f} GB/s "
               f"{r['frac_of_attainable']:.2f} of attainable ({r['bound']})")
-    print("combined", res["config4"]["lse_combined_set"])
-    for r in res["config3"]["rows"]:
+    if "config4" in res:
+        print("combined", res["config4"]["lse_combined_set"])
+    for r in res.get("config3", {}).get("rows", []):
         print(f"B={r['B']:4d} {r['ms_6_layers']:.3f} ms/6 layers {r['images_per_s']:9.0f} images/s {r['tflops']:.0f} TF")
 
 

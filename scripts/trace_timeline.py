@@ -16,8 +16,8 @@ sys.path.insert(0, ROOT)
 CAP = 4096
 NAMES = {1: "Q_ISSUE", 2: "KV_WAIT", 3: "KV_ISSUE", 4: "P_WAIT", 5: "P_READY", 6: "PV_ISSUED", 7: "QK_WAIT",
          8: "QK_ISSUED", 9: "S_WAIT", 10: "S_READY", 11: "MAX_DONE", 12: "EXP_DONE", 13: "P_ARRIVE", 14: "O_WAIT",
-         15: "O_READY", 16: "STORE_ISSUED"}
-ROLES = ["producer", "mma", "softmax_A", "softmax_B", "epilogue"]
+         15: "O_READY", 16: "STORE_ISSUED", 17: "QK_GOT", 18: "PV_GOT", 19: "Q_GOT"}
+ROLES = ["producer", "mma", "softmax_A", "softmax_B", "epilogue", "pv"]
 
 
 def run(args):
@@ -31,7 +31,7 @@ def run(args):
     cfg = dfa.AttentionConfig(4096, args.w, args.r, h, 64, offs)
     q, k, v = (torch.randn((args.batch, 4096, h, 64), device="cuda", dtype=torch.bfloat16) for _ in range(3))
     o = torch.empty_like(q)
-    tr = torch.zeros(5 * CAP, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(6 * CAP, dtype=torch.int64, device="cuda")
     c = cfg._c()
     for _ in range(3):  # warm (clocks, L2 state)
         dfa.dfa_forward(q, k, v, cfg, out=o)
@@ -82,11 +82,12 @@ def show(path):
         print(f"{role}: {n} steps; per step mean: wait-S {sw.mean():.0f}, ld+max {mx.mean():.0f}, "
               f"exp {ex.mean():.0f}, tail {pa.mean():.0f}, between {gap.mean():.0f}; busy {busy / end:.1%} "
               f"(wait-S total {sw.sum() / end:.1%})")
-    m = ev["mma"]
-    pw = spans(m, "P_WAIT", "P_READY")
-    qw = spans(m, "QK_WAIT", "QK_ISSUED")
-    print(f"mma: p-wait mean {pw.mean():.0f} (total {pw.sum() / end:.1%}), qk wait+issue mean {qw.mean():.0f} "
-          f"(total {qw.sum() / end:.1%})")
+    m, pv = ev["mma"], ev["pv"]
+    print(f"qk issuer: q_full wait {spans(m, 'QK_WAIT', 'Q_GOT').mean():.0f} per unit, "
+          f"k_full wait {spans(m, 'Q_GOT', 'QK_GOT').mean():.0f}, issue gaps {np.diff([t for n, t in m if n == 'QK_ISSUED']).mean():.0f}")
+    pw = spans(pv, "P_WAIT", "P_READY")
+    print(f"pv issuer: p-wait mean {pw.mean():.0f} (total {pw.sum() / end:.1%}), operands {spans(pv, 'P_READY', 'PV_GOT').mean():.0f}, "
+          f"issue {spans(pv, 'PV_GOT', 'PV_ISSUED').mean():.0f}")
     pr = ev["producer"]
     kw = spans(pr, "KV_WAIT", "KV_ISSUE")
     print(f"producer: kv-empty wait mean {kw.mean():.0f} (total {kw.sum() / end:.1%})")
@@ -96,7 +97,7 @@ def show(path):
     print(f"epilogue: o-full wait mean {ow.mean():.0f} (total {ow.sum() / end:.1%}), "
           f"readout+store mean {st.mean():.0f}")
     # first few steps in detail
-    for role in ("mma", "softmax_A", "softmax_B"):
+    for role in ("mma", "pv", "softmax_A", "softmax_B"):
         print(role, " ".join(f"{n}@{t}" for n, t in ev[role][:24]))
 
 

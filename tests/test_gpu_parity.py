@@ -351,3 +351,54 @@ def test_tcgen05_many_units_per_cta(dfa, cuda, w, r):
     err = (a.float() - b.float()).abs()
     assert err.max().item() <= BF16_MAX_ABS
     assert (err.sum() / b.float().abs().sum()).item() <= BF16_MEAN_REL
+
+
+@pytest.mark.parametrize("branches", [
+    [(512, 1), (1024, 2), (2048, 4), (4096, 8)],
+    [(4096, 8), (256, 4), (512, 1)],  # sparse first branch: later merges land on zero rows
+    [(256, 2), (256, 2)],             # duplicate branch: weights 1/2 each, o unchanged
+])
+def test_multibranch_fused_epilogue_matches_unfused(dfa, cuda, branches):
+    """bf16 fused path (branch 0 writes o + running lse, later branches merge in
+    their epilogue: one launch per branch, no combine kernel) vs the unfused
+    path (per-branch o_b/lse_b + combine kernel, forced via the SIMT override)."""
+    torch = _torch()
+    from paper_2403_09195_b200 import _lib, path_override
+
+    g = torch.Generator(device="cuda").manual_seed(len(branches))
+    B, n, h = 4, 4096, 6
+    q, k, v = (torch.randn((B, n, h, 64), device="cuda", generator=g, dtype=torch.bfloat16) for _ in range(3))
+    cfg = make_cfg(dfa, n, 512, 1, h, 64)
+    L1 = torch.empty((B, h, n), dtype=torch.float32, device="cuda")
+    a = dfa.dfa_forward_multibranch(q, k, v, cfg, branches, lse=L1)
+    assert dfa.last_launch_count() == len(branches)
+    L2 = torch.empty_like(L1)
+    with path_override(_lib.DFA_PATH_SIMT):
+        b = dfa.dfa_forward_multibranch(q, k, v, cfg, branches, lse=L2)
+    torch.cuda.synchronize()
+    err = (a.float() - b.float()).abs()
+    assert err.max().item() <= BF16_MAX_ABS
+    assert (err.sum() / b.float().abs().sum()).item() <= BF16_MEAN_REL
+    fin = torch.isfinite(L2)
+    assert torch.equal(torch.isfinite(L1), fin)
+    assert (L1[fin] - L2[fin]).abs().max().item() <= 2e-3
+    # rows no branch selects are exactly zero
+    assert (a.float()[~fin.permute(0, 2, 1)] == 0).all()
+    if branches[0] == branches[1]:
+        c = dfa.dfa_forward(q, k, v, make_cfg(dfa, n, 256, 2, h, 64))
+        assert (a.float() - c.float()).abs().max().item() <= 1e-2
+
+
+def test_multibranch_fault_hook_once(dfa, cuda):
+    """The recompose fault hook perturbs the combined output once."""
+    torch = _torch()
+    q, k, v = (torch.randn((1, 1024, 2, 64), device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    cfg = make_cfg(dfa, 1024, 256, 2, 2, 64)
+    br = [(256, 2), (512, 4)]
+    a = dfa.dfa_forward_multibranch(q, k, v, cfg, br)
+    with dfa.fault_perturb():
+        b = dfa.dfa_forward_multibranch(q, k, v, cfg, br)
+    torch.cuda.synchronize()
+    d = (b.float() - a.float()).flatten()
+    assert d[1:].abs().max().item() == 0.0
+    assert abs(d[0].item() - 1e-3) <= 8e-3  # bf16 rounding of o[0] + 1e-3
