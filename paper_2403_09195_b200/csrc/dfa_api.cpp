@@ -2,6 +2,7 @@
 // messages, geometry resolution, device-path dispatch, host-buffer entry
 // points and the fault hook.  No CPU compute path exists: every forward is a
 // device kernel (tcgen05 for bf16/d=64 geometries, SIMT otherwise).
+#include <algorithm>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -101,9 +102,15 @@ size_t elem_size(dfa_dtype_t t) { return t == DFA_F32 ? 4 : 2; }
 
 }  // namespace
 
+// Device staging for the host-buffer entry points, plus the copy streams and
+// events of the chunked H2D -> kernel -> D2H pipeline (created on first use).
+constexpr int kHostChunks = 8;
 struct dfa_workspace {
   void* dev = nullptr;
   size_t bytes = 0;
+  bool pipe = false;
+  cudaStream_t in_s = nullptr, out_s = nullptr;
+  cudaEvent_t start = nullptr, in_done[kHostChunks] = {}, fwd_done[kHostChunks] = {};
 };
 
 extern "C" {
@@ -243,6 +250,17 @@ dfa_status_t dfa_workspace_create(size_t bytes, dfa_workspace_t** ws) {
 
 dfa_status_t dfa_workspace_destroy(dfa_workspace_t* ws) {
   if (!ws) return DFA_OK;
+  if (ws->pipe) {
+    cudaStreamSynchronize(ws->in_s);
+    cudaStreamSynchronize(ws->out_s);
+    cudaEventDestroy(ws->start);
+    for (int c = 0; c < kHostChunks; ++c) {
+      cudaEventDestroy(ws->in_done[c]);
+      cudaEventDestroy(ws->fwd_done[c]);
+    }
+    cudaStreamDestroy(ws->in_s);
+    cudaStreamDestroy(ws->out_s);
+  }
   if (ws->dev) cudaFree(ws->dev);
   delete ws;
   return DFA_OK;
@@ -265,24 +283,60 @@ dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_
   if (ws->bytes < need)
     return fail(DFA_ERR_DIMENSION, "dfa_forward_host: workspace has %zu bytes, needs %zu", ws->bytes, need);
   char* base = static_cast<char*>(ws->dev);
-  void* dq = base;
-  void* dk = base + up(bqk);
-  void* dv = base + 2 * up(bqk);
-  void* dout = base + 2 * up(bqk) + up(bv);
+  char* dq = base;
+  char* dk = base + up(bqk);
+  char* dv = base + 2 * up(bqk);
+  char* dout = base + 2 * up(bqk) + up(bv);
   float* dl = lse ? reinterpret_cast<float*>(base + 2 * up(bqk) + 2 * up(bv)) : nullptr;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaError_t err;
-  if ((err = cudaMemcpyAsync(dq, q, bqk, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-      (err = cudaMemcpyAsync(dk, k, bqk, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
-      (err = cudaMemcpyAsync(dv, v, bv, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-    return fail(DFA_ERR_CUDA, "dfa_forward_host: H2D: %s", cudaGetErrorString(err));
-  st = dfa_forward(cfg, dtype, batch, dq, dk, dv, dout, dl, stream);
-  if (st != DFA_OK) return st;
-  if ((err = cudaMemcpyAsync(o, dout, bv, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-      (lse && (err = cudaMemcpyAsync(lse, dl, bl, cudaMemcpyDeviceToHost, s)) != cudaSuccess))
-    return fail(DFA_ERR_CUDA, "dfa_forward_host: D2H: %s", cudaGetErrorString(err));
-  if ((err = cudaStreamSynchronize(s)) != cudaSuccess)
+  cudaError_t err = cudaSuccess;
+  if (!ws->pipe) {
+    bool ok = cudaStreamCreateWithFlags(&ws->in_s, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&ws->out_s, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ws->start, cudaEventDisableTiming) == cudaSuccess;
+    for (int c = 0; ok && c < kHostChunks; ++c)
+      ok = cudaEventCreateWithFlags(&ws->in_done[c], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&ws->fwd_done[c], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) return fail(DFA_ERR_CUDA, "dfa_forward_host: stream/event creation failed");
+    ws->pipe = true;
+  }
+  // Pipeline over image chunks: H2D of chunk c+1 (copy engine 1) overlaps
+  // the kernel of chunk c and the D2H of chunk c-1 (copy engine 2), so the
+  // call costs ~max(H2D, D2H) instead of their sum.
+  const int64_t n_chunks = std::min<int64_t>(kHostChunks, g.B);
+  const int64_t per = (g.B + n_chunks - 1) / n_chunks;
+  const size_t img_qk = bqk / (size_t)g.B, img_v = bv / (size_t)g.B, img_l = bl / (size_t)g.B;
+  int launches = 0;
+  if ((err = cudaEventRecord(ws->start, s)) != cudaSuccess ||
+      (err = cudaStreamWaitEvent(ws->in_s, ws->start, 0)) != cudaSuccess)
     return fail(DFA_ERR_CUDA, "dfa_forward_host: %s", cudaGetErrorString(err));
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int64_t b0 = c * per, nb = std::min<int64_t>(per, g.B - b0);
+    if (nb <= 0) break;
+    const size_t oqk = (size_t)b0 * img_qk, ov = (size_t)b0 * img_v, ol = (size_t)b0 * img_l;
+    if ((err = cudaMemcpyAsync(dq + oqk, static_cast<const char*>(q) + oqk, nb * img_qk, cudaMemcpyHostToDevice,
+                               ws->in_s)) != cudaSuccess ||
+        (err = cudaMemcpyAsync(dk + oqk, static_cast<const char*>(k) + oqk, nb * img_qk, cudaMemcpyHostToDevice,
+                               ws->in_s)) != cudaSuccess ||
+        (err = cudaMemcpyAsync(dv + ov, static_cast<const char*>(v) + ov, nb * img_v, cudaMemcpyHostToDevice,
+                               ws->in_s)) != cudaSuccess ||
+        (err = cudaEventRecord(ws->in_done[c], ws->in_s)) != cudaSuccess ||
+        (err = cudaStreamWaitEvent(s, ws->in_done[c], 0)) != cudaSuccess)
+      return fail(DFA_ERR_CUDA, "dfa_forward_host: H2D: %s", cudaGetErrorString(err));
+    st = dfa_forward(cfg, dtype, nb, dq + oqk, dk + oqk, dv + ov, dout + ov, dl ? dl + ol / 4 : nullptr, stream);
+    if (st != DFA_OK) return st;
+    launches += g_launches;
+    if ((err = cudaEventRecord(ws->fwd_done[c], s)) != cudaSuccess ||
+        (err = cudaStreamWaitEvent(ws->out_s, ws->fwd_done[c], 0)) != cudaSuccess ||
+        (err = cudaMemcpyAsync(static_cast<char*>(o) + ov, dout + ov, nb * img_v, cudaMemcpyDeviceToHost,
+                               ws->out_s)) != cudaSuccess ||
+        (lse && (err = cudaMemcpyAsync(reinterpret_cast<char*>(lse) + ol, reinterpret_cast<char*>(dl) + ol,
+                                       nb * img_l, cudaMemcpyDeviceToHost, ws->out_s)) != cudaSuccess))
+      return fail(DFA_ERR_CUDA, "dfa_forward_host: D2H: %s", cudaGetErrorString(err));
+  }
+  if ((err = cudaStreamSynchronize(ws->out_s)) != cudaSuccess || (err = cudaStreamSynchronize(s)) != cudaSuccess)
+    return fail(DFA_ERR_CUDA, "dfa_forward_host: %s", cudaGetErrorString(err));
+  g_launches = launches;
   return DFA_OK;
 }
 
