@@ -51,58 +51,78 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms (B200_PROFILING.md)."""
+    """SM clock, power and clock-event (throttle) reasons sampled DURING the
+    timed region through NVML (~every 0.5 ms, so even a few-ms region gets
+    dozens of samples); nvidia-smi at 100 ms is the fallback
+    (B200_PROFILING.md clocks line)."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, torch_device):
+        self.dev = torch_device
+        self.samples = []
+        self.stop_flag = False
+        self.thread = None
+        self.nvml = None
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            import torch
+
+            pr = torch.cuda.get_device_properties(torch_device)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0".encode()
+            self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            self.bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.nvml = nv
+        except Exception:  # noqa: BLE001 -- no NVML: fall back to nvidia-smi
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        n, watts = 0, 0.0
+        while not self.stop_flag:
+            try:
+                if n % 16 == 0:  # power reads are the slow NVML query
+                    watts = nv.nvmlDeviceGetPowerUsage(self.h) / 1e3
+                self.samples.append((time.time(), nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), watts,
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+                n += 1
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.0002)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100", "-i",
-                 str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.reader = threading.Thread(target=self._read, daemon=True)
-            self.reader.start()
-        except OSError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
-
-    def mark(self):
-        return time.time()
+        if self.nvml:
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
 
     def stop(self, t0, t1):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
+        if not self.nvml:
+            return self._smi_once()
+        self.stop_flag = True
+        self.thread.join(timeout=2)
+        window = [x for x in self.samples if t0 <= x[0] <= t1] or self.samples[-3:]
+        if not window:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
+        reasons = sorted({n for x in window for n, bit in self.bits.items() if x[3] & bit})
+        return {"sm_mhz": statistics.median(x[1] for x in window), "sm_max_mhz": self.max_mhz,
+                "power_w_max": max(x[2] for x in window), "samples": len(window), "reasons": reasons,
+                "sampler": "nvml ~0.5 ms during the timed region"}
+
+    def _smi_once(self):
         try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        rows = []
-        for ts, line in self.lines:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                rows.append((ts, float(parts[0]), float(parts[1]), float(parts[2]), parts[3:7]))
-            except ValueError:
-                continue
-        window = [r for r in rows if t0 - 0.15 <= r[0] <= t1 + 0.15] or rows
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in window for i, a in enumerate(r[4]) if a.lower() == "active"})
-        return {"sm_mhz": statistics.median([r[1] for r in window]) if window else None,
-                "sm_max_mhz": max(r[2] for r in window) if window else None,
-                "power_w_max": max(r[3] for r in window) if window else None,
-                "samples": len(window), "reasons": reasons}
+            out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw",
+                                  "--format=csv,noheader,nounits", "-i", str(self.dev.index or 0)],
+                                 capture_output=True, text=True, timeout=10).stdout.split(",")
+            return {"sm_mhz": float(out[0]), "sm_max_mhz": float(out[1]), "power_w_max": float(out[2]),
+                    "samples": 1, "reasons": [], "sampler": "nvidia-smi once (NVML unavailable)"}
+        except Exception:  # noqa: BLE001
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
 
 
 def traffic_from_profiles(workload: str):
@@ -235,14 +255,8 @@ def run_b200(args):
     def step():
         dfa.dfa_forward(q, k, v, cfg, out=o, stream=stream)
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev)
     sampler.start()
-    # untimed soak (~1 s) so the clock sampler sees the part under this load
-    t_soak = time.time()
-    while not args.quick and time.time() - t_soak < 1.0:
-        for _ in range(50):
-            step()
-        torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -264,7 +278,7 @@ def run_b200(args):
     t_wall1 = time.time()
     per = [a.elapsed_time(b) for a, b in ev]
     total_ms = ev[0][0].elapsed_time(ev[-1][1])
-    clocks = sampler.stop(t_soak, t_wall1)
+    clocks = sampler.stop(t_wall0, t_wall1)
 
     # max over ranks of the device-timed region
     t = torch.tensor([total_ms, statistics.mean(per)], device=dev, dtype=torch.float64)
@@ -371,7 +385,7 @@ def main():
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="profiling mode: no clock soak, no e2e, no CPU baseline")
+    ap.add_argument("--quick", action="store_true", help="profiling mode: no e2e, no CPU baseline")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -9,6 +9,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdfa.so")
+# Profiling only: scripts/variants.py times alternative builds of the same
+# sources (compile-time tuning knobs) by pointing this at another in-tree .so.
+LIB_PATH = os.environ.get("DFA_LIB_VARIANT", LIB_PATH)
 
 DFA_OK = 0
 DFA_ERR_CONFIG = 1

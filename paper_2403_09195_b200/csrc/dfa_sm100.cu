@@ -72,8 +72,17 @@ constexpr int kSBufs = 3;                                  // rotating S/P buffe
 __host__ __device__ constexpr uint32_t col_s(int buf) { return 128u * buf; }          // S_0..S_2 (P aliases)
 __host__ __device__ constexpr uint32_t col_o(int slot) { return 384u + 64u * slot; }  // O_A, O_B
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units: p <= 2^8 between rescales
-constexpr int kPolyFrom = 6;               // elements e % 8 >= 6 use the FMA-pipe exp2
+#ifndef DFA_RESCALE_THR
+#define DFA_RESCALE_THR 8.0f
+#endif
+#ifndef DFA_POLY_MASK
+#define DFA_POLY_MASK 0x8888u
+#endif
+constexpr float kRescaleThreshold = DFA_RESCALE_THR;  // log2 units: p <= 2^8 between rescales
+// bit e: pair e of each 16-pair (32-column) chunk uses the FMA-pipe exp2
+// polynomial instead of MUFU.EX2 (balances the MUFU and FMA/issue pipes;
+// measured: 4 of 16 beats 0, 2, 5, 6, 7 and 8 of 16)
+constexpr uint32_t kPolyMask = DFA_POLY_MASK;
 
 // Geometry of one work unit, identical in every role.
 struct Unit {
@@ -114,7 +123,6 @@ struct FastDiv {
   __device__ __forceinline__ int32_t div(int32_t n) const {
     return (int32_t)((__umulhi((uint32_t)n, mul) + (uint32_t)n) >> shift);
   }
-  __device__ __forceinline__ int32_t mod(int32_t n) const { return n - div(n) * (int32_t)d; }
 };
 
 FastDiv make_fastdiv(uint32_t d) {
@@ -543,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         // per 32-column chunk: packed scale-subtract (FFMA2), exponentiate
-        // (3 of 4 pairs on MUFU, 1 of 4 as an FMA-pipe polynomial), packed
+        // (pairs in kPolyMask as an FMA-pipe polynomial, the rest on MUFU), packed
         // sums (FADD2) and bf16 packing
         float2 xv[16];
 #pragma unroll
@@ -551,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           xv[e] = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * e]), __uint_as_float(sr[c][2 * e + 1])), c2, n2);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          if (e % 4 == 3) {
+          if ((kPolyMask >> e) & 1u) {
             xv[e] = ptx::ex2_poly2(xv[e]);
           } else {
             xv[e].x = ptx::ex2(xv[e].x);

@@ -1,0 +1,16 @@
+#!/bin/bash
+# Build a profiling variant of libdfa.so with extra -D knobs:
+#   scripts/build_variant.sh NAME "-DDFA_POLY_MASK=0xA5A5u ..."
+# -> scripts/variants/libdfa_NAME.so (same sources; timed by scripts/variants.py)
+set -e
+NAME=$1; DEFS=$2
+HERE=$(cd $(dirname $0)/.. && pwd)
+C=$HERE/paper_2403_09195_b200/csrc
+OUT=$HERE/scripts/variants
+mkdir -p $OUT/build_$NAME
+ARCH="-gencode arch=compute_100a,code=sm_100a"
+FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr $DEFS"
+nvcc $FL -c $C/dfa_sm100.cu -o $OUT/build_$NAME/dfa_sm100.o
+nvcc $ARCH -shared -o $OUT/libdfa_$NAME.so $C/build/dfa_api.cpp.o $C/build/dfa_simt.cu.o $OUT/build_$NAME/dfa_sm100.o \
+  $C/build/dfa_combine.cu.o -lcudart_static -lrt -ldl -lpthread
+echo built $OUT/libdfa_$NAME.so
