@@ -41,7 +41,8 @@ typedef enum {
   DFA_ERR_OUT_OF_RANGE = 3, /* std::out_of_range        */
   DFA_ERR_CONTRACT = 4,     /* attnkit::contract_error  */
   DFA_ERR_CUDA = 5,         /* CUDA runtime/driver failure (no reference analogue) */
-  DFA_ERR_UNSUPPORTED = 6   /* valid config outside what the device kernels implement */
+  DFA_ERR_UNSUPPORTED = 6,  /* valid config outside what the device kernels implement */
+  DFA_ERR_IO = 7            /* attnkit::io_error (DTNSR1 tensor files)  */
 } dfa_status_t;
 
 typedef enum { DFA_F32 = 0, DFA_BF16 = 1 } dfa_dtype_t;
@@ -152,6 +153,18 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t n_branche
                                      dfa_dtype_t dtype, int64_t batch, const void* q, const void* k, const void* v,
                                      void* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Backward of the dilated core (the reference computes
+ * it on its autodiff tape for the dilated branch of detail::attention_mix,
+ * encoder.hpp:204-219, ops autodiff.hpp:99-179, 269-289): gradients of a loss
+ * w.r.t. q, k, v given dO = dloss/do.  o and lse are dfa_forward's outputs for
+ * the same inputs (lse required).  Layouts as dfa_forward; dq, dk [B,N,h,d],
+ * dv [B,N,h,d_v]; rows no view selects get 0.  `workspace` (device) holds
+ * dfa_backward_workspace_bytes bytes (per-row dO . O).  Deterministic. */
+dfa_status_t dfa_backward_workspace_bytes(const dfa_config_t* cfg, int64_t batch, size_t* bytes);
+dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
+                          const void* v, const void* o, const float* lse, const void* dout, void* dq, void* dk,
+                          void* dv, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Profiling hook: dfa_forward (bf16, tcgen05 path only) of a build of the
  * kernel that records a timeline of CTA 0 into `trace` (6 x 4096 uint64:
  * per role producer / QK issuer / softmax A / softmax B / epilogue / PV issuer, entries
@@ -164,6 +177,18 @@ dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const vo
  * `watchdog` (2 x gridDim uint64, host-mapped memory) and traps. */
 dfa_status_t dfa_forward_debug(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
                                void* o, uint64_t* trace, unsigned long long* watchdog, void* stream);
+
+/* DTNSR1 tensor files (tensor_io.hpp:15-19, 52-156): the reference's on-disk
+ * format for golden vectors and datasets.  dtype codes 0 = f32, 1 = f64;
+ * rank <= 8; dims are written as uint32 little-endian.  Errors: DFA_ERR_IO
+ * with the reference's io_error text ("bad magic in tensor file: ...",
+ * "truncated tensor file: ...", "unknown dtype code ..."). */
+dfa_status_t dfa_tensor_header(const char* path, int32_t* dtype, int32_t* rank, int64_t* dims /* [8] */);
+/* load_tensor<Scalar> (:147-153): payload converted to `dtype` (f32 <-> f64
+ * like read_payload's cast); `capacity` = scalars `out` can hold. */
+dfa_status_t dfa_tensor_load(const char* path, int32_t dtype, void* out, int64_t capacity);
+/* save_tensor (:86-91) / write_tensor (:52-84). */
+dfa_status_t dfa_tensor_save(const char* path, int32_t dtype, int32_t rank, const int64_t* dims, const void* data);
 
 /* Number of device kernels the last dfa_forward on this thread launched
  * (evidence for bench.py's gpu_launches). */

@@ -368,3 +368,76 @@ double oracle_time_dilated_f32(const float* q, const float* k, const float* v, i
   clock_gettime(CLOCK_MONOTONIC, &t1);
   return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
 }
+
+/* Backward of the dilated core: gradients of
+ * loss = sum(O * dO) w.r.t. q, k, v for one head at offset gamma, as the
+ * reference's tape computes them for the dilated branch of
+ * detail::attention_mix (encoder.hpp:204-219): per segment view,
+ *   S = (Qs Ks^T) * sc            ag::scale(ag::matmul)    autodiff.hpp:99-137
+ *   P = softmax_rows(S)           autodiff.hpp:166-179: dS = P o (dP - rowsum(dP o P))
+ *   Os = P Vs                     matmul backward: dP = dO Vs^T, dVs = P^T dO
+ * and slice_rows_strided / scatter_rows (:269-289) route the row gradients
+ * back to the global rows; rows no view selects get 0.  f64 throughout.
+ * sc = 1/sqrt(d) when `scale` (attention_mix always scales). */
+int oracle_dilated_backward_f64(const double* q, const double* k, const double* v, const double* dout, int64_t n,
+                                int64_t d, int64_t dv, int64_t w, int64_t r, int64_t gamma, int32_t scale,
+                                double* dq, double* dk, double* dvo) {
+  const int64_t off = gamma;
+  if (oracle_validate(n, w, r, 1, d, &off, 1, 0, 1, 0) != ORC_OK) return ORC_ERR_CONFIG;
+  if (gamma < 0 || gamma >= r) return ORC_ERR_OUT_OF_RANGE;
+  const double sc = scale ? 1.0 / sqrt((double)d) : 1.0;
+  const int64_t n_seg = (n + w - 1) / w, mmax = (w + r - 1) / r;
+  int64_t* rows = (int64_t*)malloc(sizeof(int64_t) * (size_t)mmax);
+  double* P = (double*)malloc(sizeof(double) * (size_t)(mmax * mmax));
+  double* dP = (double*)malloc(sizeof(double) * (size_t)(mmax * mmax));
+  memset(dq, 0, sizeof(double) * (size_t)(n * d));
+  memset(dk, 0, sizeof(double) * (size_t)(n * d));
+  memset(dvo, 0, sizeof(double) * (size_t)(n * dv));
+  for (int64_t s = 0; s < n_seg; ++s) {
+    int64_t m = 0;
+    oracle_segment_view(n, w, r, s, gamma, rows, mmax, &m);
+    if (m == 0) continue;
+    for (int64_t i = 0; i < m; ++i) {
+      const double* qi = q + rows[i] * d;
+      double mx = -INFINITY;
+      for (int64_t j = 0; j < m; ++j) {
+        const double* kj = k + rows[j] * d;
+        double acc = 0;
+        for (int64_t c = 0; c < d; ++c) acc += qi[c] * kj[c];
+        P[i * m + j] = acc * sc;
+        mx = P[i * m + j] > mx ? P[i * m + j] : mx;
+      }
+      double sum = 0;
+      for (int64_t j = 0; j < m; ++j) {
+        P[i * m + j] = exp(P[i * m + j] - mx);
+        sum += P[i * m + j];
+      }
+      for (int64_t j = 0; j < m; ++j) P[i * m + j] /= sum;
+    }
+    for (int64_t i = 0; i < m; ++i) {
+      const double* gi = dout + rows[i] * dv;
+      double dot = 0;
+      for (int64_t j = 0; j < m; ++j) {
+        const double* vj = v + rows[j] * dv;
+        double acc = 0;
+        for (int64_t c = 0; c < dv; ++c) acc += gi[c] * vj[c];
+        dP[i * m + j] = acc;
+        dot += acc * P[i * m + j];
+      }
+      for (int64_t j = 0; j < m; ++j) dP[i * m + j] = P[i * m + j] * (dP[i * m + j] - dot) * sc; /* dS * sc */
+    }
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < m; ++j) {
+        const double pij = P[i * m + j], sij = dP[i * m + j];
+        for (int64_t c = 0; c < dv; ++c) dvo[rows[j] * dv + c] += pij * dout[rows[i] * dv + c];
+        for (int64_t c = 0; c < d; ++c) {
+          dq[rows[i] * d + c] += sij * k[rows[j] * d + c];
+          dk[rows[j] * d + c] += sij * q[rows[i] * d + c];
+        }
+      }
+  }
+  free(rows);
+  free(P);
+  free(dP);
+  return ORC_OK;
+}

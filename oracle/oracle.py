@@ -74,6 +74,8 @@ class Port:
         L.oracle_multibranch_f64.argtypes = [_d, _d, _d, _i64, _i64, _i64, _i64, _i64p, _i64p, _i64p, _i32, _d, _d]
         L.oracle_time_dilated_f32.restype = ctypes.c_double
         L.oracle_time_dilated_f32.argtypes = [_f, _f, _f, _i64, _i64, _i64, _i64, _i64, _i64, _f]
+        L.oracle_dilated_backward_f64.restype = _i32
+        L.oracle_dilated_backward_f64.argtypes = [_d, _d, _d, _d, _i64, _i64, _i64, _i64, _i64, _i64, _i32, _d, _d, _d]
 
     def validate(self, n, w, r, h, d, offsets, tiled=False, tile=1, full=False) -> int:
         offs = np.asarray(offsets, dtype=np.int64)
@@ -146,6 +148,18 @@ class Port:
             raise OracleError(st)
         return out, lse
 
+    def dilated_backward(self, q, k, v, do, w, r, gamma, scale=True):
+        """Gradients (dq, dk, dv) of sum(O * do) for one head (f64)."""
+        q, k, v, do = (np.ascontiguousarray(x, dtype=np.float64) for x in (q, k, v, do))
+        n, d = q.shape
+        dv = v.shape[1]
+        gq, gk, gv = np.zeros((n, d)), np.zeros((n, d)), np.zeros((n, dv))
+        st = self.lib.oracle_dilated_backward_f64(_ptr(q, _d), _ptr(k, _d), _ptr(v, _d), _ptr(do, _d), n, d, dv, w,
+                                                  r, gamma, int(scale), _ptr(gq, _d), _ptr(gk, _d), _ptr(gv, _d))
+        if st:
+            raise OracleError(st)
+        return gq, gk, gv
+
     def time_dilated_f32(self, q, k, v, w, r, units):
         """q, k, v: [distinct, N, d] float32.  Seconds for `units` forwards, 1 thread."""
         q, k, v = (np.ascontiguousarray(x, dtype=np.float32) for x in (q, k, v))
@@ -186,6 +200,18 @@ class Reference:
                                      ctypes.c_char_p, _i64]
         L.ref_time_dilated_f32.restype = ctypes.c_double
         L.ref_time_dilated_f32.argtypes = [_i64, _i64, _i64, _i64, _i64, _i32, _i32, ctypes.c_uint64]
+        L.ref_save_tensor.restype = _i32
+        L.ref_save_tensor.argtypes = [ctypes.c_char_p, _i32, _i32, _i64p, ctypes.c_void_p]
+        L.ref_load_tensor_f64.restype = _i32
+        L.ref_load_tensor_f64.argtypes = [ctypes.c_char_p, _d, _i64, ctypes.POINTER(_i32), _i64p]
+        for sfx, tp in (("f32", _f), ("f64", _d)):
+            fn = getattr(L, f"ref_multi_head_dilated_{sfx}")
+            fn.restype = _i32
+            fn.argtypes = [tp, tp, tp, tp, tp, _i64, _i64, _i64, _i64, _i64, _i64p, tp]
+        L.ref_dilated_backward_f64.restype = _i32
+        L.ref_dilated_backward_f64.argtypes = [_d, _d, _d, _d, _i64, _i64, _i64, _i64, _i64, _i64, _d, _d, _d]
+        L.ref_encoder_block_f64.restype = _i32
+        L.ref_encoder_block_f64.argtypes = [_d, _i64, _i64, _i64, _i64, _i64, _i64] + [_d] * 14
 
     def last_error(self) -> str:
         return self.lib.ref_last_error().decode()
@@ -257,6 +283,68 @@ class Reference:
 
     def time_dilated_f32(self, n, w, r, d, units, threads, distinct=8, seed=901):
         return self.lib.ref_time_dilated_f32(n, w, r, d, units, threads, distinct, seed)
+
+    # ------------------------------------------------------------ §8(f) rows
+    def save_tensor(self, path, array):
+        a = np.asarray(array)
+        a = np.asarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64, order="C")
+        dims = np.array(a.shape, dtype=np.int64).reshape(-1)
+        st = self.lib.ref_save_tensor(os.fsencode(path), 0 if a.dtype == np.float32 else 1, a.ndim,
+                                      _ptr(dims, _i64p) if a.ndim else None, a.ctypes.data)
+        if st:
+            raise OracleError(st, self.last_error())
+
+    def load_tensor(self, path, cap=1 << 24):
+        out = np.zeros(cap)
+        rank = ctypes.c_int32(0)
+        dims = np.zeros(8, dtype=np.int64)
+        st = self.lib.ref_load_tensor_f64(os.fsencode(path), _ptr(out, _d), cap, ctypes.byref(rank), _ptr(dims, _i64p))
+        if st:
+            raise OracleError(st, self.last_error())
+        shape = tuple(int(x) for x in dims[: rank.value])
+        return out[: int(np.prod(shape)) if shape else 1].reshape(shape)
+
+    def multi_head_dilated(self, x, wq, wk, wv, wo, w, r, offsets=None):
+        """x [N, D]; wq/wk/wv [h, D, d]; wo [D, D] (float32 or float64)."""
+        dt = x.dtype
+        tp, fn = (_f, self.lib.ref_multi_head_dilated_f32) if dt == np.float32 else (
+            _d, self.lib.ref_multi_head_dilated_f64)
+        x, wq, wk, wv, wo = (np.ascontiguousarray(a, dtype=dt) for a in (x, wq, wk, wv, wo))
+        n, dm = x.shape
+        h = wq.shape[0]
+        offs = np.asarray(offsets if offsets is not None else [j % r for j in range(h)], dtype=np.int64)
+        out = np.zeros((n, dm), dtype=dt)
+        st = fn(_ptr(x, tp), _ptr(wq, tp), _ptr(wk, tp), _ptr(wv, tp), _ptr(wo, tp), n, dm, h, w, r,
+                _ptr(offs, _i64p), _ptr(out, tp))
+        if st:
+            raise OracleError(st, self.last_error())
+        return out
+
+    def dilated_backward(self, q, k, v, do, w, r, gamma):
+        q, k, v, do = (np.ascontiguousarray(a, dtype=np.float64) for a in (q, k, v, do))
+        n, d = q.shape
+        dv = v.shape[1]
+        gq, gk, gv = np.zeros((n, d)), np.zeros((n, d)), np.zeros((n, dv))
+        st = self.lib.ref_dilated_backward_f64(_ptr(q, _d), _ptr(k, _d), _ptr(v, _d), _ptr(do, _d), n, d, dv, w, r,
+                                               gamma, _ptr(gq, _d), _ptr(gk, _d), _ptr(gv, _d))
+        if st:
+            raise OracleError(st, self.last_error())
+        return gq, gk, gv
+
+    def encoder_block(self, x, p, h, w, r):
+        """One pre-norm block (encoder.hpp:241-248).  p: dict with ln1_g, ln1_b,
+        wq, wk, wv [h, D, d], wo, bo, ln2_g, ln2_b, w1, b1, w2, b2."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n, dm = x.shape
+        hidden = p["w1"].shape[1]
+        keys = ["ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2"]
+        arrs = [np.ascontiguousarray(p[k], dtype=np.float64) for k in keys]
+        out = np.zeros((n, dm))
+        st = self.lib.ref_encoder_block_f64(_ptr(x, _d), n, dm, h, hidden, w, r, *[_ptr(a, _d) for a in arrs],
+                                            _ptr(out, _d))
+        if st:
+            raise OracleError(st, self.last_error())
+        return out
 
 
 def reference_available() -> bool:

@@ -19,8 +19,11 @@
 #include <vector>
 
 #include "attnkit/attention.hpp"
+#include "attnkit/autodiff.hpp"
+#include "attnkit/encoder.hpp"
 #include "attnkit/oracles.hpp"
 #include "attnkit/tensor.hpp"
+#include "attnkit/tensor_io.hpp"
 
 using namespace attnkit;
 
@@ -29,7 +32,8 @@ namespace {
 thread_local std::string g_err;
 
 // Status codes shared with include/dfa.h (DFA_OK .. DFA_ERR_CONTRACT).
-enum : int { OK = 0, ERR_CONFIG = 1, ERR_DIMENSION = 2, ERR_OUT_OF_RANGE = 3, ERR_CONTRACT = 4, ERR_OTHER = 9 };
+enum : int { OK = 0, ERR_CONFIG = 1, ERR_DIMENSION = 2, ERR_OUT_OF_RANGE = 3, ERR_CONTRACT = 4, ERR_IO = 7,
+             ERR_OTHER = 9 };
 
 template <class F>
 int guarded(F&& f) {
@@ -48,6 +52,9 @@ int guarded(F&& f) {
   } catch (const contract_error& e) {
     g_err = e.what();
     return ERR_CONTRACT;
+  } catch (const io_error& e) {
+    g_err = e.what();
+    return ERR_IO;
   } catch (const std::exception& e) {
     g_err = e.what();
     return ERR_OTHER;
@@ -85,6 +92,25 @@ int dilated(const S* q, const S* k, const S* v, int64_t n, int64_t d, int64_t dv
   });
 }
 
+// attention.hpp:340-360 multi_head_dilated: x [N x D], wq/wk/wv [h x D x d],
+// wo [D x D] -> out [N x D]; offsets spread_offsets(h, r).
+template <class S>
+int multi_head(const S* x, const S* wq, const S* wk, const S* wv, const S* wo, int64_t n, int64_t dm, int64_t h,
+               int64_t w, int64_t r, const int64_t* offsets, S* out) {
+  return guarded([&] {
+    AttentionConfig cfg = make_cfg(n, w, r, h, dm / h, offsets, 0, 1, 1);
+    MultiHeadWeights<S> mw;
+    const int64_t d = dm / h;
+    for (int64_t j = 0; j < h; ++j) {
+      mw.wq.push_back(wrap(wq + j * dm * d, dm, d));
+      mw.wk.push_back(wrap(wk + j * dm * d, dm, d));
+      mw.wv.push_back(wrap(wv + j * dm * d, dm, d));
+    }
+    mw.wo = wrap(wo, dm, dm);
+    auto o = multi_head_dilated(wrap(x, n, dm), mw, cfg, 1);
+    std::memcpy(out, o.data(), sizeof(S) * static_cast<size_t>(o.numel()));
+  });
+}
 }  // namespace
 
 extern "C" {
@@ -229,6 +255,135 @@ double ref_time_dilated_f32(int64_t n, int64_t w, int64_t r, int64_t d, int64_t 
   volatile double keep = sink.load();
   (void)keep;
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// ---------------------------------------------------------------- §8(f) rows
+
+// tensor_io.hpp:86-91 save_tensor / :147-153 load_tensor (DTNSR1).
+int ref_save_tensor(const char* path, int32_t dtype, int32_t rank, const int64_t* dims, const void* data) {
+  return guarded([&] {
+    Shape shape(dims, dims + rank);
+    int64_t n = 1;
+    for (int i = 0; i < rank; ++i) n *= dims[i];
+    if (dtype == 0) {
+      const float* f = static_cast<const float*>(data);
+      save_tensor(path, Tensor<float>(shape, std::vector<float>(f, f + n)));
+    } else {
+      const double* f = static_cast<const double*>(data);
+      save_tensor(path, Tensor<double>(shape, std::vector<double>(f, f + n)));
+    }
+  });
+}
+int ref_load_tensor_f64(const char* path, double* out, int64_t cap, int32_t* rank, int64_t* dims) {
+  return guarded([&] {
+    auto t = load_tensor<double>(path);
+    if (t.numel() > cap) throw dimension_error("ref_load_tensor_f64: buffer too small");
+    *rank = static_cast<int32_t>(t.rank());
+    for (Index i = 0; i < t.rank(); ++i) dims[i] = t.dim(i);
+    std::memcpy(out, t.data(), sizeof(double) * static_cast<size_t>(t.numel()));
+  });
+}
+
+int ref_multi_head_dilated_f64(const double* x, const double* wq, const double* wk, const double* wv,
+                               const double* wo, int64_t n, int64_t dm, int64_t h, int64_t w, int64_t r,
+                               const int64_t* offsets, double* out) {
+  return multi_head(x, wq, wk, wv, wo, n, dm, h, w, r, offsets, out);
+}
+int ref_multi_head_dilated_f32(const float* x, const float* wq, const float* wk, const float* wv, const float* wo,
+                               int64_t n, int64_t dm, int64_t h, int64_t w, int64_t r, const int64_t* offsets,
+                               float* out) {
+  return multi_head(x, wq, wk, wv, wo, n, dm, h, w, r, offsets, out);
+}
+
+// Backward of one dilated head on the reference's tape: the dilated branch
+// of detail::attention_mix (encoder.hpp:204-219) on leaves q, k, v, with
+// loss = sum(head o dO) so the head's incoming gradient is dO; ag::backward
+// (autodiff.hpp:66-95) fills q/k/v grads.
+int ref_dilated_backward_f64(const double* q, const double* k, const double* v, const double* dout, int64_t n,
+                             int64_t d, int64_t dv, int64_t w, int64_t r, int64_t gamma, double* dq, double* dk,
+                             double* dvo) {
+  return guarded([&] {
+    const int64_t off = gamma;
+    AttentionConfig acfg = make_cfg(n, w, r, 1, d, &off, 0, 1, 1);
+    acfg.validate();
+    auto qv = ag::leaf(wrap(q, n, d)), kv = ag::leaf(wrap(k, n, d)), vv = ag::leaf(wrap(v, n, dv));
+    const double sc = 1.0 / std::sqrt(static_cast<double>(d));
+    ag::Var<double> head;
+    bool first = true;
+    for (Index s = 0; s < acfg.num_segments(); ++s) {
+      const auto view = make_segment_view(acfg.seq_len, acfg.segment_len, acfg.interval, s, gamma);
+      const auto m = static_cast<Index>(view.row_indices.size());
+      if (m == 0) continue;
+      auto qs = ag::slice_rows_strided(qv, view.row_indices.front(), acfg.interval, m);
+      auto ks = ag::slice_rows_strided(kv, view.row_indices.front(), acfg.interval, m);
+      auto vs = ag::slice_rows_strided(vv, view.row_indices.front(), acfg.interval, m);
+      auto scores = ag::scale(ag::matmul(qs, ag::transpose(ks)), sc);
+      auto placed = ag::scatter_rows(ag::matmul(ag::softmax_rows(scores), vs), view.row_indices, acfg.seq_len);
+      head = first ? placed : ag::add(head, placed);
+      first = false;
+    }
+    auto loss = ag::sum(ag::hadamard(head, ag::leaf(wrap(dout, n, dv))));
+    ag::backward(loss);
+    std::memcpy(dq, qv.grad().data(), sizeof(double) * static_cast<size_t>(n * d));
+    std::memcpy(dk, kv.grad().data(), sizeof(double) * static_cast<size_t>(n * d));
+    std::memcpy(dvo, vv.grad().data(), sizeof(double) * static_cast<size_t>(n * dv));
+  });
+}
+
+// One pre-norm encoder block (encoder.hpp:241-248, the loop body of
+// encoder_forward) on the reference's own ops: LN1 -> attention_mix (dilated,
+// per-head wq/wk/wv, wo, bo) -> residual -> LN2 -> w1/b1 -> GELU(erf) -> w2/b2
+// -> residual.  x [N x D]; wq/wk/wv [h x D x d]; mlp hidden = w1 cols.
+int ref_encoder_block_f64(const double* x, int64_t n, int64_t dm, int64_t h, int64_t hidden, int64_t w, int64_t r,
+                          const double* ln1_g, const double* ln1_b, const double* wq, const double* wk,
+                          const double* wv, const double* wo, const double* bo, const double* ln2_g,
+                          const double* ln2_b, const double* w1, const double* b1, const double* w2,
+                          const double* b2, double* out) {
+  return guarded([&] {
+    EncoderConfig cfg;
+    cfg.embed_dim = dm;
+    cfg.num_heads = static_cast<int>(h);
+    cfg.num_layers = 1;
+    cfg.attention_mode = AttentionMode::dilated;
+    cfg.segment_len = w;
+    cfg.interval = r;
+    // token count comes from the image geometry: a 1-channel image of
+    // sqrt(N) x sqrt(N) patches of size 1
+    const auto g = static_cast<Index>(std::llround(std::sqrt(static_cast<double>(n))));
+    if (g * g != n) throw config_error("ref_encoder_block_f64: N must be a square");
+    cfg.image_size = g;
+    cfg.patch_size = 1;
+    cfg.mlp_ratio = static_cast<double>(hidden) / static_cast<double>(dm);
+    if (cfg.mlp_hidden() != hidden) throw config_error("ref_encoder_block_f64: hidden/D not representable");
+    const int64_t d = dm / h;
+    ParamSet<double> p;
+    const std::string b = detail::block_prefix(0);
+    auto vec = [](const double* src, int64_t len) { return Tensor<double>({len}, std::vector<double>(src, src + len)); };
+    p.add(b + "ln1.g", vec(ln1_g, dm));
+    p.add(b + "ln1.b", vec(ln1_b, dm));
+    for (int64_t j = 0; j < h; ++j) {
+      p.add(msg(b, "attn.wq", j), wrap(wq + j * dm * d, dm, d));
+      p.add(msg(b, "attn.wk", j), wrap(wk + j * dm * d, dm, d));
+      p.add(msg(b, "attn.wv", j), wrap(wv + j * dm * d, dm, d));
+    }
+    p.add(b + "attn.wo", wrap(wo, dm, dm));
+    p.add(b + "attn.bo", vec(bo, dm));
+    p.add(b + "ln2.g", vec(ln2_g, dm));
+    p.add(b + "ln2.b", vec(ln2_b, dm));
+    p.add(b + "mlp.w1", wrap(w1, dm, hidden));
+    p.add(b + "mlp.b1", vec(b1, hidden));
+    p.add(b + "mlp.w2", wrap(w2, hidden, dm));
+    p.add(b + "mlp.b2", vec(b2, dm));
+    cfg.validate();
+    auto xv = ag::leaf(wrap(x, n, dm));
+    auto normed = ag::layer_norm(xv, p.at(b + "ln1.g"), p.at(b + "ln1.b"));
+    auto x1 = ag::add(xv, detail::attention_mix(normed, p, b, cfg));
+    auto normed2 = ag::layer_norm(x1, p.at(b + "ln2.g"), p.at(b + "ln2.b"));
+    auto hid = ag::gelu(ag::add_rowvec(ag::matmul(normed2, p.at(b + "mlp.w1")), p.at(b + "mlp.b1")));
+    auto mixed = ag::add_rowvec(ag::matmul(hid, p.at(b + "mlp.w2")), p.at(b + "mlp.b2"));
+    auto y = ag::add(x1, mixed);
+    std::memcpy(out, y.value().data(), sizeof(double) * static_cast<size_t>(n * dm));
+  });
 }
 
 }  // extern "C"

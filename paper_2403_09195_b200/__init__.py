@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -79,6 +80,10 @@ class UnsupportedError(DfaError):
     """A valid configuration the device kernels do not implement."""
 
 
+class TensorIOError(DfaError):
+    """attnkit::io_error (DTNSR1 tensor files)."""
+
+
 _ERRORS = {
     _lib.DFA_ERR_CONFIG: ConfigError,
     _lib.DFA_ERR_DIMENSION: DimensionError,
@@ -86,6 +91,7 @@ _ERRORS = {
     _lib.DFA_ERR_CONTRACT: ContractError,
     _lib.DFA_ERR_CUDA: CudaError,
     _lib.DFA_ERR_UNSUPPORTED: UnsupportedError,
+    _lib.DFA_ERR_IO: TensorIOError,
 }
 
 
@@ -396,3 +402,96 @@ def path_override(path: int):
         yield
     finally:
         lib.dfa_set_path_override(0)
+
+
+# ------------------------------------------------------------ backward (§8(f) 3)
+def dfa_backward(q, k, v, o, lse, do, cfg: AttentionConfig, dq=None, dk=None, dv=None, stream=None,
+                 workspace=None):
+    """Gradients (dq, dk, dv) of a loss w.r.t. q, k, v given do = dloss/do,
+    for o, lse = dfa_forward(q, k, v, cfg, lse=...) (include/dfa.h dfa_backward;
+    the reference's tape for the dilated branch of attention_mix,
+    encoder.hpp:204-219)."""
+    torch = _torch()
+    B, N, h, d = q.shape
+    dvd = v.shape[3]
+    for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("do", do), ("lse", lse)):
+        if not t.is_cuda or not t.is_contiguous():
+            raise DimensionError(f"dfa_backward: {name} must be a contiguous CUDA tensor")
+    if tuple(o.shape) != (B, N, h, dvd) or tuple(do.shape) != (B, N, h, dvd):
+        raise DimensionError("dfa_backward: o / do must be [B, N, h, d_v]")
+    if tuple(lse.shape) != (B, h, N) or lse.dtype != torch.float32:
+        raise DimensionError("dfa_backward: lse must be float32 [B, h, N]")
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    c = cfg._c()
+    c.value_dim = dvd
+    need = ctypes.c_size_t(0)
+    _check(lib.dfa_backward_workspace_bytes(ctypes.byref(c), B, ctypes.byref(need)))
+    if workspace is None or workspace.numel() < need.value:
+        workspace = torch.empty(max(need.value, 1), dtype=torch.uint8, device=q.device)
+    _check(lib.dfa_backward(ctypes.byref(c), _dtype_code(q), B, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                            o.data_ptr(), lse.data_ptr(), do.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                            workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
+    return dq, dk, dv
+
+
+_AUTOGRAD_FN = None
+
+
+def dilated_attention_fn(q, k, v, cfg: AttentionConfig):
+    """Differentiable dfa_forward (torch.autograd.Function over dfa_forward /
+    dfa_backward): o = DFA(q, k, v); o.backward(g) fills q/k/v .grad."""
+    global _AUTOGRAD_FN
+    torch = _torch()
+    if _AUTOGRAD_FN is None:
+        class _DFA(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, q_, k_, v_, cfg_):
+                B, N, h, _ = q_.shape
+                lse = torch.empty((B, h, N), dtype=torch.float32, device=q_.device)
+                o = dfa_forward(q_, k_, v_, cfg_, lse=lse)
+                ctx.save_for_backward(q_, k_, v_, o, lse)
+                ctx.cfg = cfg_
+                return o
+
+            @staticmethod
+            def backward(ctx, g):
+                q_, k_, v_, o, lse = ctx.saved_tensors
+                gq, gk, gv = dfa_backward(q_, k_, v_, o, lse, g.contiguous(), ctx.cfg)
+                return gq, gk, gv, None
+
+        _AUTOGRAD_FN = _DFA
+    return _AUTOGRAD_FN.apply(q, k, v, cfg)
+
+
+# ------------------------------------------------------------ DTNSR1 files
+def tensor_header(path: str):
+    """tensor_io.hpp:97-118: (dtype "f32"|"f64", shape tuple)."""
+    dt, rk = ctypes.c_int32(0), ctypes.c_int32(0)
+    dims = (ctypes.c_int64 * 8)()
+    _check(lib.dfa_tensor_header(os.fsencode(path), ctypes.byref(dt), ctypes.byref(rk), dims))
+    return ("f32" if dt.value == 0 else "f64"), tuple(dims[i] for i in range(rk.value))
+
+
+def load_tensor(path: str, dtype: str = "f64"):
+    """load_tensor<Scalar> (tensor_io.hpp:147-153) into a numpy array of `dtype`
+    ("f32" | "f64"), converting the stored scalar type like the reference."""
+    import numpy as np
+
+    _, shape = tensor_header(path)
+    out = np.empty(shape, dtype=np.float32 if dtype == "f32" else np.float64)
+    _check(lib.dfa_tensor_load(os.fsencode(path), 0 if dtype == "f32" else 1, out.ctypes.data, out.size))
+    return out
+
+
+def save_tensor(path: str, array) -> None:
+    """save_tensor (tensor_io.hpp:86-91); float32 arrays are written as f32,
+    everything else as f64 (the format's two dtypes)."""
+    import numpy as np
+
+    a = np.asarray(array)
+    a = np.asarray(a, dtype=np.float32 if a.dtype == np.float32 else np.float64, order="C")
+    dims = (ctypes.c_int64 * max(a.ndim, 1))(*a.shape)
+    _check(lib.dfa_tensor_save(os.fsencode(path), 0 if a.dtype == np.float32 else 1, a.ndim, dims,
+                               a.ctypes.data if a.size else None))

@@ -20,6 +20,7 @@ DFA_ERR_OUT_OF_RANGE = 3
 DFA_ERR_CONTRACT = 4
 DFA_ERR_CUDA = 5
 DFA_ERR_UNSUPPORTED = 6
+DFA_ERR_IO = 7
 
 DFA_F32 = 0
 DFA_BF16 = 1
@@ -50,6 +51,11 @@ EXPORTED = (
     "dfa_forward_multibranch",
     "dfa_last_launch_count",
     "dfa_version",
+    "dfa_backward_workspace_bytes",
+    "dfa_backward",
+    "dfa_tensor_header",
+    "dfa_tensor_load",
+    "dfa_tensor_save",
 )
 
 
@@ -115,6 +121,11 @@ def _load() -> ctypes.CDLL:
                                             c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]),
         "dfa_last_launch_count": (c_i32, []),
         "dfa_version": (c_i32, []),
+        "dfa_backward_workspace_bytes": (c_i32, [p_cfg, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
+        "dfa_backward": (c_i32, [p_cfg, c_i32, c_i64] + [c_vp] * 10 + [ctypes.c_size_t, c_vp]),
+        "dfa_tensor_header": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), p_i64]),
+        "dfa_tensor_load": (c_i32, [ctypes.c_char_p, c_i32, c_vp, c_i64]),
+        "dfa_tensor_save": (c_i32, [ctypes.c_char_p, c_i32, c_i32, p_i64, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

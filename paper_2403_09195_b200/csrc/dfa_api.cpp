@@ -102,6 +102,18 @@ size_t elem_size(dfa_dtype_t t) { return t == DFA_F32 ? 4 : 2; }
 
 }  // namespace
 
+namespace dfa_impl {
+dfa_status_t fail_msg(dfa_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+}  // namespace dfa_impl
+
 // Device staging for the host-buffer entry points, plus the copy streams and
 // events of the chunked H2D -> kernel -> D2H pipeline (created on first use).
 constexpr int kHostChunks = 8;
@@ -420,6 +432,39 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t nb, const
     if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "multibranch: fault hook: %s", cudaGetErrorString(err));
   }
   g_launches = launches;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_backward_workspace_bytes(const dfa_config_t* cfg, int64_t batch, size_t* bytes) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(cfg, batch, &g);
+  if (st != DFA_OK) return st;
+  if (!bytes) return fail(DFA_ERR_DIMENSION, "dfa_backward_workspace_bytes: null output");
+  *bytes = up256((size_t)(g.B * g.h * g.N) * 4);
+  return DFA_OK;
+}
+
+// Backward of dfa_forward (the reference's tape for the dilated branch of
+// detail::attention_mix, encoder.hpp:204-219).  lse is dfa_forward's output.
+dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
+                          const void* v, const void* o, const float* lse, const void* dout, void* dq, void* dk,
+                          void* dv, void* workspace, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(cfg, batch, &g);
+  if (st != DFA_OK) return st;
+  if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_CONFIG, "dfa_backward: unknown dtype %d", (int)dtype);
+  if (batch == 0) return DFA_OK;
+  if (!q || !k || !v || !o || !lse || !dout || !dq || !dk || !dv)
+    return fail(DFA_ERR_DIMENSION, "dfa_backward: null tensor pointer");
+  const size_t need = up256((size_t)(g.B * g.h * g.N) * 4);
+  if (!workspace || ws_bytes < need)
+    return fail(DFA_ERR_DIMENSION, "dfa_backward: workspace has %zu bytes, needs %zu", ws_bytes, need);
+  cudaError_t err = cudaSuccess;
+  const int n = dfa_impl::launch_backward(g, dtype, q, k, v, o, dout, lse, static_cast<float*>(workspace), dq, dk, dv,
+                                          reinterpret_cast<cudaStream_t>(stream), &err);
+  if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "dfa_backward: launch failed: %s", cudaGetErrorString(err));
+  g_launches = n;
   return DFA_OK;
 }
 

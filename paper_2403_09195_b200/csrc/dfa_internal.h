@@ -40,6 +40,11 @@ int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int n
                    const float* const* lse, void* out, float* lse_out, cudaStream_t stream, cudaError_t* err);
 constexpr int kMaxBranches = 8;
 
+// Backward of the dilated core (dfa_bwd.cu): delta = workspace [B, h, N] fp32.
+int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o,
+                    const void* dout, const float* lse, float* delta, void* dq, void* dk, void* dv,
+                    cudaStream_t stream, cudaError_t* err);
+
 // Fault hook (attention.hpp:272): out[0] += 1e-3.
 int launch_perturb(int dtype, void* o, cudaStream_t stream);
 
