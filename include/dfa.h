@@ -165,6 +165,39 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
                           const void* v, const void* o, const float* lse, const void* dout, void* dq, void* dk,
                           void* dv, void* workspace, size_t workspace_bytes, void* stream);
 
+/* attention.hpp:340-360 multi_head_dilated for a batch: x [B, N, D] with
+ * D = h * d; wq, wk, wv [h, D, d] (the reference's per-head D x d
+ * projections, stacked); wo [D, D]; out [B, N, D] = concat_j(head_j) wo,
+ * head_j = dilated_attention(x wq_j, x wk_j, x wv_j) at offset gamma_j.
+ * Requires full coverage (attention.hpp:343).  All tensors `dtype`, device.
+ * Projections are cuBLASLt GEMMs writing the core's [B, N, h, d] layout
+ * directly; `workspace` holds dfa_multi_head_workspace_bytes bytes. */
+dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
+                                            size_t* bytes);
+dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,
+                                    const void* wq, const void* wk, const void* wv, const void* wo, void* out,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
+/* One pre-norm encoder block (encoder.hpp:241-248; parameters as
+ * init_encoder_params names them, :287-304): x1 = x + attention_mix(LN1(x))
+ * (attention_mix = multi_head_dilated + bias bo, encoder.hpp:189-223);
+ * out = x1 + GELU(LN2(x1) w1 + b1) w2 + b2, GELU the erf form
+ * (tensor.hpp:262-265), LayerNorm eps 1e-5 with population variance. */
+typedef struct {
+  const void *ln1_g, *ln1_b;   /* [D] */
+  const void *wq, *wk, *wv;    /* [h, D, d] */
+  const void *wo, *bo;         /* [D, D], [D] */
+  const void *ln2_g, *ln2_b;   /* [D] */
+  const void *w1, *b1;         /* [D, hidden], [hidden] */
+  const void *w2, *b2;         /* [hidden, D], [D] */
+  int64_t hidden;              /* mlp width (mlp_ratio * D) */
+} dfa_block_weights_t;
+dfa_status_t dfa_encoder_block_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
+                                               int64_t hidden, size_t* bytes);
+dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,
+                                       const dfa_block_weights_t* weights, void* out, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+
 /* Profiling hook: dfa_forward (bf16, tcgen05 path only) of a build of the
  * kernel that records a timeline of CTA 0 into `trace` (6 x 4096 uint64:
  * per role producer / QK issuer / softmax A / softmax B / epilogue / PV issuer, entries

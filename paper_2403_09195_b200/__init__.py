@@ -465,6 +465,72 @@ def dilated_attention_fn(q, k, v, cfg: AttentionConfig):
     return _AUTOGRAD_FN.apply(q, k, v, cfg)
 
 
+# ------------------------------------------------- projections / block (§8(f) 1-2)
+def _layer_check(x, cfg, who):
+    if not x.is_cuda or not x.is_contiguous() or x.dim() != 3:
+        raise DimensionError(f"{who}: x must be a contiguous CUDA [B, N, D] tensor")
+    D = cfg.num_heads * cfg.head_dim
+    if x.shape[1] != cfg.seq_len or x.shape[2] != D:
+        raise DimensionError(f"{who}: input {list(x.shape[1:])}, expected [{cfg.seq_len}x{D}]")
+
+
+def _ws(nbytes, like, workspace):
+    torch = _torch()
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=like.device)
+    return workspace
+
+
+def multi_head_dilated(x, wq, wk, wv, wo, cfg: AttentionConfig, out=None, stream=None, workspace=None):
+    """attention.hpp:340-360 for a batch: x [B, N, D]; wq/wk/wv [h, D, d]; wo [D, D]."""
+    torch = _torch()
+    _layer_check(x, cfg, "multi_head_dilated")
+    for w_ in (wq, wk, wv, wo):
+        if not w_.is_cuda or not w_.is_contiguous() or w_.dtype != x.dtype:
+            raise DimensionError("multi_head_dilated: weights must be contiguous CUDA tensors of x's dtype")
+    h, D, d = cfg.num_heads, cfg.num_heads * cfg.head_dim, cfg.head_dim
+    if tuple(wq.shape) != (h, D, d) or tuple(wk.shape) != (h, D, d) or tuple(wv.shape) != (h, D, d):
+        raise DimensionError(f"multi_head_dilated: head projections must be [{h}, {D}, {d}]")
+    if tuple(wo.shape) != (D, D):
+        raise DimensionError(f"multi_head_dilated: output projection is {list(wo.shape)}, expected [{D}x{D}]")
+    B = x.shape[0]
+    c = cfg._c()
+    need = ctypes.c_size_t(0)
+    _check(lib.dfa_multi_head_workspace_bytes(ctypes.byref(c), _dtype_code(x), B, ctypes.byref(need)))
+    workspace = _ws(need.value, x, workspace)
+    out = torch.empty_like(x) if out is None else out
+    _check(lib.dfa_multi_head_dilated(ctypes.byref(c), _dtype_code(x), B, x.data_ptr(), wq.data_ptr(), wk.data_ptr(),
+                                      wv.data_ptr(), wo.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+                                      workspace.numel(), _stream_ptr(stream)))
+    return out
+
+
+BLOCK_KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2")
+
+
+def encoder_block_forward(x, weights: dict, cfg: AttentionConfig, out=None, stream=None, workspace=None):
+    """One pre-norm encoder block (encoder.hpp:241-248).  weights: BLOCK_KEYS ->
+    CUDA tensors of x's dtype (wq/wk/wv [h, D, d], w1 [D, hidden], w2 [hidden, D])."""
+    torch = _torch()
+    _layer_check(x, cfg, "encoder_block")
+    for k_ in BLOCK_KEYS:
+        t = weights[k_]
+        if not t.is_cuda or not t.is_contiguous() or t.dtype != x.dtype:
+            raise DimensionError(f"encoder_block: {k_} must be a contiguous CUDA tensor of x's dtype")
+    hidden = weights["w1"].shape[1]
+    wt = _lib.DfaBlockWeights(*[weights[k_].data_ptr() for k_ in BLOCK_KEYS], hidden)
+    B = x.shape[0]
+    c = cfg._c()
+    need = ctypes.c_size_t(0)
+    _check(lib.dfa_encoder_block_workspace_bytes(ctypes.byref(c), _dtype_code(x), B, hidden, ctypes.byref(need)))
+    workspace = _ws(need.value, x, workspace)
+    out = torch.empty_like(x) if out is None else out
+    _check(lib.dfa_encoder_block_forward(ctypes.byref(c), _dtype_code(x), B, x.data_ptr(), ctypes.byref(wt),
+                                         out.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                         _stream_ptr(stream)))
+    return out
+
+
 # ------------------------------------------------------------ DTNSR1 files
 def tensor_header(path: str):
     """tensor_io.hpp:97-118: (dtype "f32"|"f64", shape tuple)."""

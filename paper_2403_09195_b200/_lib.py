@@ -53,10 +53,21 @@ EXPORTED = (
     "dfa_version",
     "dfa_backward_workspace_bytes",
     "dfa_backward",
+    "dfa_multi_head_workspace_bytes",
+    "dfa_multi_head_dilated",
+    "dfa_encoder_block_workspace_bytes",
+    "dfa_encoder_block_forward",
     "dfa_tensor_header",
     "dfa_tensor_load",
     "dfa_tensor_save",
 )
+
+
+class DfaBlockWeights(ctypes.Structure):
+    """Mirror of dfa_block_weights_t (include/dfa.h)."""
+
+    _fields_ = [(n, ctypes.c_void_p) for n in ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "bo", "ln2_g", "ln2_b", "w1",
+                                                "b1", "w2", "b2")] + [("hidden", ctypes.c_int64)]
 
 
 class DfaConfig(ctypes.Structure):
@@ -123,6 +134,11 @@ def _load() -> ctypes.CDLL:
         "dfa_version": (c_i32, []),
         "dfa_backward_workspace_bytes": (c_i32, [p_cfg, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_backward": (c_i32, [p_cfg, c_i32, c_i64] + [c_vp] * 10 + [ctypes.c_size_t, c_vp]),
+        "dfa_multi_head_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
+        "dfa_multi_head_dilated": (c_i32, [p_cfg, c_i32, c_i64] + [c_vp] * 7 + [ctypes.c_size_t, c_vp]),
+        "dfa_encoder_block_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
+        "dfa_encoder_block_forward": (c_i32, [p_cfg, c_i32, c_i64, c_vp, ctypes.POINTER(DfaBlockWeights), c_vp, c_vp,
+                                              ctypes.c_size_t, c_vp]),
         "dfa_tensor_header": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), p_i64]),
         "dfa_tensor_load": (c_i32, [ctypes.c_char_p, c_i32, c_vp, c_i64]),
         "dfa_tensor_save": (c_i32, [ctypes.c_char_p, c_i32, c_i32, p_i64, c_vp]),

@@ -468,6 +468,139 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
   return DFA_OK;
 }
 
+// ------------------------------------------------------------ §8(f) 1-2
+static constexpr size_t kLtWorkspace = 32u << 20;
+
+static dfa_status_t layer_geometry(const dfa_config_t* cfg, int64_t batch, dfa_impl::Geometry* g, const char* who) {
+  dfa_status_t st = validate(cfg, 1);  // attention.hpp:343 / EncoderConfig::validate: full coverage
+  if (st != DFA_OK) return st;
+  st = resolve(cfg, batch, g);
+  if (st != DFA_OK) return st;
+  if (cfg->value_dim != 0 && cfg->value_dim != cfg->head_dim)
+    return fail(DFA_ERR_DIMENSION, "%s: value_dim must equal head_dim", who);
+  if (g->h * g->d > 1024) return fail(DFA_ERR_UNSUPPORTED, "%s: model dim %lld > 1024", who, (long long)(g->h * g->d));
+  return DFA_OK;
+}
+
+dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
+                                            size_t* bytes) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = layer_geometry(cfg, batch, &g, "multi_head_dilated");
+  if (st != DFA_OK) return st;
+  *bytes = 4 * up256((size_t)(g.B * g.N * g.h * g.d) * elem_size(dtype)) + kLtWorkspace;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,
+                                    const void* wq, const void* wk, const void* wv, const void* wo, void* out,
+                                    void* workspace, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  dfa_impl::Geometry g;
+  dfa_status_t st = layer_geometry(cfg, batch, &g, "multi_head_dilated");
+  if (st != DFA_OK) return st;
+  size_t need = 0;
+  dfa_multi_head_workspace_bytes(cfg, dtype, batch, &need);
+  if (!workspace || ws_bytes < need)
+    return fail(DFA_ERR_DIMENSION, "multi_head_dilated: workspace has %zu bytes, needs %zu", ws_bytes, need);
+  if (batch == 0) return DFA_OK;
+  if (!x || !wq || !wk || !wv || !wo || !out) return fail(DFA_ERR_DIMENSION, "multi_head_dilated: null pointer");
+  const int64_t M = g.B * g.N, D = g.h * g.d;
+  const size_t act = up256((size_t)(M * D) * elem_size(dtype));
+  char* base = static_cast<char*>(workspace);
+  void* qkv[3] = {base, base + act, base + 2 * act};
+  void* att = base + 3 * act;
+  void* lt = base + 4 * act;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const char* why = "";
+  const void* w3[3] = {wq, wk, wv};
+  int launches = 0;
+  for (int i = 0; i < 3; ++i) {  // x [M, D] . w_j [D, d] -> column block j of [M, h*d], one batched call
+    if (!dfa_impl::gemm_rowmajor(dtype, M, g.d, D, x, D, 0, w3[i], g.d, D * g.d, qkv[i], D, g.d, nullptr, 0, 0.0f,
+                                 nullptr, (int)g.h, lt, kLtWorkspace, s, &why))
+      return fail(DFA_ERR_CUDA, "multi_head_dilated: projection: %s", why);
+    ++launches;
+  }
+  st = dfa_forward(cfg, dtype, batch, qkv[0], qkv[1], qkv[2], att, nullptr, stream);
+  if (st != DFA_OK) return st;
+  launches += g_launches;
+  if (!dfa_impl::gemm_rowmajor(dtype, M, D, D, att, D, 0, wo, D, 0, out, D, 0, nullptr, 0, 0.0f, nullptr, 1, lt,
+                               kLtWorkspace, s, &why))
+    return fail(DFA_ERR_CUDA, "multi_head_dilated: output projection: %s", why);
+  g_launches = launches + 1;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_encoder_block_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
+                                               int64_t hidden, size_t* bytes) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = layer_geometry(cfg, batch, &g, "encoder_block");
+  if (st != DFA_OK) return st;
+  if (hidden < 1) return fail(DFA_ERR_CONFIG, "encoder: mlp_ratio must yield a positive width");
+  const size_t es = elem_size(dtype);
+  const size_t act = up256((size_t)(g.B * g.N * g.h * g.d) * es);
+  *bytes = 6 * act + up256((size_t)(g.B * g.N * hidden) * es) + kLtWorkspace;
+  return DFA_OK;
+}
+
+dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,
+                                       const dfa_block_weights_t* wt, void* out, void* workspace, size_t ws_bytes,
+                                       void* stream) {
+  g_launches = 0;
+  if (!wt) return fail(DFA_ERR_DIMENSION, "encoder_block: null weights");
+  dfa_impl::Geometry g;
+  dfa_status_t st = layer_geometry(cfg, batch, &g, "encoder_block");
+  if (st != DFA_OK) return st;
+  size_t need = 0;
+  st = dfa_encoder_block_workspace_bytes(cfg, dtype, batch, wt->hidden, &need);
+  if (st != DFA_OK) return st;
+  if (!workspace || ws_bytes < need)
+    return fail(DFA_ERR_DIMENSION, "encoder_block: workspace has %zu bytes, needs %zu", ws_bytes, need);
+  if (batch == 0) return DFA_OK;
+  const void* ptrs[] = {wt->ln1_g, wt->ln1_b, wt->wq, wt->wk, wt->wv, wt->wo, wt->bo,
+                        wt->ln2_g, wt->ln2_b, wt->w1, wt->b1, wt->w2, wt->b2};
+  for (const void* p : ptrs)
+    if (!p) return fail(DFA_ERR_DIMENSION, "encoder_block: null weight pointer");
+  if (!x || !out) return fail(DFA_ERR_DIMENSION, "encoder_block: null tensor pointer");
+  const int64_t M = g.B * g.N, D = g.h * g.d, H = wt->hidden;
+  const size_t es = elem_size(dtype), act = up256((size_t)(M * D) * es);
+  char* base = static_cast<char*>(workspace);
+  void* ln = base;
+  void* qkv[3] = {base + act, base + 2 * act, base + 3 * act};
+  void* att = base + 4 * act;
+  void* x1 = base + 5 * act;
+  void* hid = base + 6 * act;
+  void* lt = base + 6 * act + up256((size_t)(M * H) * es);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const char* why = "";
+  int launches = 0;
+  auto gemm = [&](int64_t m, int64_t n, int64_t k, const void* a, const void* b, void* d, const void* c,
+                  const void* bias) {
+    ++launches;
+    return dfa_impl::gemm_rowmajor(dtype, m, n, k, a, k, 0, b, n, 0, d, n, 0, c, n, c ? 1.0f : 0.0f, bias, 1, lt,
+                                   kLtWorkspace, s, &why);
+  };
+  launches += dfa_impl::launch_layer_norm(dtype, x, wt->ln1_g, wt->ln1_b, ln, M, (int)D, s);
+  const void* w3[3] = {wt->wq, wt->wk, wt->wv};
+  for (int i = 0; i < 3; ++i) {
+    ++launches;
+    if (!dfa_impl::gemm_rowmajor(dtype, M, g.d, D, ln, D, 0, w3[i], g.d, D * g.d, qkv[i], D, g.d, nullptr, 0, 0.0f,
+                                 nullptr, (int)g.h, lt, kLtWorkspace, s, &why))
+      return fail(DFA_ERR_CUDA, "encoder_block: projection: %s", why);
+  }
+  st = dfa_forward(cfg, dtype, batch, qkv[0], qkv[1], qkv[2], att, nullptr, stream);
+  if (st != DFA_OK) return st;
+  launches += g_launches;
+  if (!gemm(M, D, D, att, wt->wo, x1, x, wt->bo)) return fail(DFA_ERR_CUDA, "encoder_block: wo: %s", why);
+  launches += dfa_impl::launch_layer_norm(dtype, x1, wt->ln2_g, wt->ln2_b, ln, M, (int)D, s);
+  if (!gemm(M, H, D, ln, wt->w1, hid, nullptr, wt->b1)) return fail(DFA_ERR_CUDA, "encoder_block: w1: %s", why);
+  launches += dfa_impl::launch_gelu(dtype, hid, M * H, s);
+  if (!gemm(M, D, H, hid, wt->w2, out, x1, wt->b2)) return fail(DFA_ERR_CUDA, "encoder_block: w2: %s", why);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "encoder_block: %s", cudaGetErrorString(err));
+  g_launches = launches;
+  return DFA_OK;
+}
+
 dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t with_lse,
                                  size_t* bytes) {
   dfa_impl::Geometry g;

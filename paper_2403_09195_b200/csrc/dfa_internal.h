@@ -45,6 +45,15 @@ int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, 
                     const void* dout, const float* lse, float* delta, void* dq, void* dk, void* dv,
                     cudaStream_t stream, cudaError_t* err);
 
+// dfa_layers.cu: cuBLASLt row-major GEMM D = A B (+ bias) (+ beta C), strided
+// batch; LayerNorm (eps 1e-5) and erf-GELU kernels.  Return 0 on failure.
+int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
+                  int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
+                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why);
+int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
+                      cudaStream_t stream);
+int launch_gelu(int dtype, void* x, int64_t n, cudaStream_t stream);
+
 // Fault hook (attention.hpp:272): out[0] += 1e-3.
 int launch_perturb(int dtype, void* o, cudaStream_t stream);
 

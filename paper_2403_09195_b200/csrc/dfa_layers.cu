@@ -1,0 +1,200 @@
+// Callers either side of the hot path:
+//   * multi_head_dilated (attention.hpp:340-360): per-head Q/K/V projections
+//     -> dilated core per head -> concat -> output projection;
+//   * one pre-norm encoder block (encoder.hpp:241-248): LN1 -> attention_mix
+//     (+ bo) -> residual -> LN2 -> W1 + b1 -> GELU(erf) -> W2 + b2 -> residual.
+//
+// B200 layout: activations stay in the core's [B, N, h, d] = [B*N, D] layout
+// end to end, so the projections write exactly what the TMA boxes of the
+// attention kernel read and the concat of the heads IS the attention output
+// -- no gather, scatter or transpose pass exists.  The plain GEMMs go to
+// cuBLASLt (row-major via the transposed problem; per-head projections as
+// one strided-batched call writing the head's column block; bias and the
+// residual ride in the GEMM epilogue as bias + beta * C).  LayerNorm and the
+// erf-GELU (autodiff.hpp / tensor.hpp:262-279 -- cuBLASLt's GELU epilogue is
+// the tanh approximation, so it is not used) are this file's own kernels.
+// fp32 runs with CUBLAS_COMPUTE_32F (no TF32) as the validation mode.
+#include <cublasLt.h>
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "dfa_internal.h"
+
+namespace dfa_impl {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p) {
+  return *p;
+}
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) {
+  return __bfloat162float(*p);
+}
+template <typename T>
+__device__ __forceinline__ T stf(float x);
+template <>
+__device__ __forceinline__ float stf<float>(float x) {
+  return x;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 stf<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+// tensor.hpp:281-300 / autodiff.hpp:191-243 layer_norm: population variance,
+// eps 1e-5, y = (x - mean) / sqrt(var + eps) * g + b.  One warp per row,
+// two-pass in fp32 over the row held in registers (D <= 32 * 32).
+template <typename T>
+__global__ void __launch_bounds__(256) layer_norm_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                                         const T* __restrict__ b, T* __restrict__ y, int64_t rows,
+                                                         int cols) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const T* xr = x + row * cols;
+  float v[32];
+  float sum = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < cols ? ldf(xr + c) : 0.0f;
+    sum += v[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / (float)cols;
+  float var = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = lane + 32 * i;
+    const float d = c < cols ? v[i] - mean : 0.0f;
+    var = fmaf(d, d, var);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+  const float inv = 1.0f / sqrtf(var / (float)cols + 1e-5f);
+  T* yr = y + row * cols;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = lane + 32 * i;
+    if (c < cols) yr[c] = stf<T>((v[i] - mean) * inv * ldf(g + c) + ldf(b + c));
+  }
+}
+
+// tensor.hpp:262-265 gelu_scalar: x * 0.5 * (1 + erf(x / sqrt(2))), in place.
+template <typename T>
+__global__ void __launch_bounds__(256) gelu_kernel(T* __restrict__ x, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = ldf(x + i);
+    x[i] = stf<T>(v * 0.5f * (1.0f + erff(v * 0.70710678118654752f)));
+  }
+}
+
+struct LtHandle {
+  cublasLtHandle_t h = nullptr;
+  ~LtHandle() {
+    if (h) cublasLtDestroy(h);
+  }
+};
+cublasLtHandle_t lt_handle() {
+  thread_local LtHandle lh;
+  if (!lh.h && cublasLtCreate(&lh.h) != CUBLAS_STATUS_SUCCESS) lh.h = nullptr;
+  return lh.h;
+}
+
+}  // namespace
+
+// Row-major D[M, N] (ldd) = A[M, K] (lda) * B[K, N] (ldb) (+ bias[N]) (+ beta * C[M, N] (ldc)),
+// `batch` problems at element strides sa / sb / sc / sd (sa may be 0).
+// Column-major cuBLASLt sees D^T = B^T A^T: m = N, n = M.
+int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
+                  int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
+                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why) {
+  cublasLtHandle_t h = lt_handle();
+  if (!h) {
+    *why = "cublasLtCreate failed";
+    return 0;
+  }
+  const cudaDataType_t dt = dtype == 0 ? CUDA_R_32F : CUDA_R_16BF;
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr, ld = nullptr;
+  cublasLtMatmulPreference_t pref = nullptr;
+  int ok = 0;
+  do {
+    if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS) break;
+    cublasLtEpilogue_t epi = bias ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT;
+    cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi));
+    if (bias) {
+      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
+      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &dt, sizeof(dt));
+    }
+    // cublas operand "A" = our B^T ([N x K] col-major, ld = ldb); "B" = our A^T ([K x M], ld = lda)
+    if (cublasLtMatrixLayoutCreate(&la, dt, N, K, ldb) != CUBLAS_STATUS_SUCCESS) break;
+    if (cublasLtMatrixLayoutCreate(&lb, dt, K, M, lda) != CUBLAS_STATUS_SUCCESS) break;
+    if (cublasLtMatrixLayoutCreate(&lc, dt, N, M, C ? ldc : ldd) != CUBLAS_STATUS_SUCCESS) break;
+    if (cublasLtMatrixLayoutCreate(&ld, dt, N, M, ldd) != CUBLAS_STATUS_SUCCESS) break;
+    if (batch > 1) {
+      const int32_t bc = batch;
+      const int64_t strides[4] = {sb, sa, C ? sd : sd, sd};
+      cublasLtMatrixLayout_t ls[4] = {la, lb, lc, ld};
+      for (int i = 0; i < 4; ++i) {
+        cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
+        cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &strides[i],
+                                         sizeof(int64_t));
+      }
+    }
+    if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS) break;
+    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes, sizeof(ws_bytes));
+    cublasLtMatmulHeuristicResult_t res;
+    int found = 0;
+    if (cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, ld, pref, 1, &res, &found) != CUBLAS_STATUS_SUCCESS ||
+        found == 0) {
+      *why = "no cuBLASLt algorithm for this GEMM";
+      break;
+    }
+    const float alpha = 1.0f;
+    const float b2 = C ? beta : 0.0f;
+    if (cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res.algo, ws, ws_bytes, stream) !=
+        CUBLAS_STATUS_SUCCESS) {
+      *why = "cublasLtMatmul failed";
+      break;
+    }
+    ok = 1;
+  } while (0);
+  if (pref) cublasLtMatmulPreferenceDestroy(pref);
+  if (ld) cublasLtMatrixLayoutDestroy(ld);
+  if (lc) cublasLtMatrixLayoutDestroy(lc);
+  if (lb) cublasLtMatrixLayoutDestroy(lb);
+  if (la) cublasLtMatrixLayoutDestroy(la);
+  if (op) cublasLtMatmulDescDestroy(op);
+  return ok;
+}
+
+int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
+                      cudaStream_t stream) {
+  const unsigned grid = (unsigned)((rows * 32 + 255) / 256);
+  if (dtype == 0)
+    layer_norm_kernel<float><<<grid, 256, 0, stream>>>((const float*)x, (const float*)g, (const float*)b, (float*)y,
+                                                       rows, cols);
+  else
+    layer_norm_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
+                                                               (const __nv_bfloat16*)b, (__nv_bfloat16*)y, rows,
+                                                               cols);
+  return 1;
+}
+
+int launch_gelu(int dtype, void* x, int64_t n, cudaStream_t stream) {
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (dtype == 0)
+    gelu_kernel<float><<<grid, 256, 0, stream>>>((float*)x, n);
+  else
+    gelu_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((__nv_bfloat16*)x, n);
+  return 1;
+}
+
+}  // namespace dfa_impl
