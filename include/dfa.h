@@ -103,6 +103,15 @@ dfa_status_t dfa_query_path(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t 
 dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
                          const void* v, void* o, float* lse, void* stream);
 
+/* dfa_forward with explicit token (row) strides in elements: q row n of
+ * image b at q + (b * N + n) * ldq (heads contiguous inside the row), same
+ * for k / v / o.  ldq, ldk >= h * d; ldv, ldo >= h * d_v.  Lets the core read
+ * q, k, v as column blocks of one fused QKV projection ([B, N, 3, h, d]:
+ * ld = 3 h d) without a split pass. */
+dfa_status_t dfa_forward_strided(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                                 int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* o,
+                                 int64_t ldo, float* lse, void* stream);
+
 /* Reference-shaped single-head call on HOST buffers, synchronous:
  * q, k [N x d], v [N x d_v] -> out [N x d_v] (attention.hpp:280-282).
  * `workers` is accepted and ignored (the GPU grid replaces parallel_for).
@@ -170,8 +179,10 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
  * projections, stacked); wo [D, D]; out [B, N, D] = concat_j(head_j) wo,
  * head_j = dilated_attention(x wq_j, x wk_j, x wv_j) at offset gamma_j.
  * Requires full coverage (attention.hpp:343).  All tensors `dtype`, device.
- * Projections are cuBLASLt GEMMs writing the core's [B, N, h, d] layout
- * directly; `workspace` holds dfa_multi_head_workspace_bytes bytes. */
+ * The three projections run as ONE cuBLASLt GEMM against the weights packed
+ * [D, 3, h, d]; the core reads q / k / v straight out of its [B, N, 3, h, d]
+ * output (dfa_forward_strided) and writes the concat layout the output
+ * projection consumes.  `workspace` holds dfa_multi_head_workspace_bytes. */
 dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
                                             size_t* bytes);
 dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,

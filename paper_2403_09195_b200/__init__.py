@@ -283,6 +283,24 @@ def dfa_forward(q, k, v, cfg: AttentionConfig, out=None, lse=None, stream=None):
     return out
 
 
+def dfa_forward_strided(qkv, cfg: AttentionConfig, out=None, lse=None, stream=None):
+    """Core on a fused projection output qkv [B, N, 3, h, d] (q | k | v column
+    blocks per token, token stride 3 h d) -> o [B, N, h, d] (dfa_forward_strided)."""
+    torch = _torch()
+    if not qkv.is_cuda or not qkv.is_contiguous() or qkv.dim() != 5 or qkv.shape[2] != 3:
+        raise DimensionError("dfa_forward_strided: qkv must be a contiguous CUDA [B, N, 3, h, d] tensor")
+    B, N, _, h, d = qkv.shape
+    out = torch.empty((B, N, h, d), dtype=qkv.dtype, device=qkv.device) if out is None else out
+    c = cfg._c()
+    es = qkv.element_size()
+    base = qkv.data_ptr()
+    ld = 3 * h * d
+    _check(lib.dfa_forward_strided(ctypes.byref(c), _dtype_code(qkv), B, base, ld, base + h * d * es, ld,
+                                   base + 2 * h * d * es, ld, out.data_ptr(), out.stride(1),
+                                   lse.data_ptr() if lse is not None else None, _stream_ptr(stream)))
+    return out
+
+
 def dilated_attention(q, k, v, cfg: AttentionConfig, head_offset: int, workers: int = 1, stream=None):
     """attention.hpp:280-301 on CUDA tensors: q, k [N, d], v [N, d_v] -> [N, d_v].
 

@@ -41,6 +41,7 @@ EXPORTED = (
     "dfa_workspace_destroy",
     "dfa_dilated_attention_host",
     "dfa_forward_host",
+    "dfa_forward_strided",
     "dfa_set_fault_perturb",
     "dfa_get_fault_perturb",
     "dfa_workspace_bytes",
@@ -139,6 +140,8 @@ def _load() -> ctypes.CDLL:
         "dfa_encoder_block_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_encoder_block_forward": (c_i32, [p_cfg, c_i32, c_i64, c_vp, ctypes.POINTER(DfaBlockWeights), c_vp, c_vp,
                                               ctypes.c_size_t, c_vp]),
+        "dfa_forward_strided": (c_i32, [p_cfg, c_i32, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                        c_vp, c_vp]),
         "dfa_tensor_header": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), p_i64]),
         "dfa_tensor_load": (c_i32, [ctypes.c_char_p, c_i32, c_vp, c_i64]),
         "dfa_tensor_save": (c_i32, [ctypes.c_char_p, c_i32, c_i32, p_i64, c_vp]),

@@ -81,6 +81,8 @@ dfa_status_t resolve(const dfa_config_t* c, int64_t batch, dfa_impl::Geometry* g
   if (g->d > 256 || g->dv > 256)
     return fail(DFA_ERR_UNSUPPORTED, "dfa_forward: head_dim %lld / value_dim %lld exceed the device limit 256",
                 (long long)g->d, (long long)g->dv);
+  g->ldq = g->ldk = g->h * g->d;
+  g->ldv = g->ldo = g->h * g->dv;
   g->n_seg = (g->N + g->w - 1) / g->w;
   g->m_max = (g->w + g->r - 1) / g->r;
   // attention.hpp:112-115: Scalar(1)/sqrt(Scalar(d)) in the working precision.
@@ -190,11 +192,19 @@ dfa_status_t dfa_query_path(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t 
 
 static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
                                  const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace,
-                                 unsigned long long* watchdog = nullptr, bool apply_fault = true);
+                                 unsigned long long* watchdog = nullptr, bool apply_fault = true,
+                                 const int64_t* ld = nullptr);
 
 dfa_status_t dfa_forward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q, const void* k,
                          const void* v, void* o, float* lse, void* stream) {
   return forward_impl(cfg, dtype, batch, q, k, v, o, lse, stream, nullptr);
+}
+
+dfa_status_t dfa_forward_strided(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                                 int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* o,
+                                 int64_t ldo, float* lse, void* stream) {
+  const int64_t ld[4] = {ldq, ldk, ldv, ldo};
+  return forward_impl(cfg, dtype, batch, q, k, v, o, lse, stream, nullptr, nullptr, true, ld);
 }
 
 dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,
@@ -211,11 +221,20 @@ dfa_status_t dfa_forward_debug(const dfa_config_t* cfg, int64_t batch, const voi
 
 static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
                                  const void* k, const void* v, void* o, float* lse, void* stream, uint64_t* trace,
-                                 unsigned long long* watchdog, bool apply_fault) {
+                                 unsigned long long* watchdog, bool apply_fault, const int64_t* ld) {
   g_launches = 0;
   dfa_impl::Geometry g;
   dfa_status_t st = resolve(cfg, batch, &g);
   if (st != DFA_OK) return st;
+  if (ld) {
+    if (ld[0] < g.h * g.d || ld[1] < g.h * g.d || ld[2] < g.h * g.dv || ld[3] < g.h * g.dv)
+      return fail(DFA_ERR_DIMENSION, "dfa_forward_strided: token strides (%lld, %lld, %lld, %lld) below h*d",
+                  (long long)ld[0], (long long)ld[1], (long long)ld[2], (long long)ld[3]);
+    g.ldq = ld[0];
+    g.ldk = ld[1];
+    g.ldv = ld[2];
+    g.ldo = ld[3];
+  }
   if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_CONFIG, "dfa_forward: unknown dtype %d", (int)dtype);
   if (batch == 0) return DFA_OK;
   if (!q || !k || !v || !o) return fail(DFA_ERR_DIMENSION, "dfa_forward: null tensor pointer");
@@ -487,7 +506,30 @@ dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t
   dfa_impl::Geometry g;
   dfa_status_t st = layer_geometry(cfg, batch, &g, "multi_head_dilated");
   if (st != DFA_OK) return st;
-  *bytes = 4 * up256((size_t)(g.B * g.N * g.h * g.d) * elem_size(dtype)) + kLtWorkspace;
+  const size_t es = elem_size(dtype), D = (size_t)(g.h * g.d);
+  *bytes = 4 * up256((size_t)(g.B * g.N) * D * es) + up256(3 * D * D * es) + kLtWorkspace;
+  return DFA_OK;
+}
+
+// x [M, D] -> qkv [M, 3, h, d] with ONE GEMM against the packed [D, 3, h, d]
+// weights, then the core reads q / k / v as column blocks (token stride 3hd).
+static dfa_status_t fused_qkv_attention(const dfa_config_t* cfg, dfa_dtype_t dtype, const dfa_impl::Geometry& g,
+                                        const void* x, const void* wq, const void* wk, const void* wv, char* qkv,
+                                        char* wpack, void* att, void* lt, cudaStream_t s, int* launches,
+                                        const char* who) {
+  const int64_t M = g.B * g.N, D = g.h * g.d;
+  const char* why = "";
+  *launches += dfa_impl::launch_pack_qkv(dtype, wq, wk, wv, wpack, g.h, D, g.d, s);
+  if (!dfa_impl::gemm_rowmajor(dtype, M, 3 * D, D, x, D, 0, wpack, 3 * D, 0, qkv, 3 * D, 0, nullptr, 0, 0.0f, nullptr,
+                               1, lt, kLtWorkspace, s, &why))
+    return fail(DFA_ERR_CUDA, "%s: QKV projection: %s", who, why);
+  ++*launches;
+  const size_t es = elem_size(dtype);
+  const int64_t ld[4] = {3 * D, 3 * D, 3 * D, D};
+  dfa_status_t st = forward_impl(cfg, dtype, g.B, qkv, qkv + D * es, qkv + 2 * D * es, att, nullptr,
+                                 reinterpret_cast<void*>(s), nullptr, nullptr, false, ld);
+  if (st != DFA_OK) return st;
+  *launches += g_launches;
   return DFA_OK;
 }
 
@@ -505,27 +547,21 @@ dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, 
   if (batch == 0) return DFA_OK;
   if (!x || !wq || !wk || !wv || !wo || !out) return fail(DFA_ERR_DIMENSION, "multi_head_dilated: null pointer");
   const int64_t M = g.B * g.N, D = g.h * g.d;
-  const size_t act = up256((size_t)(M * D) * elem_size(dtype));
+  const size_t es = elem_size(dtype), act = up256((size_t)(M * D) * es);
   char* base = static_cast<char*>(workspace);
-  void* qkv[3] = {base, base + act, base + 2 * act};
-  void* att = base + 3 * act;
-  void* lt = base + 4 * act;
+  char* qkv = base;                   // [M, 3, h, d]
+  void* att = base + 3 * act;         // [M, h, d]
+  char* wpack = base + 4 * act;       // [D, 3, h, d]
+  void* lt = wpack + up256((size_t)(3 * D * D) * es);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const char* why = "";
-  const void* w3[3] = {wq, wk, wv};
   int launches = 0;
-  for (int i = 0; i < 3; ++i) {  // x [M, D] . w_j [D, d] -> column block j of [M, h*d], one batched call
-    if (!dfa_impl::gemm_rowmajor(dtype, M, g.d, D, x, D, 0, w3[i], g.d, D * g.d, qkv[i], D, g.d, nullptr, 0, 0.0f,
-                                 nullptr, (int)g.h, lt, kLtWorkspace, s, &why))
-      return fail(DFA_ERR_CUDA, "multi_head_dilated: projection: %s", why);
-    ++launches;
-  }
-  st = dfa_forward(cfg, dtype, batch, qkv[0], qkv[1], qkv[2], att, nullptr, stream);
+  st = fused_qkv_attention(cfg, dtype, g, x, wq, wk, wv, qkv, wpack, att, lt, s, &launches, "multi_head_dilated");
   if (st != DFA_OK) return st;
-  launches += g_launches;
+  const char* why = "";
   if (!dfa_impl::gemm_rowmajor(dtype, M, D, D, att, D, 0, wo, D, 0, out, D, 0, nullptr, 0, 0.0f, nullptr, 1, lt,
                                kLtWorkspace, s, &why))
     return fail(DFA_ERR_CUDA, "multi_head_dilated: output projection: %s", why);
+  if (g_fault.load()) launches += dfa_impl::launch_perturb(dtype, out, s);
   g_launches = launches + 1;
   return DFA_OK;
 }
@@ -536,9 +572,9 @@ dfa_status_t dfa_encoder_block_workspace_bytes(const dfa_config_t* cfg, dfa_dtyp
   dfa_status_t st = layer_geometry(cfg, batch, &g, "encoder_block");
   if (st != DFA_OK) return st;
   if (hidden < 1) return fail(DFA_ERR_CONFIG, "encoder: mlp_ratio must yield a positive width");
-  const size_t es = elem_size(dtype);
-  const size_t act = up256((size_t)(g.B * g.N * g.h * g.d) * es);
-  *bytes = 6 * act + up256((size_t)(g.B * g.N * hidden) * es) + kLtWorkspace;
+  const size_t es = elem_size(dtype), D = (size_t)(g.h * g.d);
+  const size_t act = up256((size_t)(g.B * g.N) * D * es);
+  *bytes = 6 * act + up256((size_t)(g.B * g.N * hidden) * es) + up256(3 * D * D * es) + kLtWorkspace;
   return DFA_OK;
 }
 
@@ -565,11 +601,12 @@ dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtyp
   const size_t es = elem_size(dtype), act = up256((size_t)(M * D) * es);
   char* base = static_cast<char*>(workspace);
   void* ln = base;
-  void* qkv[3] = {base + act, base + 2 * act, base + 3 * act};
+  char* qkv = base + act;        // [M, 3, h, d]
   void* att = base + 4 * act;
   void* x1 = base + 5 * act;
-  void* hid = base + 6 * act;
-  void* lt = base + 6 * act + up256((size_t)(M * H) * es);
+  char* hid = base + 6 * act;
+  char* wpack = hid + up256((size_t)(M * H) * es);
+  void* lt = wpack + up256((size_t)(3 * D * D) * es);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const char* why = "";
   int launches = 0;
@@ -580,16 +617,9 @@ dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtyp
                                    kLtWorkspace, s, &why);
   };
   launches += dfa_impl::launch_layer_norm(dtype, x, wt->ln1_g, wt->ln1_b, ln, M, (int)D, s);
-  const void* w3[3] = {wt->wq, wt->wk, wt->wv};
-  for (int i = 0; i < 3; ++i) {
-    ++launches;
-    if (!dfa_impl::gemm_rowmajor(dtype, M, g.d, D, ln, D, 0, w3[i], g.d, D * g.d, qkv[i], D, g.d, nullptr, 0, 0.0f,
-                                 nullptr, (int)g.h, lt, kLtWorkspace, s, &why))
-      return fail(DFA_ERR_CUDA, "encoder_block: projection: %s", why);
-  }
-  st = dfa_forward(cfg, dtype, batch, qkv[0], qkv[1], qkv[2], att, nullptr, stream);
+  st = fused_qkv_attention(cfg, dtype, g, ln, wt->wq, wt->wk, wt->wv, qkv, wpack, att, lt, s, &launches,
+                           "encoder_block");
   if (st != DFA_OK) return st;
-  launches += g_launches;
   if (!gemm(M, D, D, att, wt->wo, x1, x, wt->bo)) return fail(DFA_ERR_CUDA, "encoder_block: wo: %s", why);
   launches += dfa_impl::launch_layer_norm(dtype, x1, wt->ln2_g, wt->ln2_b, ln, M, (int)D, s);
   if (!gemm(M, H, D, ln, wt->w1, hid, nullptr, wt->b1)) return fail(DFA_ERR_CUDA, "encoder_block: w1: %s", why);

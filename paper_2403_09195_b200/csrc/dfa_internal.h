@@ -15,6 +15,7 @@ struct Geometry {
   int64_t n_seg;  // ceil(N / w)            attention.hpp:35
   int64_t m_max;  // ceil(w / r): rows per full view
   float scale;    // 1/sqrt(d) or 1         attention.hpp:112-115
+  int64_t ldq, ldk, ldv, ldo;  // token (row) strides in elements; h*d / h*dv when contiguous
   int32_t offsets[kMaxHeads];
 };
 
@@ -53,6 +54,9 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
                       cudaStream_t stream);
 int launch_gelu(int dtype, void* x, int64_t n, cudaStream_t stream);
+// wq/wk/wv [h, D, d] -> packed [D, 3, h, d] (one QKV GEMM writes q|k|v per token).
+int launch_pack_qkv(int dtype, const void* wq, const void* wk, const void* wv, void* out, int64_t h, int64_t D,
+                    int64_t d, cudaStream_t stream);
 
 // Fault hook (attention.hpp:272): out[0] += 1e-3.
 int launch_perturb(int dtype, void* o, cudaStream_t stream);

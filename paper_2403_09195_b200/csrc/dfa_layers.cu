@@ -95,6 +95,20 @@ __global__ void __launch_bounds__(256) gelu_kernel(T* __restrict__ x, int64_t n)
   }
 }
 
+// wq/wk/wv [h, D, d] -> [D, 3, h, d]: column block (which, j) of the fused
+// QKV projection is head j's D x d matrix of q / k / v.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_qkv_kernel(const T* __restrict__ wq, const T* __restrict__ wk,
+                                                       const T* __restrict__ wv, T* __restrict__ out, int64_t h,
+                                                       int64_t D, int64_t d) {
+  const int64_t n = 3 * D * h * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i % d, j = (i / d) % h, which = (i / (d * h)) % 3, c = i / (3 * h * d);
+    const T* src = which == 0 ? wq : (which == 1 ? wk : wv);
+    out[i] = src[(j * D + c) * d + e];
+  }
+}
+
 struct LtHandle {
   cublasLtHandle_t h = nullptr;
   ~LtHandle() {
@@ -185,6 +199,18 @@ int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, vo
     layer_norm_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
                                                                (const __nv_bfloat16*)b, (__nv_bfloat16*)y, rows,
                                                                cols);
+  return 1;
+}
+
+int launch_pack_qkv(int dtype, const void* wq, const void* wk, const void* wv, void* out, int64_t h, int64_t D,
+                    int64_t d, cudaStream_t stream) {
+  const unsigned grid = (unsigned)std::min<int64_t>((3 * D * h * d + 255) / 256, 148 * 8);
+  if (dtype == 0)
+    pack_qkv_kernel<float><<<grid, 256, 0, stream>>>((const float*)wq, (const float*)wk, (const float*)wv,
+                                                     (float*)out, h, D, d);
+  else
+    pack_qkv_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)wq, (const __nv_bfloat16*)wk,
+                                                             (const __nv_bfloat16*)wv, (__nv_bfloat16*)out, h, D, d);
   return 1;
 }
 

@@ -21,6 +21,7 @@ namespace {
 
 struct SimtParams {
   int64_t N, w, r, h, d, dv, n_chunks;
+  int64_t ldq, ldk, ldv, ldo;  // token strides (elements)
   float scale;
   int32_t offsets[kMaxHeads];
 };
@@ -63,18 +64,17 @@ __global__ void __launch_bounds__(128) simt_kernel(const T* __restrict__ q, cons
   const int64_t seg_end = min(seg_begin + p.w, p.N);
   const int64_t seg_rows = seg_end - seg_begin;
   const int64_t m = g >= seg_rows ? 0 : (seg_rows - g + p.r - 1) / p.r;  // attention.hpp:96
-  const int64_t hd = p.h * p.d, hdv = p.h * p.dv;
-  const T* qb = q + b * p.N * hd + j * p.d;
-  const T* kb = k + b * p.N * hd + j * p.d;
-  const T* vb = v + b * p.N * hdv + j * p.dv;
-  T* ob = o + b * p.N * hdv + j * p.dv;
+  const T* qb = q + b * p.N * p.ldq + j * p.d;
+  const T* kb = k + b * p.N * p.ldk + j * p.d;
+  const T* vb = v + b * p.N * p.ldv + j * p.dv;
+  T* ob = o + b * p.N * p.ldo + j * p.dv;
   float* lb = lse ? lse + (b * p.h + j) * p.N : nullptr;
 
   // Rows of this segment that the view does not select: exact zeros.
   if (chunk == 0) {
     for (int64_t l = tid; l < seg_rows; l += blockDim.x) {
       if (l % p.r == g && l >= g) continue;
-      T* orow = ob + (seg_begin + l) * hdv;
+      T* orow = ob + (seg_begin + l) * p.ldo;
       for (int64_t c = 0; c < p.dv; ++c) orow[c] = from_f<T>(0.0f);
       if (lb) lb[seg_begin + l] = -INFINITY;
     }
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(128) simt_kernel(const T* __restrict__ q, cons
   float qr[DMAX], acc[DMAX];
 #pragma unroll
   for (int c = 0; c < DMAX; ++c) {
-    qr[c] = (active && c < p.d) ? to_f(qb[row * hd + c]) : 0.0f;
+    qr[c] = (active && c < p.d) ? to_f(qb[row * p.ldq + c]) : 0.0f;
     acc[c] = 0.0f;
   }
   float mx = -INFINITY, l = 0.0f;
@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(128) simt_kernel(const T* __restrict__ q, cons
       const int jj = e / DMAX, c = e % DMAX;
       const int64_t tk = k0 + jj;
       const int64_t krow = seg_begin + g + tk * p.r;
-      ks[jj][c] = (tk < m && c < p.d) ? to_f(kb[krow * hd + c]) : 0.0f;
-      vs[jj][c] = (tk < m && c < p.dv) ? to_f(vb[krow * hdv + c]) : 0.0f;
+      ks[jj][c] = (tk < m && c < p.d) ? to_f(kb[krow * p.ldk + c]) : 0.0f;
+      vs[jj][c] = (tk < m && c < p.dv) ? to_f(vb[krow * p.ldv + c]) : 0.0f;
     }
     __syncthreads();
     if (!active) continue;
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(128) simt_kernel(const T* __restrict__ q, cons
   }
   if (active) {
     const float inv = 1.0f / l;
-    T* orow = ob + row * hdv;
+    T* orow = ob + row * p.ldo;
 #pragma unroll
     for (int c = 0; c < DMAX; ++c)
       if (c < p.dv) orow[c] = from_f<T>(acc[c] * inv);
@@ -147,6 +147,10 @@ int launch_t(const Geometry& g, const void* q, const void* k, const void* v, voi
   p.h = g.h;
   p.d = g.d;
   p.dv = g.dv;
+  p.ldq = g.ldq;
+  p.ldk = g.ldk;
+  p.ldv = g.ldv;
+  p.ldo = g.ldo;
   p.n_chunks = (g.m_max + 127) / 128;
   if (p.n_chunks < 1) p.n_chunks = 1;
   p.scale = g.scale;

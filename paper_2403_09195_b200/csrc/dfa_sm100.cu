@@ -739,13 +739,14 @@ EncodeTiledFn get_encode_fn() {
 
 // [B][N/r][r][h][64] bf16 view; box (64, 1, 1, 128, 1), 128-byte swizzle.
 // The t' extent is N/r per image, so boxes never cross into the next image:
-// out-of-range rows are zero-filled on load and dropped on store.
-bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h) {
+// out-of-range rows are zero-filled on load and dropped on store.  `ld` is
+// the token stride in elements (h * 64 when contiguous; 3 * h * 64 when q,
+// k, v are column blocks of one fused-projection output).
+bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[5] = {(cuuint64_t)kD, (cuuint64_t)h, (cuuint64_t)r, (cuuint64_t)(N / r), (cuuint64_t)B};
-  cuuint64_t strides[4] = {(cuuint64_t)kD * 2, (cuuint64_t)h * kD * 2, (cuuint64_t)r * h * kD * 2,
-                           (cuuint64_t)N * h * kD * 2};
+  cuuint64_t strides[4] = {(cuuint64_t)kD * 2, (cuuint64_t)ld * 2, (cuuint64_t)r * ld * 2, (cuuint64_t)N * ld * 2};
   cuuint32_t box[5] = {kD, 1, 1, 128, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
@@ -776,6 +777,8 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
   if (g.h > kMaxHeads) return false;
   auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
   if (!al(q) || !al(k) || !al(v) || !al(o)) return false;
+  for (int64_t ld : {g.ldq, g.ldk, g.ldv, g.ldo})  // TMA global strides: multiples of 16 B
+    if (ld % 8 != 0) return false;
   if (g.N > (int64_t)INT32_MAX / 2 || g.B > (int64_t)INT32_MAX) return false;  // TMA coordinates are int32
   const int64_t units = g.B * g.h * ((g.N / g.r + kUnitRows - 1) / kUnitRows);
   if (units > (int64_t)INT32_MAX) return false;
@@ -791,8 +794,8 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
     return 0;
   }
   CUtensorMap mq, mk, mv, mo;
-  if (!make_map(&mq, q, g.B, g.N, g.r, g.h) || !make_map(&mk, k, g.B, g.N, g.r, g.h) ||
-      !make_map(&mv, v, g.B, g.N, g.r, g.h) || !make_map(&mo, o, g.B, g.N, g.r, g.h)) {
+  if (!make_map(&mq, q, g.B, g.N, g.r, g.h, g.ldq) || !make_map(&mk, k, g.B, g.N, g.r, g.h, g.ldk) ||
+      !make_map(&mv, v, g.B, g.N, g.r, g.h, g.ldv) || !make_map(&mo, o, g.B, g.N, g.r, g.h, g.ldo)) {
     *why = "cuTensorMapEncodeTiled failed";
     *err = cudaErrorInvalidValue;
     return 0;

@@ -402,3 +402,24 @@ def test_multibranch_fault_hook_once(dfa, cuda):
     d = (b.float() - a.float()).flatten()
     assert d[1:].abs().max().item() == 0.0
     assert abs(d[0].item() - 1e-3) <= 8e-3  # bf16 rounding of o[0] + 1e-3
+
+
+@pytest.mark.parametrize("dt,w,r", [("bf16", 512, 2), ("bf16", 256, 4), ("f32", 512, 2), ("bf16", 300, 3)])
+def test_strided_qkv_equals_contiguous(dfa, cuda, dt, w, r):
+    """dfa_forward_strided on q|k|v column blocks of one [B, N, 3, h, d]
+    buffer (the fused projection output) is bit-identical to dfa_forward on
+    contiguous copies, on both device paths."""
+    torch = _torch()
+    td = torch.float32 if dt == "f32" else torch.bfloat16
+    B, n, h, d = 2, 1200 if w == 300 else 2048, 6, 64
+    g = torch.Generator(device="cuda").manual_seed(w * r)
+    qkv = torch.randn((B, n, 3, h, d), device="cuda", dtype=td, generator=g)
+    cfg = make_cfg(dfa, n, w, r, h, d)
+    L1 = torch.empty((B, h, n), dtype=torch.float32, device="cuda")
+    L2 = torch.empty_like(L1)
+    a = dfa.dfa_forward_strided(qkv, cfg, lse=L1)
+    q, k, v = (qkv[:, :, i].contiguous() for i in range(3))
+    b = dfa.dfa_forward(q, k, v, cfg, lse=L2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert torch.equal(L1, L2)
