@@ -480,9 +480,12 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
   if (!workspace || ws_bytes < need)
     return fail(DFA_ERR_DIMENSION, "dfa_backward: workspace has %zu bytes, needs %zu", ws_bytes, need);
   cudaError_t err = cudaSuccess;
+  const char* why = "";
+  const bool allow = g_path_override.load() != DFA_PATH_SIMT;
   const int n = dfa_impl::launch_backward(g, dtype, q, k, v, o, dout, lse, static_cast<float*>(workspace), dq, dk, dv,
-                                          reinterpret_cast<cudaStream_t>(stream), &err);
-  if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "dfa_backward: launch failed: %s", cudaGetErrorString(err));
+                                          reinterpret_cast<cudaStream_t>(stream), &err, allow, &why);
+  if (err != cudaSuccess || n == 0)
+    return fail(DFA_ERR_CUDA, "dfa_backward: launch failed: %s (%s)", cudaGetErrorString(err), why);
   g_launches = n;
   return DFA_OK;
 }

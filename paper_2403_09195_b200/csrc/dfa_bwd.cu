@@ -309,7 +309,15 @@ int launch_bwd_dtype(const Geometry& g, const void* q, const void* k, const void
 
 int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o,
                     const void* dout, const float* lse, float* delta, void* dq, void* dk, void* dv,
-                    cudaStream_t stream, cudaError_t* err) {
+                    cudaStream_t stream, cudaError_t* err, bool allow_sm100, const char** why) {
+  const void* ptrs[] = {q, k, v, dout, dq, dk, dv};
+  if (allow_sm100 && bwd_sm100_supported(g, dtype, ptrs, 7)) {
+    const int64_t rows = g.B * g.N * g.h;
+    delta_kernel<__nv_bfloat16><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, stream>>>(
+        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, delta, rows, g.N, g.h, g.dv);
+    const int n = launch_bwd_sm100(g, q, k, v, dout, lse, delta, dq, dk, dv, stream, err, why);
+    return n ? n + 1 : 0;
+  }
   if (dtype == 0) return launch_bwd_dtype<float>(g, q, k, v, o, dout, lse, delta, dq, dk, dv, stream, err);
   return launch_bwd_dtype<__nv_bfloat16>(g, q, k, v, o, dout, lse, delta, dq, dk, dv, stream, err);
 }

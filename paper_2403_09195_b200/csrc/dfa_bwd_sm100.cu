@@ -1,0 +1,359 @@
+// Backward of the Dilated Flash Attention core on sm_100a: TMA + tcgen05 +
+// TMEM (bf16 in/out, fp32 accumulate), for segments whose view holds
+// m = w / r in {128, 256} rows (r | w, w | N, d = d_v = 64) -- e.g. the
+// headline (512, 2) and every m = 256 branch of BASELINE config 4.  Other
+// geometries take the SIMT kernels in dfa_bwd.cu.
+//
+// Math (same as dfa_bwd.cu; the reference's tape for the dilated branch of
+// attention_mix, encoder.hpp:204-219): with P = exp(S sc - lse),
+// Delta = rowsum(dO o O) (delta_kernel), dS = P o (dP - Delta):
+//   dV = P^T dO,  dK = sc dS^T Q,  dQ = sc dS K.
+//
+// One CTA per (image, head, segment); the whole view (Q, K, V, dO: m x 64
+// each) is TMA-loaded once into shared memory as 128-row SW128 tiles of the
+// t'-stream (the forward's index mapping: no gather).  For key block kb and
+// query block qb (128 each), one elected thread issues
+//   S^T  = K_kb Q_qb^T            (M=128 keys, N=128 queries)  -> TMEM [0,128)
+//   dP^T = V_kb dO_qb^T                                         -> TMEM [128,256)
+// the 128-thread gradient warpgroup (thread = key row = TMEM lane) turns them
+// into P^T (bf16 over S^T's columns) and dS^T (bf16 over dP^T's columns, and
+// into shared memory as the MN-major A operand of dQ), then
+//   dV_kb += P^T dO_qb   (A = P^T from TMEM, B = dO MN-major)   -> TMEM [256,320)
+//   dK_kb += dS^T Q_qb   (A = dS^T from TMEM, B = Q MN-major)   -> TMEM [320,384)
+//   dQ_qb += dS K_kb     (A = dS from smem, MN-major; B = K MN-major) -> TMEM [384 + 64 qb, ...)
+// dK/dV leave after a key block, dQ after the last one: TMEM -> bf16 -> SW128
+// staging -> TMA store, plus zero boxes for the rows of the other offset
+// classes (their gradient is 0).  Deterministic: no atomics, every output
+// element written once.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <mutex>
+
+#include "dfa_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace dfa_impl {
+namespace {
+
+constexpr int kD = 64;
+constexpr int kB = 128;                // rows per tile (keys / queries)
+constexpr int kTile = 128 * 128;       // 128 rows x 128 B (64 bf16), SW128
+constexpr int kMaxBlk = 2;             // m <= 256
+constexpr int kThreads = 256;          // warp 0: TMA + MMA, warp 1: TMEM alloc, warps 4-7: gradient WG
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct __align__(1024) BwdSmem {
+  uint8_t q[kMaxBlk][kTile];
+  uint8_t k[kMaxBlk][kTile];
+  uint8_t v[kMaxBlk][kTile];
+  uint8_t g[kMaxBlk][kTile];      // dO
+  uint8_t ds[2][kTile];           // dS^T as the MN-major A operand: queries [0,64) | [64,128)
+  uint8_t stage[2][kTile];        // output staging (dK | dV, then dQ blocks)
+  uint8_t zero[kTile];
+  float lse2[kMaxBlk * kB];       // lse * log2(e) of the view's query rows
+  float dlt[kMaxBlk * kB];        // Delta of the view's query rows
+  uint64_t load_full, s_full, p_full, kv_done, q_done;
+  uint32_t tmem_base;
+};
+
+struct BwdSm100Params {
+  int32_t N, T, m, r, h, n_seg, nblk;
+  float c, scale;
+  int32_t offsets[kMaxHeads];
+};
+
+__device__ __forceinline__ void wait(uint64_t* bar, uint32_t par) { ptx::mbar_wait(bar, par); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    dfa_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
+                         const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dk,
+                         const __grid_constant__ CUtensorMap tm_dv, const float* __restrict__ lse,
+                         const float* __restrict__ delta, const __grid_constant__ BwdSm100Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  BwdSmem& sm = *reinterpret_cast<BwdSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int32_t seg = blockIdx.x % p.n_seg;
+  const int32_t bj = blockIdx.x / p.n_seg;
+  const int32_t j = bj % p.h, b = bj / p.h;
+  const int32_t gamma = p.offsets[j];
+  const int32_t t0 = seg * p.m;  // first t' of the view
+  const int nb = p.nblk;
+
+  for (uint32_t i = threadIdx.x; i < kTile / 16; i += kThreads) ptx::st_shared_v4(ptx::smem_u32(sm.zero) + 16 * i, 0, 0, 0, 0);
+  if (threadIdx.x >= 128) {  // gradient warpgroup: the view's lse (log2 units) and Delta
+    const int t = threadIdx.x - 128;
+    const float* lb = lse + ((int64_t)b * p.h + j) * p.N;
+    const float* db = delta + ((int64_t)b * p.h + j) * p.N;
+    for (int tt = t; tt < nb * kB; tt += 128) {
+      const int64_t n = (int64_t)(t0 + tt) * p.r + gamma;
+      sm.lse2[tt] = lb[n] * kLog2e;
+      sm.dlt[tt] = db[n];
+    }
+  }
+  ptx::fence_proxy_async_smem();
+  if (warp == 0 && lane == 0) {
+    ptx::mbar_init(&sm.load_full, 1);
+    ptx::mbar_init(&sm.s_full, 1);
+    ptx::mbar_init(&sm.p_full, kB);
+    ptx::mbar_init(&sm.kv_done, 1);
+    ptx::mbar_init(&sm.q_done, 1);
+    ptx::fence_barrier_init();
+  } else if (warp == 1) {
+    ptx::tmem_alloc<512>(&sm.tmem_base);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+  constexpr uint32_t cS = 0, cDP = 128, cDV = 256, cDK = 320, cDQ = 384;
+
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      // ---------------------------------------------------------- loads
+      const uint64_t pol = ptx::policy_evict_first();
+      ptx::mbar_arrive_expect_tx(&sm.load_full, 4 * nb * kTile);
+      for (int blk = 0; blk < nb; ++blk) {
+        const int32_t tb = t0 + blk * kB;
+        ptx::tma_load_5d(sm.q[blk], &tm_q, &sm.load_full, 0, j, gamma, tb, b, pol);
+        ptx::tma_load_5d(sm.k[blk], &tm_k, &sm.load_full, 0, j, gamma, tb, b, pol);
+        ptx::tma_load_5d(sm.v[blk], &tm_v, &sm.load_full, 0, j, gamma, tb, b, pol);
+        ptx::tma_load_5d(sm.g[blk], &tm_g, &sm.load_full, 0, j, gamma, tb, b, pol);
+      }
+      wait(&sm.load_full, 0);
+      ptx::tc_fence_after();
+      // ------------------------------------------------------------ MMA
+      constexpr uint32_t id_ss = ptx::idesc_bf16(kB, kB, 0, 0);   // S^T, dP^T: K-major A and B
+      constexpr uint32_t id_ts = ptx::idesc_bf16(kB, kD, 0, 1);   // dV, dK: A from TMEM, B MN-major
+      constexpr uint32_t id_dq = ptx::idesc_bf16(kB, kD, 1, 1);   // dQ: A (dS) MN-major, B (K) MN-major
+      uint32_t step = 0;
+      for (int kb = 0; kb < nb; ++kb) {
+        const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k[kb]));
+        const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v[kb]));
+        for (int qb = 0; qb < nb; ++qb, ++step) {
+          const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[qb]));
+          const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[qb]));
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            ptx::mma_ss(tbase + cS, kd + 2 * kk, qd + 2 * kk, id_ss, kk > 0);
+            ptx::mma_ss(tbase + cDP, vd + 2 * kk, gd + 2 * kk, id_ss, kk > 0);
+          }
+          ptx::tc_commit(&sm.s_full);
+          wait(&sm.p_full, step & 1);
+          ptx::tc_fence_after();
+          const uint64_t dsd = ptx::sdesc_sw128(ptx::smem_u32(sm.ds[0]), 1024, kTile);  // LBO: next 64 queries
+#pragma unroll
+          for (int kk = 0; kk < kB / 16; ++kk) {
+            // K-step of 16 queries: 8 packed TMEM columns of P^T / dS^T, 16 rows (2048 B) of dO / Q
+            ptx::mma_ts(tbase + cDV, tbase + cS + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_ts(tbase + cDK, tbase + cDP + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < kB / 16; ++kk)  // K-step of 16 keys: 16 rows of dS / K
+            ptx::mma_ss(tbase + cDQ + 64 * qb, dsd + kk * 128, kd + kk * 128, id_dq, (kb > 0 || kk > 0) ? 1u : 0u);
+        }
+        ptx::tc_commit(&sm.kv_done);
+      }
+      ptx::tc_commit(&sm.q_done);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ gradient warpgroup
+    const uint32_t row = (warp - 4) * 32 + lane;  // key row (TMEM lane) / query row for dQ
+    const uint32_t lane_base = ((warp - 4) * 32) << 16;
+    const bool leader = warp == 4 && lane == 0;
+    uint32_t step = 0;
+    auto stage_store = [&](uint8_t* st, const uint32_t (&v)[2][32], float mul) {
+      const uint32_t a0 = ptx::smem_u32(st);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float* f = reinterpret_cast<const float*>(&v[c >> 2][(c & 3) * 8]);
+        ptx::st_shared_v4(a0 + row * 128 + ((c ^ (row & 7)) * 16), ptx::pack_bf16x2(f[0] * mul, f[1] * mul),
+                          ptx::pack_bf16x2(f[2] * mul, f[3] * mul), ptx::pack_bf16x2(f[4] * mul, f[5] * mul),
+                          ptx::pack_bf16x2(f[6] * mul, f[7] * mul));
+      }
+    };
+    for (int kb = 0; kb < nb; ++kb) {
+      for (int qb = 0; qb < nb; ++qb, ++step) {
+        wait(&sm.s_full, step & 1);
+        ptx::tc_fence_after();
+        const float* l2 = sm.lse2 + qb * kB;
+        const float* dl = sm.dlt + qb * kB;
+        const uint32_t dsa = ptx::smem_u32(sm.ds[0]);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {  // 32 queries per chunk
+          uint32_t s[32], dp[32];
+          ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, s);
+          ptx::tmem_ld32(tbase + lane_base + cDP + 32 * c, dp);
+          ptx::tmem_ld_wait();
+          uint32_t pp[16], dd[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int q0 = 32 * c + 2 * e;
+            const float p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
+            const float p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
+            pp[e] = ptx::pack_bf16x2(p0, p1);
+            dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl[q0]),
+                                     p1 * (__uint_as_float(dp[2 * e + 1]) - dl[q0 + 1]));
+          }
+          ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
+          ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
+          // dS^T row `row` (key) -> MN-major A of dQ: queries 32c..32c+31 are
+          // 16-byte chunks 4(c&1)..4(c&1)+3 of sub-tile c>>1, SW128-swizzled
+          const uint32_t sub = dsa + (c >> 1) * kTile + row * 128;
+#pragma unroll
+          for (int h4 = 0; h4 < 4; ++h4) {
+            const uint32_t chunk = 4 * (c & 1) + h4;
+            ptx::st_shared_v4(sub + ((chunk ^ (row & 7)) * 16), dd[4 * h4], dd[4 * h4 + 1], dd[4 * h4 + 2],
+                              dd[4 * h4 + 3]);
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.p_full);
+      }
+      // dK, dV of key block kb
+      wait(&sm.kv_done, kb & 1);
+      ptx::tc_fence_after();
+      uint32_t a[2][32];
+      if (leader) ptx::tma_store_wait_read<0>();
+      ptx::named_bar_sync(1, 128);
+      ptx::tmem_ld32(tbase + lane_base + cDV, a[0]);
+      ptx::tmem_ld32(tbase + lane_base + cDV + 32, a[1]);
+      ptx::tmem_ld_wait();
+      stage_store(sm.stage[1], a, 1.0f);
+      ptx::tmem_ld32(tbase + lane_base + cDK, a[0]);
+      ptx::tmem_ld32(tbase + lane_base + cDK + 32, a[1]);
+      ptx::tmem_ld_wait();
+      stage_store(sm.stage[0], a, p.scale);
+      ptx::tc_fence_before();
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (leader) {
+        const int32_t tb = t0 + kb * kB;
+        ptx::tma_store_5d(&tm_dk, sm.stage[0], 0, j, gamma, tb, b);
+        ptx::tma_store_5d(&tm_dv, sm.stage[1], 0, j, gamma, tb, b);
+        for (int32_t gz = 0; gz < p.r; ++gz)
+          if (gz != gamma) {
+            ptx::tma_store_5d(&tm_dk, sm.zero, 0, j, gz, tb, b);
+            ptx::tma_store_5d(&tm_dv, sm.zero, 0, j, gz, tb, b);
+            ptx::tma_store_5d(&tm_dq, sm.zero, 0, j, gz, tb, b);
+          }
+        ptx::tma_store_commit();
+      }
+    }
+    // dQ blocks (TMEM lanes = query rows)
+    wait(&sm.q_done, 0);
+    ptx::tc_fence_after();
+    for (int qb = 0; qb < nb; ++qb) {
+      uint32_t a[2][32];
+      if (leader) ptx::tma_store_wait_read<0>();
+      ptx::named_bar_sync(1, 128);
+      ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb, a[0]);
+      ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb + 32, a[1]);
+      ptx::tmem_ld_wait();
+      stage_store(sm.stage[qb & 1], a, p.scale);
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (leader) {
+        ptx::tma_store_5d(&tm_dq, sm.stage[qb & 1], 0, j, gamma, t0 + qb * kB, b);
+        ptx::tma_store_commit();
+      }
+    }
+    if (leader) ptx::tma_store_wait_all<0>();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tbase);
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+// The forward's t'-stream view [B][N/r][r][h][64], box (64, 1, 1, 128, 1), SW128.
+bool map5(CUtensorMap* map, const void* base, const Geometry& g) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const int64_t ld = g.h * kD;
+  cuuint64_t dims[5] = {(cuuint64_t)kD, (cuuint64_t)g.h, (cuuint64_t)g.r, (cuuint64_t)(g.N / g.r), (cuuint64_t)g.B};
+  cuuint64_t strides[4] = {(cuuint64_t)kD * 2, (cuuint64_t)ld * 2, (cuuint64_t)(g.r * ld * 2),
+                           (cuuint64_t)(g.N * ld * 2)};
+  cuuint32_t box[5] = {kD, 1, 1, 128, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool bwd_sm100_supported(const Geometry& g, int dtype, const void* const* ptrs, int n_ptrs) {
+  if (dtype != 1 || g.d != kD || g.dv != kD) return false;
+  if (g.N % g.w != 0 || g.w % g.r != 0) return false;
+  const int64_t m = g.w / g.r;
+  if (m != 128 && m != 256) return false;
+  if (g.h > kMaxHeads || g.N > (int64_t)INT32_MAX / 2 || g.B * g.h * (g.N / g.w) > (int64_t)INT32_MAX) return false;
+  for (int i = 0; i < n_ptrs; ++i)
+    if (reinterpret_cast<uintptr_t>(ptrs[i]) & 15u) return false;
+  return true;
+}
+
+int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void* v, const void* dout,
+                     const float* lse, const float* delta, void* dq, void* dk, void* dv, cudaStream_t stream,
+                     cudaError_t* err, const char** why) {
+  CUtensorMap mq, mk, mv, mg, mdq, mdk, mdv;
+  if (!map5(&mq, q, g) || !map5(&mk, k, g) || !map5(&mv, v, g) || !map5(&mg, dout, g) || !map5(&mdq, dq, g) ||
+      !map5(&mdk, dk, g) || !map5(&mdv, dv, g)) {
+    *why = "cuTensorMapEncodeTiled failed";
+    *err = cudaErrorInvalidValue;
+    return 0;
+  }
+  BwdSm100Params p;
+  p.N = (int32_t)g.N;
+  p.T = (int32_t)(g.N / g.r);
+  p.m = (int32_t)(g.w / g.r);
+  p.r = (int32_t)g.r;
+  p.h = (int32_t)g.h;
+  p.n_seg = (int32_t)(g.N / g.w);
+  p.nblk = p.m / kB;
+  p.scale = g.scale;
+  p.c = g.scale * kLog2e;
+  for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
+  const size_t smem = sizeof(BwdSmem) + 1024;
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [&] {
+    attr = cudaFuncSetAttribute(dfa_bwd_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr != cudaSuccess) {
+    *err = attr;
+    *why = "cudaFuncSetAttribute failed";
+    return 0;
+  }
+  const unsigned grid = (unsigned)(g.B * g.h * p.n_seg);
+  dfa_bwd_sm100_kernel<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mg, mdq, mdk, mdv, lse, delta, p);
+  *err = cudaGetLastError();
+  return 1;
+}
+
+}  // namespace dfa_impl

@@ -42,9 +42,14 @@ int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int n
 constexpr int kMaxBranches = 8;
 
 // Backward of the dilated core (dfa_bwd.cu): delta = workspace [B, h, N] fp32.
+// allow_sm100: take the tcgen05 kernel (dfa_bwd_sm100.cu) when it covers the call.
 int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o,
                     const void* dout, const float* lse, float* delta, void* dq, void* dk, void* dv,
-                    cudaStream_t stream, cudaError_t* err);
+                    cudaStream_t stream, cudaError_t* err, bool allow_sm100, const char** why);
+bool bwd_sm100_supported(const Geometry& g, int dtype, const void* const* ptrs, int n_ptrs);
+int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void* v, const void* dout,
+                     const float* lse, const float* delta, void* dq, void* dk, void* dv, cudaStream_t stream,
+                     cudaError_t* err, const char** why);
 
 // dfa_layers.cu: cuBLASLt row-major GEMM D = A B (+ bias) (+ beta C), strided
 // batch; LayerNorm (eps 1e-5) and erf-GELU kernels.  Return 0 on failure.

@@ -16,9 +16,11 @@
 // fp32 runs with CUBLAS_COMPUTE_32F (no TF32) as the validation mode.
 #include <cublasLt.h>
 #include <cuda_bf16.h>
+#include <dlfcn.h>
 #include <math.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "dfa_internal.h"
 
@@ -109,15 +111,70 @@ __global__ void __launch_bounds__(256) pack_qkv_kernel(const T* __restrict__ wq,
   }
 }
 
+// cuBLASLt is bound at run time, not linked: if the process already holds a
+// libcublasLt.so.12 (e.g. PyTorch's wheel copy) that one is used, otherwise
+// the CUDA toolkit's is loaded.  Linking it would pin a second copy under the
+// same soname and break the host framework's own cuBLAS.
+struct Lt {
+#define DFA_LT_FN(name) decltype(&::name) name = nullptr;
+  DFA_LT_FN(cublasLtCreate)
+  DFA_LT_FN(cublasLtDestroy)
+  DFA_LT_FN(cublasLtMatmulDescCreate)
+  DFA_LT_FN(cublasLtMatmulDescDestroy)
+  DFA_LT_FN(cublasLtMatmulDescSetAttribute)
+  DFA_LT_FN(cublasLtMatrixLayoutCreate)
+  DFA_LT_FN(cublasLtMatrixLayoutDestroy)
+  DFA_LT_FN(cublasLtMatrixLayoutSetAttribute)
+  DFA_LT_FN(cublasLtMatmulPreferenceCreate)
+  DFA_LT_FN(cublasLtMatmulPreferenceDestroy)
+  DFA_LT_FN(cublasLtMatmulPreferenceSetAttribute)
+  DFA_LT_FN(cublasLtMatmulAlgoGetHeuristic)
+  DFA_LT_FN(cublasLtMatmul)
+#undef DFA_LT_FN
+  bool ok = false;
+};
+
+const Lt& lt() {
+  static Lt t;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libcublasLt.so.12", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcublasLt.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("/usr/local/cuda/lib64/libcublasLt.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    bool ok = true;
+#define DFA_LT_SYM(name) \
+  t.name = reinterpret_cast<decltype(&::name)>(dlsym(h, #name)); \
+  ok = ok && t.name;
+    DFA_LT_SYM(cublasLtCreate)
+    DFA_LT_SYM(cublasLtDestroy)
+    DFA_LT_SYM(cublasLtMatmulDescCreate)
+    DFA_LT_SYM(cublasLtMatmulDescDestroy)
+    DFA_LT_SYM(cublasLtMatmulDescSetAttribute)
+    DFA_LT_SYM(cublasLtMatrixLayoutCreate)
+    DFA_LT_SYM(cublasLtMatrixLayoutDestroy)
+    DFA_LT_SYM(cublasLtMatrixLayoutSetAttribute)
+    DFA_LT_SYM(cublasLtMatmulPreferenceCreate)
+    DFA_LT_SYM(cublasLtMatmulPreferenceDestroy)
+    DFA_LT_SYM(cublasLtMatmulPreferenceSetAttribute)
+    DFA_LT_SYM(cublasLtMatmulAlgoGetHeuristic)
+    DFA_LT_SYM(cublasLtMatmul)
+#undef DFA_LT_SYM
+    t.ok = ok;
+  });
+  return t;
+}
+
 struct LtHandle {
   cublasLtHandle_t h = nullptr;
   ~LtHandle() {
-    if (h) cublasLtDestroy(h);
+    if (h && lt().ok) lt().cublasLtDestroy(h);
   }
 };
 cublasLtHandle_t lt_handle() {
+  if (!lt().ok) return nullptr;
   thread_local LtHandle lh;
-  if (!lh.h && cublasLtCreate(&lh.h) != CUBLAS_STATUS_SUCCESS) lh.h = nullptr;
+  if (!lh.h && lt().cublasLtCreate(&lh.h) != CUBLAS_STATUS_SUCCESS) lh.h = nullptr;
   return lh.h;
 }
 
@@ -130,8 +187,9 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
                   int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
                   const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why) {
   cublasLtHandle_t h = lt_handle();
+  const Lt& L = lt();
   if (!h) {
-    *why = "cublasLtCreate failed";
+    *why = "cuBLASLt unavailable (libcublasLt.so.12 not loadable)";
     return 0;
   }
   const cudaDataType_t dt = dtype == 0 ? CUDA_R_32F : CUDA_R_16BF;
@@ -140,52 +198,52 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
   cublasLtMatmulPreference_t pref = nullptr;
   int ok = 0;
   do {
-    if (cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS) break;
+    if (L.cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS) break;
     cublasLtEpilogue_t epi = bias ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT;
-    cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi));
+    L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi));
     if (bias) {
-      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
-      cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &dt, sizeof(dt));
+      L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
+      L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &dt, sizeof(dt));
     }
     // cublas operand "A" = our B^T ([N x K] col-major, ld = ldb); "B" = our A^T ([K x M], ld = lda)
-    if (cublasLtMatrixLayoutCreate(&la, dt, N, K, ldb) != CUBLAS_STATUS_SUCCESS) break;
-    if (cublasLtMatrixLayoutCreate(&lb, dt, K, M, lda) != CUBLAS_STATUS_SUCCESS) break;
-    if (cublasLtMatrixLayoutCreate(&lc, dt, N, M, C ? ldc : ldd) != CUBLAS_STATUS_SUCCESS) break;
-    if (cublasLtMatrixLayoutCreate(&ld, dt, N, M, ldd) != CUBLAS_STATUS_SUCCESS) break;
+    if (L.cublasLtMatrixLayoutCreate(&la, dt, N, K, ldb) != CUBLAS_STATUS_SUCCESS) break;
+    if (L.cublasLtMatrixLayoutCreate(&lb, dt, K, M, lda) != CUBLAS_STATUS_SUCCESS) break;
+    if (L.cublasLtMatrixLayoutCreate(&lc, dt, N, M, C ? ldc : ldd) != CUBLAS_STATUS_SUCCESS) break;
+    if (L.cublasLtMatrixLayoutCreate(&ld, dt, N, M, ldd) != CUBLAS_STATUS_SUCCESS) break;
     if (batch > 1) {
       const int32_t bc = batch;
       const int64_t strides[4] = {sb, sa, C ? sd : sd, sd};
       cublasLtMatrixLayout_t ls[4] = {la, lb, lc, ld};
       for (int i = 0; i < 4; ++i) {
-        cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
-        cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &strides[i],
+        L.cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
+        L.cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &strides[i],
                                          sizeof(int64_t));
       }
     }
-    if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS) break;
-    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes, sizeof(ws_bytes));
+    if (L.cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS) break;
+    L.cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes, sizeof(ws_bytes));
     cublasLtMatmulHeuristicResult_t res;
     int found = 0;
-    if (cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, ld, pref, 1, &res, &found) != CUBLAS_STATUS_SUCCESS ||
+    if (L.cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, ld, pref, 1, &res, &found) != CUBLAS_STATUS_SUCCESS ||
         found == 0) {
       *why = "no cuBLASLt algorithm for this GEMM";
       break;
     }
     const float alpha = 1.0f;
     const float b2 = C ? beta : 0.0f;
-    if (cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res.algo, ws, ws_bytes, stream) !=
+    if (L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res.algo, ws, ws_bytes, stream) !=
         CUBLAS_STATUS_SUCCESS) {
       *why = "cublasLtMatmul failed";
       break;
     }
     ok = 1;
   } while (0);
-  if (pref) cublasLtMatmulPreferenceDestroy(pref);
-  if (ld) cublasLtMatrixLayoutDestroy(ld);
-  if (lc) cublasLtMatrixLayoutDestroy(lc);
-  if (lb) cublasLtMatrixLayoutDestroy(lb);
-  if (la) cublasLtMatrixLayoutDestroy(la);
-  if (op) cublasLtMatmulDescDestroy(op);
+  if (pref) L.cublasLtMatmulPreferenceDestroy(pref);
+  if (ld) L.cublasLtMatrixLayoutDestroy(ld);
+  if (lc) L.cublasLtMatrixLayoutDestroy(lc);
+  if (lb) L.cublasLtMatrixLayoutDestroy(lb);
+  if (la) L.cublasLtMatrixLayoutDestroy(la);
+  if (op) L.cublasLtMatmulDescDestroy(op);
   return ok;
 }
 

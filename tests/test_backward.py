@@ -79,7 +79,7 @@ def test_backward_vs_oracle(dfa, port, cuda, B, n, h, w, r, d, dv, dtype):
     L = torch.empty((B, h, n), dtype=torch.float32, device="cuda")
     o = dfa.dfa_forward(dev[0], dev[1], dev[2], cfg, lse=L)
     gq, gk, gv = dfa.dfa_backward(dev[0], dev[1], dev[2], o, L, dev[3], cfg)
-    assert dfa.last_launch_count() == 3
+    assert dfa.last_launch_count() in (2, 3)  # tcgen05 (delta + 1) or SIMT (delta + 2)
     torch.cuda.synchronize()
     want = _oracle_batched_bwd(port, q, k, v, do, w, r, offs)
     for got, ref_ in zip((gq, gk, gv), want):
@@ -132,3 +132,33 @@ def test_backward_deterministic_and_autograd(dfa, cuda):
         err = (a.double() - t.grad).abs()
         assert err.max().item() <= 2e-2 * max(1.0, t.grad.abs().max().item())
         assert (err.sum() / t.grad.abs().sum()).item() <= 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("w,r,B", [(512, 2, 4), (256, 1, 2), (256, 2, 4), (1024, 4, 2), (512, 4, 2), (2048, 8, 1)])
+def test_tcgen05_backward_vs_simt(dfa, cuda, w, r, B):
+    """bf16 tcgen05 backward (m = w/r in {128, 256}) vs the SIMT backward on the
+    same inputs (path override), h = 6, offsets j mod r; and determinism."""
+    import torch
+    from paper_2403_09195_b200 import _lib, path_override
+
+    n, h, d = 4096, 6, 64
+    cfg = dfa.AttentionConfig(n, w, r, h, d, [j % r for j in range(h)])
+    g = torch.Generator(device="cuda").manual_seed(w + r)
+    q, k, v, do = (torch.randn((B, n, h, d), device="cuda", generator=g, dtype=torch.bfloat16) for _ in range(4))
+    L = torch.empty((B, h, n), dtype=torch.float32, device="cuda")
+    o = dfa.dfa_forward(q, k, v, cfg, lse=L)
+    a = dfa.dfa_backward(q, k, v, o, L, do, cfg)
+    assert dfa.last_launch_count() == 2  # delta + tcgen05 kernel
+    a2 = dfa.dfa_backward(q, k, v, o, L, do, cfg)
+    with path_override(_lib.DFA_PATH_SIMT):
+        b = dfa.dfa_backward(q, k, v, o, L, do, cfg)
+        assert dfa.last_launch_count() == 3
+    torch.cuda.synchronize()
+    for x, x2, y in zip(a, a2, b):
+        assert torch.equal(x, x2)
+        err = (x.float() - y.float()).abs()
+        scale = max(1.0, y.float().abs().max().item())
+        assert err.max().item() <= 2e-2 * scale, err.max().item()
+        assert (err.sum() / y.float().abs().sum()).item() <= 1e-2
