@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "dfa_internal.h"
 
 namespace dfa_impl {
@@ -75,20 +77,33 @@ __device__ __forceinline__ SegView seg_view(const BwdParams& p, int64_t seg, int
 }
 
 // Delta_i = dO_i . O_i for every row of [B, N, h, dv]; delta is [B, h, N].
+// One thread per row: 16-byte vector loads when the row allows them (the
+// row-of-a-warp form issued 2-byte loads and int64 divisions per row).
 template <typename T>
 __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ o, const T* __restrict__ dout,
                                                     float* __restrict__ delta, int64_t rows, int64_t N, int64_t h,
                                                     int64_t dv) {
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const T* a = o + row * dv;
-  const T* b = dout + row * dv;
-  float acc = 0.0f;
-  for (int64_t c = lane; c < dv; c += 32) acc = fmaf(ld(a + c), ld(b + c), acc);
-  acc = part_sum<32>(acc);
-  if (lane == 0) {
-    const int64_t j = row % h, n = (row / h) % N, bb = row / (h * N);
+  constexpr int V = 16 / sizeof(T);
+  const bool vec = dv % V == 0 && ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(dout)) & 15u) == 0;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < rows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const T* a = o + row * dv;
+    const T* b = dout + row * dv;
+    float acc = 0.0f;
+    if (vec) {
+      for (int64_t c = 0; c < dv; c += V) {
+        const uint4 x = *reinterpret_cast<const uint4*>(a + c);
+        const uint4 y = *reinterpret_cast<const uint4*>(b + c);
+        const T* xa = reinterpret_cast<const T*>(&x);
+        const T* ya = reinterpret_cast<const T*>(&y);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc = fmaf(ld(xa + e), ld(ya + e), acc);
+      }
+    } else {
+      for (int64_t c = 0; c < dv; ++c) acc = fmaf(ld(a + c), ld(b + c), acc);
+    }
+    const int64_t j = row % h, rest = row / h;
+    const int64_t n = rest % N, bb = rest / N;
     delta[(bb * h + j) * N + n] = acc;
   }
 }
@@ -282,8 +297,8 @@ int launch_bwd_t(const Geometry& g, const void* q, const void* k, const void* v,
   p.scale = g.scale;
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
   const int64_t rows = g.B * g.N * g.h;
-  delta_kernel<T><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, stream>>>((const T*)o, (const T*)dout, delta, rows,
-                                                                             g.N, g.h, g.dv);
+  delta_kernel<T><<<(unsigned)std::min<int64_t>((rows + 255) / 256, 148 * 32), 256, 0, stream>>>(
+      (const T*)o, (const T*)dout, delta, rows, g.N, g.h, g.dv);
   dim3 grid((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
   dkdv_kernel<T, DMAX, PARTS, TILE><<<grid, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v,
                                                                (const T*)dout, lse, delta, (T*)dk, (T*)dv, p);
@@ -313,7 +328,7 @@ int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, 
   const void* ptrs[] = {q, k, v, dout, dq, dk, dv};
   if (allow_sm100 && bwd_sm100_supported(g, dtype, ptrs, 7)) {
     const int64_t rows = g.B * g.N * g.h;
-    delta_kernel<__nv_bfloat16><<<(unsigned)((rows * 32 + 255) / 256), 256, 0, stream>>>(
+    delta_kernel<__nv_bfloat16><<<(unsigned)std::min<int64_t>((rows + 255) / 256, 148 * 32), 256, 0, stream>>>(
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, delta, rows, g.N, g.h, g.dv);
     const int n = launch_bwd_sm100(g, q, k, v, dout, lse, delta, dq, dk, dv, stream, err, why);
     return n ? n + 1 : 0;

@@ -15,7 +15,7 @@
 // query block qb (128 each), one elected thread issues
 //   S^T  = K_kb Q_qb^T            (M=128 keys, N=128 queries)  -> TMEM [0,128)
 //   dP^T = V_kb dO_qb^T                                         -> TMEM [128,256)
-// the 128-thread gradient warpgroup (thread = key row = TMEM lane) turns them
+// two gradient warpgroups (thread = key row = TMEM lane, half the queries each) turn them
 // into P^T (bf16 over S^T's columns) and dS^T (bf16 over dP^T's columns, and
 // into shared memory as the MN-major A operand of dQ), then
 //   dV_kb += P^T dO_qb   (A = P^T from TMEM, B = dO MN-major)   -> TMEM [256,320)
@@ -42,7 +42,7 @@ constexpr int kD = 64;
 constexpr int kB = 128;                // rows per tile (keys / queries)
 constexpr int kTile = 128 * 128;       // 128 rows x 128 B (64 bf16), SW128
 constexpr int kMaxBlk = 2;             // m <= 256
-constexpr int kThreads = 256;          // warp 0: TMA + MMA, warp 1: TMEM alloc, warps 4-7: gradient WG
+constexpr int kThreads = 384;          // warp 0: TMA + MMA, warp 1: TMEM alloc, warps 4-11: gradient WGs
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct __align__(1024) BwdSmem {
@@ -83,28 +83,38 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int32_t t0 = seg * p.m;  // first t' of the view
   const int nb = p.nblk;
 
+  if (warp == 0 && lane == 0) {
+    // barriers first, then the view's TMA loads go out before anything else
+    ptx::mbar_init(&sm.load_full, 1);
+    ptx::mbar_init(&sm.s_full, 1);
+    ptx::mbar_init(&sm.p_full, 2 * kB);
+    ptx::mbar_init(&sm.kv_done, 1);
+    ptx::mbar_init(&sm.q_done, 1);
+    ptx::fence_barrier_init();
+    const uint64_t pol = ptx::policy_evict_first();
+    ptx::mbar_arrive_expect_tx(&sm.load_full, 4 * nb * kTile);
+    for (int blk = 0; blk < nb; ++blk) {
+      const int32_t tb = t0 + blk * kB;
+      ptx::tma_load_5d(sm.q[blk], &tm_q, &sm.load_full, 0, j, gamma, tb, b, pol);
+      ptx::tma_load_5d(sm.k[blk], &tm_k, &sm.load_full, 0, j, gamma, tb, b, pol);
+      ptx::tma_load_5d(sm.v[blk], &tm_v, &sm.load_full, 0, j, gamma, tb, b, pol);
+      ptx::tma_load_5d(sm.g[blk], &tm_g, &sm.load_full, 0, j, gamma, tb, b, pol);
+    }
+  } else if (warp == 1) {
+    ptx::tmem_alloc<512>(&sm.tmem_base);
+  }
   for (uint32_t i = threadIdx.x; i < kTile / 16; i += kThreads) ptx::st_shared_v4(ptx::smem_u32(sm.zero) + 16 * i, 0, 0, 0, 0);
-  if (threadIdx.x >= 128) {  // gradient warpgroup: the view's lse (log2 units) and Delta
+  if (threadIdx.x >= 128) {  // gradient warpgroups: the view's lse (log2 units) and Delta
     const int t = threadIdx.x - 128;
     const float* lb = lse + ((int64_t)b * p.h + j) * p.N;
     const float* db = delta + ((int64_t)b * p.h + j) * p.N;
-    for (int tt = t; tt < nb * kB; tt += 128) {
+    for (int tt = t; tt < nb * kB; tt += kThreads - 128) {
       const int64_t n = (int64_t)(t0 + tt) * p.r + gamma;
       sm.lse2[tt] = lb[n] * kLog2e;
       sm.dlt[tt] = db[n];
     }
   }
   ptx::fence_proxy_async_smem();
-  if (warp == 0 && lane == 0) {
-    ptx::mbar_init(&sm.load_full, 1);
-    ptx::mbar_init(&sm.s_full, 1);
-    ptx::mbar_init(&sm.p_full, kB);
-    ptx::mbar_init(&sm.kv_done, 1);
-    ptx::mbar_init(&sm.q_done, 1);
-    ptx::fence_barrier_init();
-  } else if (warp == 1) {
-    ptx::tmem_alloc<512>(&sm.tmem_base);
-  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -113,16 +123,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (ptx::elect_one()) {
-      // ---------------------------------------------------------- loads
-      const uint64_t pol = ptx::policy_evict_first();
-      ptx::mbar_arrive_expect_tx(&sm.load_full, 4 * nb * kTile);
-      for (int blk = 0; blk < nb; ++blk) {
-        const int32_t tb = t0 + blk * kB;
-        ptx::tma_load_5d(sm.q[blk], &tm_q, &sm.load_full, 0, j, gamma, tb, b, pol);
-        ptx::tma_load_5d(sm.k[blk], &tm_k, &sm.load_full, 0, j, gamma, tb, b, pol);
-        ptx::tma_load_5d(sm.v[blk], &tm_v, &sm.load_full, 0, j, gamma, tb, b, pol);
-        ptx::tma_load_5d(sm.g[blk], &tm_g, &sm.load_full, 0, j, gamma, tb, b, pol);
-      }
       wait(&sm.load_full, 0);
       ptx::tc_fence_after();
       // ------------------------------------------------------------ MMA
@@ -160,10 +160,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_commit(&sm.q_done);
     }
   } else if (warp >= 4) {
-    // ------------------------------------------------ gradient warpgroup
-    const uint32_t row = (warp - 4) * 32 + lane;  // key row (TMEM lane) / query row for dQ
-    const uint32_t lane_base = ((warp - 4) * 32) << 16;
-    const bool leader = warp == 4 && lane == 0;
+    // ----------------------------------------------- gradient warpgroups
+    // Two warpgroups share every step: WG0 takes queries [0, 64) of the
+    // block, WG1 [64, 128) (thread = key row = TMEM lane in both); in the
+    // epilogues WG0 writes dK, WG1 dV, and they alternate the dQ blocks.
+    const int wg = (warp - 4) / 4;
+    const uint32_t row = ((warp - 4) % 4) * 32 + lane;  // key row (TMEM lane) / query row for dQ
+    const uint32_t lane_base = (((warp - 4) % 4) * 32) << 16;
+    const bool leader = warp % 4 == 0 && lane == 0;
+    const uint32_t bar_id = 1 + wg;
     uint32_t step = 0;
     auto stage_store = [&](uint8_t* st, const uint32_t (&v)[2][32], float mul) {
       const uint32_t a0 = ptx::smem_u32(st);
@@ -183,11 +188,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float* dl = sm.dlt + qb * kB;
         const uint32_t dsa = ptx::smem_u32(sm.ds[0]);
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {  // 32 queries per chunk
+        for (int c = 2 * wg; c < 2 * wg + 2; ++c) {  // 32 queries per chunk
           uint32_t s[32], dp[32];
           ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, s);
           ptx::tmem_ld32(tbase + lane_base + cDP + 32 * c, dp);
           ptx::tmem_ld_wait();
+          // Packed P^T / dS^T of chunk c land on columns 16c.., i.e. on the
+          // fp32 columns of chunk c/2: WG1's chunks 2-3 overwrite WG0's chunk
+          // 1, so WG0 signals once chunk 1 is in registers and WG1 waits for
+          // that before its first store (WG0's own order 0, 1 is safe).
+          if (c == 1) ptx::named_bar_arrive(3, 2 * kB);
           uint32_t pp[16], dd[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -198,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl[q0]),
                                      p1 * (__uint_as_float(dp[2 * e + 1]) - dl[q0 + 1]));
           }
+          if (c == 2) ptx::named_bar_sync(3, 2 * kB);
           ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
           ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
           // dS^T row `row` (key) -> MN-major A of dQ: queries 32c..32c+31 are
@@ -215,51 +226,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(&sm.p_full);
       }
-      // dK, dV of key block kb
+      // dK (WG0) / dV (WG1) of key block kb
       wait(&sm.kv_done, kb & 1);
       ptx::tc_fence_after();
       uint32_t a[2][32];
       if (leader) ptx::tma_store_wait_read<0>();
-      ptx::named_bar_sync(1, 128);
-      ptx::tmem_ld32(tbase + lane_base + cDV, a[0]);
-      ptx::tmem_ld32(tbase + lane_base + cDV + 32, a[1]);
+      ptx::named_bar_sync(bar_id, 128);
+      const uint32_t col = wg == 0 ? cDK : cDV;
+      ptx::tmem_ld32(tbase + lane_base + col, a[0]);
+      ptx::tmem_ld32(tbase + lane_base + col + 32, a[1]);
       ptx::tmem_ld_wait();
-      stage_store(sm.stage[1], a, 1.0f);
-      ptx::tmem_ld32(tbase + lane_base + cDK, a[0]);
-      ptx::tmem_ld32(tbase + lane_base + cDK + 32, a[1]);
-      ptx::tmem_ld_wait();
-      stage_store(sm.stage[0], a, p.scale);
+      stage_store(sm.stage[wg], a, wg == 0 ? p.scale : 1.0f);
       ptx::tc_fence_before();
       ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 128);
+      ptx::named_bar_sync(bar_id, 128);
       if (leader) {
         const int32_t tb = t0 + kb * kB;
-        ptx::tma_store_5d(&tm_dk, sm.stage[0], 0, j, gamma, tb, b);
-        ptx::tma_store_5d(&tm_dv, sm.stage[1], 0, j, gamma, tb, b);
+        const CUtensorMap* mo = wg == 0 ? &tm_dk : &tm_dv;
+        ptx::tma_store_5d(mo, sm.stage[wg], 0, j, gamma, tb, b);
         for (int32_t gz = 0; gz < p.r; ++gz)
           if (gz != gamma) {
-            ptx::tma_store_5d(&tm_dk, sm.zero, 0, j, gz, tb, b);
-            ptx::tma_store_5d(&tm_dv, sm.zero, 0, j, gz, tb, b);
-            ptx::tma_store_5d(&tm_dq, sm.zero, 0, j, gz, tb, b);
+            ptx::tma_store_5d(mo, sm.zero, 0, j, gz, tb, b);
+            if (wg == 0) ptx::tma_store_5d(&tm_dq, sm.zero, 0, j, gz, tb, b);
           }
         ptx::tma_store_commit();
       }
     }
-    // dQ blocks (TMEM lanes = query rows)
+    // dQ blocks (TMEM lanes = query rows), alternating between the warpgroups
     wait(&sm.q_done, 0);
     ptx::tc_fence_after();
-    for (int qb = 0; qb < nb; ++qb) {
+    for (int qb = wg; qb < nb; qb += 2) {
       uint32_t a[2][32];
       if (leader) ptx::tma_store_wait_read<0>();
-      ptx::named_bar_sync(1, 128);
+      ptx::named_bar_sync(bar_id, 128);
       ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb, a[0]);
       ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb + 32, a[1]);
       ptx::tmem_ld_wait();
-      stage_store(sm.stage[qb & 1], a, p.scale);
+      stage_store(sm.stage[wg], a, p.scale);
       ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(1, 128);
+      ptx::named_bar_sync(bar_id, 128);
       if (leader) {
-        ptx::tma_store_5d(&tm_dq, sm.stage[qb & 1], 0, j, gamma, t0 + qb * kB, b);
+        ptx::tma_store_5d(&tm_dq, sm.stage[wg], 0, j, gamma, t0 + qb * kB, b);
         ptx::tma_store_commit();
       }
     }

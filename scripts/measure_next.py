@@ -40,6 +40,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "next.json"))
     ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--only", choices=["backward"], default=None)
     a = ap.parse_args()
     B, N, h, d, w, r = a.batch, 4096, 6, 64, 512, 2
     D, hidden = h * d, 4 * h * d
@@ -62,6 +63,9 @@ def main():
                        "forward_ms": time_ms(lambda: dfa.dfa_forward(q, k, v, cfg, out=o, lse=L)),
                        "path": "SIMT fp32-math kernels (delta, dK/dV, dQ)"}
     del q, k, v, do, o, dq, dk, dv, L
+    if a.only == "backward":
+        print(json.dumps(res, indent=1))
+        return
 
     # ---- multi-head layer
     x = torch.randn((B, N, D), device="cuda", dtype=bf, generator=g)
