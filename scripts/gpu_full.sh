@@ -17,3 +17,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.a
     --clock-control none -k regex:dfa_sm100 --csv --log-file $OUT/ncu_sweep_$TAG.csv python scripts/sweeps.py --ncu > $OUT/ncu_sweep_$TAG.log 2>&1
 python -c "import json; d=json.load(open('$OUT/bench_$TAG.json')); print('ms', d['roofline']['kernel_ms'], 'GB/s', round(d['roofline']['achieved']), 'frac', round(d['roofline']['frac'],3), 'TF', round(d['tflops']), d['clocks'])"
 ls $OUT | tail -20
+timeout 300 python scripts/measure_next.py --out $OUT/next_$TAG.json > $OUT/next_$TAG.txt 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/bwd_launches_$TAG.csv python scripts/measure_next.py --only backward > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:dfa_bwd_sm100 -s 2 -c 1 -o $OUT/prof_bwd_$TAG -f python scripts/measure_next.py --only backward > $OUT/ncu_bwd_$TAG.log 2>&1
+python -c "import json; d=json.load(open('$OUT/next_$TAG.json')); print({k: (round(v['ms'],3) if isinstance(v, dict) else v) for k, v in d.items()})"
