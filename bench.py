@@ -181,8 +181,9 @@ def run_reference(args):
     from oracle.oracle import Port, Reference, reference_available
 
     threads = cpu_threads()
-    # each step: one unit per host thread, rounded up to whole images
-    units = ((threads + H - 1) // H) * H
+    # each step: ~8 units per host thread (so the thread pool stays busy
+    # through the step), rounded up to whole images
+    units = ((8 * threads + H - 1) // H) * H
     if reference_available():
         ref = Reference()
         kind = "reference"
