@@ -90,7 +90,21 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ o, con
     const T* a = o + row * dv;
     const T* b = dout + row * dv;
     float acc = 0.0f;
-    if (vec) {
+    if (vec && dv == 64) {  // the common head width: all 16 loads in flight at once
+      uint4 x[64 / V], y[64 / V];
+#pragma unroll
+      for (int i = 0; i < 64 / V; ++i) {
+        x[i] = reinterpret_cast<const uint4*>(a)[i];
+        y[i] = reinterpret_cast<const uint4*>(b)[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 64 / V; ++i) {
+        const T* xa = reinterpret_cast<const T*>(&x[i]);
+        const T* ya = reinterpret_cast<const T*>(&y[i]);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc = fmaf(ld(xa + e), ld(ya + e), acc);
+      }
+    } else if (vec) {
       for (int64_t c = 0; c < dv; c += V) {
         const uint4 x = *reinterpret_cast<const uint4*>(a + c);
         const uint4 y = *reinterpret_cast<const uint4*>(b + c);

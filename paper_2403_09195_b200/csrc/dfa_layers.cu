@@ -48,9 +48,72 @@ __device__ __forceinline__ __nv_bfloat16 stf<__nv_bfloat16>(float x) {
   return __float2bfloat16_rn(x);
 }
 
+// 16-byte vectors of 8 bf16 / 4 f32 values.
+template <typename T>
+struct Vec {
+  static constexpr int kN = 16 / sizeof(T);
+  uint4 raw;
+  __device__ __forceinline__ float get(int e) const { return ldf(reinterpret_cast<const T*>(&raw) + e); }
+  __device__ __forceinline__ void set(int e, float x) { reinterpret_cast<T*>(&raw)[e] = stf<T>(x); }
+};
+
 // tensor.hpp:281-300 / autodiff.hpp:191-243 layer_norm: population variance,
-// eps 1e-5, y = (x - mean) / sqrt(var + eps) * g + b.  One warp per row,
-// two-pass in fp32 over the row held in registers (D <= 32 * 32).
+// eps 1e-5, y = (x - mean) / sqrt(var + eps) * g + b.  One warp per row; lane
+// l holds 16-byte vectors l, l + 32, ... of the row in registers (D <= 1024 for
+// bf16), two-pass mean / variance in fp32 with warp shuffles, 16-byte stores.
+// Requires D % (16 / sizeof(T)) == 0 and 16-byte aligned rows (checked by the
+// launcher, which falls back to the scalar form otherwise).
+template <typename T, int kMaxVec>
+__global__ void __launch_bounds__(256) layer_norm_vec_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                                             const T* __restrict__ b, T* __restrict__ y,
+                                                             int64_t rows, int cols) {
+  constexpr int V = Vec<T>::kN;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int nv = cols / V;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  Vec<T> v[kMaxVec];
+  float sum = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int vi = lane + 32 * i;
+    v[i].raw = vi < nv ? xr[vi] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int e = 0; e < V; ++e) sum += v[i].get(e);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / (float)cols;
+  float var = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i)
+    if (lane + 32 * i < nv)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const float d = v[i].get(e) - mean;
+        var = fmaf(d, d, var);
+      }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+  const float inv = 1.0f / sqrtf(var / (float)cols + 1e-5f);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  const uint4* bv = reinterpret_cast<const uint4*>(b);
+#pragma unroll
+  for (int i = 0; i < kMaxVec; ++i) {
+    const int vi = lane + 32 * i;
+    if (vi >= nv) continue;
+    Vec<T> gg, bb, out;
+    gg.raw = gv[vi];
+    bb.raw = bv[vi];
+#pragma unroll
+    for (int e = 0; e < V; ++e) out.set(e, (v[i].get(e) - mean) * inv * gg.get(e) + bb.get(e));
+    yr[vi] = out.raw;
+  }
+}
+
+// Scalar fallback (any D <= 1024, any alignment).
 template <typename T>
 __global__ void __launch_bounds__(256) layer_norm_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                          const T* __restrict__ b, T* __restrict__ y, int64_t rows,
@@ -88,10 +151,29 @@ __global__ void __launch_bounds__(256) layer_norm_kernel(const T* __restrict__ x
   }
 }
 
-// tensor.hpp:262-265 gelu_scalar: x * 0.5 * (1 + erf(x / sqrt(2))), in place.
+// tensor.hpp:262-265 gelu_scalar: x * 0.5 * (1 + erf(x / sqrt(2))), in place,
+// 16-byte vectors (n % V == 0 and 16-byte alignment; scalar tail otherwise).
 template <typename T>
-__global__ void __launch_bounds__(256) gelu_kernel(T* __restrict__ x, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) gelu_kernel(T* __restrict__ x, int64_t n, bool vec) {
+  constexpr int V = Vec<T>::kN;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    uint4* xv = reinterpret_cast<uint4*>(x);
+    const int64_t nv = n / V;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+      Vec<T> a;
+      a.raw = xv[i];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const float t = a.get(e);
+        a.set(e, t * 0.5f * (1.0f + erff(t * 0.70710678118654752f)));
+      }
+      xv[i] = a.raw;
+    }
+    done = nv * V;
+  }
+  for (int64_t i = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const float v = ldf(x + i);
     x[i] = stf<T>(v * 0.5f * (1.0f + erff(v * 0.70710678118654752f)));
   }
@@ -250,13 +332,22 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
                       cudaStream_t stream) {
   const unsigned grid = (unsigned)((rows * 32 + 255) / 256);
-  if (dtype == 0)
-    layer_norm_kernel<float><<<grid, 256, 0, stream>>>((const float*)x, (const float*)g, (const float*)b, (float*)y,
-                                                       rows, cols);
-  else
-    layer_norm_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)g,
-                                                               (const __nv_bfloat16*)b, (__nv_bfloat16*)y, rows,
-                                                               cols);
+  const bool al = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(b) |
+                    reinterpret_cast<uintptr_t>(y)) & 15u) == 0;
+  if (dtype == 0) {
+    if (al && cols % 4 == 0 && cols <= 4 * 32 * 8)
+      layer_norm_vec_kernel<float, 8><<<grid, 256, 0, stream>>>((const float*)x, (const float*)g, (const float*)b,
+                                                               (float*)y, rows, cols);
+    else
+      layer_norm_kernel<float><<<grid, 256, 0, stream>>>((const float*)x, (const float*)g, (const float*)b,
+                                                         (float*)y, rows, cols);
+  } else {
+    using B = __nv_bfloat16;
+    if (al && cols % 8 == 0 && cols <= 8 * 32 * 4)
+      layer_norm_vec_kernel<B, 4><<<grid, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
+    else
+      layer_norm_kernel<B><<<grid, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
+  }
   return 1;
 }
 
@@ -273,11 +364,13 @@ int launch_pack_qkv(int dtype, const void* wq, const void* wk, const void* wv, v
 }
 
 int launch_gelu(int dtype, void* x, int64_t n, cudaStream_t stream) {
-  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  const bool vec = (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+  const int64_t per = dtype == 0 ? 4 : 8;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n / per + 255) / 256, 148 * 64));
   if (dtype == 0)
-    gelu_kernel<float><<<grid, 256, 0, stream>>>((float*)x, n);
+    gelu_kernel<float><<<grid, 256, 0, stream>>>((float*)x, n, vec);
   else
-    gelu_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((__nv_bfloat16*)x, n);
+    gelu_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((__nv_bfloat16*)x, n, vec);
   return 1;
 }
 

@@ -107,9 +107,11 @@ __global__ void __launch_bounds__(128) simt_kernel(const T* __restrict__ q, cons
     float tmax = -INFINITY;
 #pragma unroll
     for (int jj = 0; jj < KT; ++jj) {
-      float dot = 0.0f;
+      // 4 partial sums: a 4x shorter FMA dependency chain per key
+      float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int c = 0; c < DMAX; ++c) dot = fmaf(qr[c], ks[jj][c], dot);
+      for (int c = 0; c < DMAX; ++c) d4[c & 3] = fmaf(qr[c], ks[jj][c], d4[c & 3]);
+      const float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
       s[jj] = (k0 + jj < m) ? dot * p.scale : -INFINITY;
       tmax = fmaxf(tmax, s[jj]);
     }
@@ -137,6 +139,126 @@ __global__ void __launch_bounds__(128) simt_kernel(const T* __restrict__ q, cons
   }
 }
 
+// Latency form for small grids (e.g. config 1: B = h = 1 gives 16 CTAs of the
+// kernel above): SPLIT lanes share a query row, each running the online
+// softmax over every SPLIT-th key of the tile; the partial (max, sum, acc)
+// triples are merged with shuffles at the end (the LSE merge of attention.hpp's
+// tiled recurrence over disjoint key subsets).  4x the CTAs, 1/4 the keys each.
+template <typename T, int DMAX, int KT, int SPLIT>
+__global__ void __launch_bounds__(128) simt_split_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                         const T* __restrict__ v, T* __restrict__ o,
+                                                         float* __restrict__ lse,
+                                                         const __grid_constant__ SimtParams p) {
+  constexpr int ROWS = 128 / SPLIT;
+  // rows padded by 4 floats: the SPLIT lanes of a row read SPLIT different
+  // key rows at once, and the pad puts their float4s on distinct banks
+  constexpr int LD = DMAX + 4;
+  __shared__ __align__(16) float ks[KT][LD];
+  __shared__ __align__(16) float vs[KT][LD];
+  const int tid = threadIdx.x, rr = tid / SPLIT, pp = tid % SPLIT;
+  const int64_t seg = blockIdx.x / p.n_chunks, chunk = blockIdx.x % p.n_chunks;
+  const int64_t j = blockIdx.y, b = blockIdx.z, g = p.offsets[j];
+  const int64_t seg_begin = seg * p.w;
+  const int64_t seg_rows = min(seg_begin + p.w, p.N) - seg_begin;
+  const int64_t m = g >= seg_rows ? 0 : (seg_rows - g + p.r - 1) / p.r;  // attention.hpp:96
+  const T* qb = q + b * p.N * p.ldq + j * p.d;
+  const T* kb = k + b * p.N * p.ldk + j * p.d;
+  const T* vb = v + b * p.N * p.ldv + j * p.dv;
+  T* ob = o + b * p.N * p.ldo + j * p.dv;
+  float* lb = lse ? lse + (b * p.h + j) * p.N : nullptr;
+  if (chunk == 0) {
+    for (int64_t l = tid; l < seg_rows; l += blockDim.x) {
+      if (l % p.r == g && l >= g) continue;
+      T* orow = ob + (seg_begin + l) * p.ldo;
+      for (int64_t c = 0; c < p.dv; ++c) orow[c] = from_f<T>(0.0f);
+      if (lb) lb[seg_begin + l] = -INFINITY;
+    }
+  }
+  if (chunk * ROWS >= m) return;
+  const int64_t t = chunk * ROWS + rr;
+  const bool active = t < m;
+  const int64_t row = seg_begin + g + t * p.r;
+  float qr[DMAX], acc[DMAX];
+#pragma unroll
+  for (int c = 0; c < DMAX; ++c) {
+    qr[c] = (active && c < p.d) ? to_f(qb[row * p.ldq + c]) : 0.0f;
+    acc[c] = 0.0f;
+  }
+  float mx = -INFINITY, l = 0.0f;
+  for (int64_t k0 = 0; k0 < m; k0 += KT) {
+    __syncthreads();
+    for (int e = tid; e < KT * DMAX; e += blockDim.x) {
+      const int jj = e / DMAX, c = e % DMAX;
+      const int64_t tk = k0 + jj;
+      const int64_t krow = seg_begin + g + tk * p.r;
+      ks[jj][c] = (tk < m && c < p.d) ? to_f(kb[krow * p.ldk + c]) : 0.0f;
+      vs[jj][c] = (tk < m && c < p.dv) ? to_f(vb[krow * p.ldv + c]) : 0.0f;
+    }
+    __syncthreads();
+    float s[KT / SPLIT];
+    float tmax = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < KT / SPLIT; ++i) {
+      const int jj = i * SPLIT + pp;
+      float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int c = 0; c < DMAX; c += 4) {
+        const float4 kv = *reinterpret_cast<const float4*>(&ks[jj][c]);
+        d4[0] = fmaf(qr[c], kv.x, d4[0]);
+        d4[1] = fmaf(qr[c + 1], kv.y, d4[1]);
+        d4[2] = fmaf(qr[c + 2], kv.z, d4[2]);
+        d4[3] = fmaf(qr[c + 3], kv.w, d4[3]);
+      }
+      const float dot = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+      s[i] = (k0 + jj < m) ? dot * p.scale : -INFINITY;
+      tmax = fmaxf(tmax, s[i]);
+    }
+    const float nmax = fmaxf(mx, tmax);
+    if (nmax == -INFINITY) continue;  // no key of this part in the tile yet
+    const float corr = expf(mx - nmax);
+    l *= corr;
+#pragma unroll
+    for (int c = 0; c < DMAX; ++c) acc[c] *= corr;
+#pragma unroll
+    for (int i = 0; i < KT / SPLIT; ++i) {
+      const float pj = expf(s[i] - nmax);
+      l += pj;
+#pragma unroll
+      for (int c = 0; c < DMAX; c += 4) {
+        const float4 vv = *reinterpret_cast<const float4*>(&vs[i * SPLIT + pp][c]);
+        acc[c] = fmaf(pj, vv.x, acc[c]);
+        acc[c + 1] = fmaf(pj, vv.y, acc[c + 1]);
+        acc[c + 2] = fmaf(pj, vv.z, acc[c + 2]);
+        acc[c + 3] = fmaf(pj, vv.w, acc[c + 3]);
+      }
+    }
+    mx = nmax;
+  }
+  // merge the SPLIT partial states of the row (adjacent lanes)
+  float gm = mx;
+#pragma unroll
+  for (int o2 = SPLIT / 2; o2 > 0; o2 >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o2));
+  const float f = mx == -INFINITY ? 0.0f : expf(mx - gm);
+  l *= f;
+#pragma unroll
+  for (int o2 = SPLIT / 2; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
+#pragma unroll
+  for (int c = 0; c < DMAX; ++c) {
+    float a = acc[c] * f;
+#pragma unroll
+    for (int o2 = SPLIT / 2; o2 > 0; o2 >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o2);
+    acc[c] = a;
+  }
+  if (active) {
+    const float inv = 1.0f / l;
+    T* orow = ob + row * p.ldo;
+#pragma unroll
+    for (int c = 0; c < DMAX; ++c)
+      if (c % SPLIT == pp && c < p.dv) orow[c] = from_f<T>(acc[c] * inv);
+    if (lb && pp == 0) lb[row] = gm + logf(l);
+  }
+}
+
 template <typename T, int DMAX, int KT>
 int launch_t(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
              cudaStream_t stream, cudaError_t* err) {
@@ -156,7 +278,21 @@ int launch_t(const Geometry& g, const void* q, const void* k, const void* v, voi
   p.scale = g.scale;
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
   dim3 grid((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
-  simt_kernel<T, DMAX, KT><<<grid, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o, lse, p);
+  constexpr int kSplit = 4;
+  bool launched = false;
+  if constexpr (DMAX <= 64) {
+    if ((int64_t)grid.x * grid.y * grid.z < 2 * 148) {
+      // small grid: 4 lanes per query row -> 4x the CTAs
+      p.n_chunks = (g.m_max + 128 / kSplit - 1) / (128 / kSplit);
+      if (p.n_chunks < 1) p.n_chunks = 1;
+      dim3 g2((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
+      simt_split_kernel<T, DMAX, KT, kSplit><<<g2, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o,
+                                                                     lse, p);
+      launched = true;
+    }
+  }
+  if (!launched)
+    simt_kernel<T, DMAX, KT><<<grid, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o, lse, p);
   *err = cudaGetLastError();
   return 1;
 }
