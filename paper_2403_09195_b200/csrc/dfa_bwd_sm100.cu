@@ -9,9 +9,11 @@
 // Delta = rowsum(dO o O) (delta_kernel), dS = P o (dP - Delta):
 //   dV = P^T dO,  dK = sc dS^T Q,  dQ = sc dS K.
 //
-// One CTA per (image, head, segment); the whole view (Q, K, V, dO: m x 64
-// each) is TMA-loaded once into shared memory as 128-row SW128 tiles of the
-// t'-stream (the forward's index mapping: no gather).  For key block kb and
+// Persistent CTAs (one per SM) loop over units = (image, head, segment); a
+// unit's whole view (Q, K, V, dO: m x 64 each) is TMA-loaded once into shared
+// memory as 128-row SW128 tiles of the t'-stream (the forward's index
+// mapping: no gather), and the next unit's loads are issued as soon as this
+// unit's MMAs complete, overlapping its dQ epilogue and output stores.  For key block kb and
 // query block qb (128 each), one elected thread issues
 //   S^T  = K_kb Q_qb^T            (M=128 keys, N=128 queries)  -> TMEM [0,128)
 //   dP^T = V_kb dO_qb^T                                         -> TMEM [128,256)
@@ -30,6 +32,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "dfa_internal.h"
@@ -60,7 +63,7 @@ struct __align__(1024) BwdSmem {
 };
 
 struct BwdSm100Params {
-  int32_t N, T, m, r, h, n_seg, nblk;
+  int32_t N, T, m, r, h, n_seg, nblk, n_units;
   float c, scale;
   int32_t offsets[kMaxHeads];
 };
@@ -76,44 +79,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
-  const int32_t seg = blockIdx.x % p.n_seg;
-  const int32_t bj = blockIdx.x / p.n_seg;
-  const int32_t j = bj % p.h, b = bj / p.h;
-  const int32_t gamma = p.offsets[j];
-  const int32_t t0 = seg * p.m;  // first t' of the view
   const int nb = p.nblk;
+  const int32_t n_units = p.n_units;
+  // unit u = (b * h + j) * n_seg + seg
+  struct View {
+    int32_t b, j, gamma, t0;
+  };
+  auto view = [&](int32_t u) {
+    View v;
+    const int32_t seg = u % p.n_seg, bj = u / p.n_seg;
+    v.j = bj % p.h;
+    v.b = bj / p.h;
+    v.gamma = p.offsets[v.j];
+    v.t0 = seg * p.m;  // first t' of the view
+    return v;
+  };
+  // Q, K, V, dO of unit u (the forward's t'-stream boxes) -> smem, one barrier
+  auto issue_loads = [&](int32_t u) {
+    const View x = view(u);
+    const uint64_t pol = ptx::policy_evict_first();
+    ptx::mbar_arrive_expect_tx(&sm.load_full, 4 * nb * kTile);
+    for (int blk = 0; blk < nb; ++blk) {
+      const int32_t tb = x.t0 + blk * kB;
+      ptx::tma_load_5d(sm.q[blk], &tm_q, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.k[blk], &tm_k, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.v[blk], &tm_v, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.g[blk], &tm_g, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
+    }
+  };
 
   if (warp == 0 && lane == 0) {
-    // barriers first, then the view's TMA loads go out before anything else
     ptx::mbar_init(&sm.load_full, 1);
     ptx::mbar_init(&sm.s_full, 1);
     ptx::mbar_init(&sm.p_full, 2 * kB);
     ptx::mbar_init(&sm.kv_done, 1);
     ptx::mbar_init(&sm.q_done, 1);
     ptx::fence_barrier_init();
-    const uint64_t pol = ptx::policy_evict_first();
-    ptx::mbar_arrive_expect_tx(&sm.load_full, 4 * nb * kTile);
-    for (int blk = 0; blk < nb; ++blk) {
-      const int32_t tb = t0 + blk * kB;
-      ptx::tma_load_5d(sm.q[blk], &tm_q, &sm.load_full, 0, j, gamma, tb, b, pol);
-      ptx::tma_load_5d(sm.k[blk], &tm_k, &sm.load_full, 0, j, gamma, tb, b, pol);
-      ptx::tma_load_5d(sm.v[blk], &tm_v, &sm.load_full, 0, j, gamma, tb, b, pol);
-      ptx::tma_load_5d(sm.g[blk], &tm_g, &sm.load_full, 0, j, gamma, tb, b, pol);
-    }
+    issue_loads(blockIdx.x);  // the first unit's loads go out before anything else
   } else if (warp == 1) {
     ptx::tmem_alloc<512>(&sm.tmem_base);
   }
   for (uint32_t i = threadIdx.x; i < kTile / 16; i += kThreads) ptx::st_shared_v4(ptx::smem_u32(sm.zero) + 16 * i, 0, 0, 0, 0);
-  if (threadIdx.x >= 128) {  // gradient warpgroups: the view's lse (log2 units) and Delta
-    const int t = threadIdx.x - 128;
-    const float* lb = lse + ((int64_t)b * p.h + j) * p.N;
-    const float* db = delta + ((int64_t)b * p.h + j) * p.N;
-    for (int tt = t; tt < nb * kB; tt += kThreads - 128) {
-      const int64_t n = (int64_t)(t0 + tt) * p.r + gamma;
-      sm.lse2[tt] = lb[n] * kLog2e;
-      sm.dlt[tt] = db[n];
-    }
-  }
   ptx::fence_proxy_async_smem();
   ptx::tc_fence_before();
   __syncthreads();
@@ -123,41 +129,50 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (ptx::elect_one()) {
-      wait(&sm.load_full, 0);
-      ptx::tc_fence_after();
       // ------------------------------------------------------------ MMA
       constexpr uint32_t id_ss = ptx::idesc_bf16(kB, kB, 0, 0);   // S^T, dP^T: K-major A and B
       constexpr uint32_t id_ts = ptx::idesc_bf16(kB, kD, 0, 1);   // dV, dK: A from TMEM, B MN-major
       constexpr uint32_t id_dq = ptx::idesc_bf16(kB, kD, 1, 1);   // dQ: A (dS) MN-major, B (K) MN-major
+      const uint64_t dsd = ptx::sdesc_sw128(ptx::smem_u32(sm.ds[0]), 1024, kTile);  // LBO: next 64 queries
       uint32_t step = 0;
-      for (int kb = 0; kb < nb; ++kb) {
-        const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k[kb]));
-        const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v[kb]));
-        for (int qb = 0; qb < nb; ++qb, ++step) {
-          const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[qb]));
-          const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[qb]));
+      int it = 0;
+      for (int32_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+        wait(&sm.load_full, it & 1);
+        ptx::tc_fence_after();
+        for (int kb = 0; kb < nb; ++kb) {
+          const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k[kb]));
+          const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v[kb]));
+          for (int qb = 0; qb < nb; ++qb, ++step) {
+            const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[qb]));
+            const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[qb]));
 #pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            ptx::mma_ss(tbase + cS, kd + 2 * kk, qd + 2 * kk, id_ss, kk > 0);
-            ptx::mma_ss(tbase + cDP, vd + 2 * kk, gd + 2 * kk, id_ss, kk > 0);
+            for (int kk = 0; kk < kD / 16; ++kk) {
+              ptx::mma_ss(tbase + cS, kd + 2 * kk, qd + 2 * kk, id_ss, kk > 0);
+              ptx::mma_ss(tbase + cDP, vd + 2 * kk, gd + 2 * kk, id_ss, kk > 0);
+            }
+            ptx::tc_commit(&sm.s_full);
+            wait(&sm.p_full, step & 1);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < kB / 16; ++kk) {
+              // K-step of 16 queries: 8 packed TMEM columns of P^T / dS^T, 16 rows (2048 B) of dO / Q
+              ptx::mma_ts(tbase + cDV, tbase + cS + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+              ptx::mma_ts(tbase + cDK, tbase + cDP + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+            }
+#pragma unroll
+            for (int kk = 0; kk < kB / 16; ++kk)  // K-step of 16 keys: 16 rows of dS / K
+              ptx::mma_ss(tbase + cDQ + 64 * qb, dsd + kk * 128, kd + kk * 128, id_dq, (kb > 0 || kk > 0) ? 1u : 0u);
           }
-          ptx::tc_commit(&sm.s_full);
-          wait(&sm.p_full, step & 1);
-          ptx::tc_fence_after();
-          const uint64_t dsd = ptx::sdesc_sw128(ptx::smem_u32(sm.ds[0]), 1024, kTile);  // LBO: next 64 queries
-#pragma unroll
-          for (int kk = 0; kk < kB / 16; ++kk) {
-            // K-step of 16 queries: 8 packed TMEM columns of P^T / dS^T, 16 rows (2048 B) of dO / Q
-            ptx::mma_ts(tbase + cDV, tbase + cS + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
-            ptx::mma_ts(tbase + cDK, tbase + cDP + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < kB / 16; ++kk)  // K-step of 16 keys: 16 rows of dS / K
-            ptx::mma_ss(tbase + cDQ + 64 * qb, dsd + kk * 128, kd + kk * 128, id_dq, (kb > 0 || kk > 0) ? 1u : 0u);
+          ptx::tc_commit(&sm.kv_done);
         }
-        ptx::tc_commit(&sm.kv_done);
+        ptx::tc_commit(&sm.q_done);
+        // the unit's operands are free once its MMAs complete: the next
+        // unit's loads overlap this unit's dQ epilogue and output stores
+        if (u + (int32_t)gridDim.x < n_units) {
+          wait(&sm.q_done, it & 1);
+          issue_loads(u + gridDim.x);
+        }
       }
-      ptx::tc_commit(&sm.q_done);
     }
   } else if (warp >= 4) {
     // ----------------------------------------------- gradient warpgroups
@@ -169,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = (((warp - 4) % 4) * 32) << 16;
     const bool leader = warp % 4 == 0 && lane == 0;
     const uint32_t bar_id = 1 + wg;
-    uint32_t step = 0;
+    uint32_t step = 0, kvn = 0;
     auto stage_store = [&](uint8_t* st, const uint32_t (&v)[2][32], float mul) {
       const uint32_t a0 = ptx::smem_u32(st);
 #pragma unroll
@@ -180,94 +195,113 @@ __global__ void __launch_bounds__(kThreads, 1)
                           ptx::pack_bf16x2(f[6] * mul, f[7] * mul));
       }
     };
-    for (int kb = 0; kb < nb; ++kb) {
-      for (int qb = 0; qb < nb; ++qb, ++step) {
-        wait(&sm.s_full, step & 1);
-        ptx::tc_fence_after();
-        const float* l2 = sm.lse2 + qb * kB;
-        const float* dl = sm.dlt + qb * kB;
-        const uint32_t dsa = ptx::smem_u32(sm.ds[0]);
-#pragma unroll 1
-        for (int c = 2 * wg; c < 2 * wg + 2; ++c) {  // 32 queries per chunk
-          uint32_t s[32], dp[32];
-          ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, s);
-          ptx::tmem_ld32(tbase + lane_base + cDP + 32 * c, dp);
-          ptx::tmem_ld_wait();
-          // Packed P^T / dS^T of chunk c land on columns 16c.., i.e. on the
-          // fp32 columns of chunk c/2: WG1's chunks 2-3 overwrite WG0's chunk
-          // 1, so WG0 signals once chunk 1 is in registers and WG1 waits for
-          // that before its first store (WG0's own order 0, 1 is safe).
-          if (c == 1) ptx::named_bar_arrive(3, 2 * kB);
-          uint32_t pp[16], dd[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int q0 = 32 * c + 2 * e;
-            const float p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
-            const float p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
-            pp[e] = ptx::pack_bf16x2(p0, p1);
-            dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl[q0]),
-                                     p1 * (__uint_as_float(dp[2 * e + 1]) - dl[q0 + 1]));
-          }
-          if (c == 2) ptx::named_bar_sync(3, 2 * kB);
-          ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
-          ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
-          // dS^T row `row` (key) -> MN-major A of dQ: queries 32c..32c+31 are
-          // 16-byte chunks 4(c&1)..4(c&1)+3 of sub-tile c>>1, SW128-swizzled
-          const uint32_t sub = dsa + (c >> 1) * kTile + row * 128;
-#pragma unroll
-          for (int h4 = 0; h4 < 4; ++h4) {
-            const uint32_t chunk = 4 * (c & 1) + h4;
-            ptx::st_shared_v4(sub + ((chunk ^ (row & 7)) * 16), dd[4 * h4], dd[4 * h4 + 1], dd[4 * h4 + 2],
-                              dd[4 * h4 + 3]);
-          }
+    int it = 0;
+    for (int32_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+      const View x = view(u);
+      // the view's lse (log2 units) and Delta; both warpgroups read all of it
+      ptx::named_bar_sync(4, 2 * kB);  // previous unit's steps are done with lse2 / dlt
+      {
+        const int t = threadIdx.x - 128;
+        const float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N;
+        const float* db = delta + ((int64_t)x.b * p.h + x.j) * p.N;
+        for (int tt = t; tt < nb * kB; tt += 2 * kB) {
+          const int64_t n = (int64_t)(x.t0 + tt) * p.r + x.gamma;
+          sm.lse2[tt] = lb[n] * kLog2e;
+          sm.dlt[tt] = db[n];
         }
-        ptx::tmem_st_wait();
-        ptx::fence_proxy_async_smem();
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&sm.p_full);
       }
-      // dK (WG0) / dV (WG1) of key block kb
-      wait(&sm.kv_done, kb & 1);
-      ptx::tc_fence_after();
-      uint32_t a[2][32];
-      if (leader) ptx::tma_store_wait_read<0>();
-      ptx::named_bar_sync(bar_id, 128);
-      const uint32_t col = wg == 0 ? cDK : cDV;
-      ptx::tmem_ld32(tbase + lane_base + col, a[0]);
-      ptx::tmem_ld32(tbase + lane_base + col + 32, a[1]);
-      ptx::tmem_ld_wait();
-      stage_store(sm.stage[wg], a, wg == 0 ? p.scale : 1.0f);
-      ptx::tc_fence_before();
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(bar_id, 128);
-      if (leader) {
-        const int32_t tb = t0 + kb * kB;
-        const CUtensorMap* mo = wg == 0 ? &tm_dk : &tm_dv;
-        ptx::tma_store_5d(mo, sm.stage[wg], 0, j, gamma, tb, b);
-        for (int32_t gz = 0; gz < p.r; ++gz)
-          if (gz != gamma) {
-            ptx::tma_store_5d(mo, sm.zero, 0, j, gz, tb, b);
-            if (wg == 0) ptx::tma_store_5d(&tm_dq, sm.zero, 0, j, gz, tb, b);
+      ptx::named_bar_sync(4, 2 * kB);
+      for (int kb = 0; kb < nb; ++kb) {
+        for (int qb = 0; qb < nb; ++qb, ++step) {
+          wait(&sm.s_full, step & 1);
+          ptx::tc_fence_after();
+          const float* l2 = sm.lse2 + qb * kB;
+          const float* dl = sm.dlt + qb * kB;
+          const uint32_t dsa = ptx::smem_u32(sm.ds[0]);
+#pragma unroll 1
+          for (int c = 2 * wg; c < 2 * wg + 2; ++c) {  // 32 queries per chunk
+            uint32_t s[32], dp[32];
+            ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, s);
+            ptx::tmem_ld32(tbase + lane_base + cDP + 32 * c, dp);
+            ptx::tmem_ld_wait();
+            // Packed P^T / dS^T of chunk c land on columns 16c.., i.e. on the
+            // fp32 columns of chunk c/2: WG1's chunks 2-3 overwrite WG0's chunk
+            // 1, so WG0 signals once chunk 1 is in registers and WG1 waits for
+            // that before its first store (WG0's own order 0, 1 is safe).
+            if (c == 1) ptx::named_bar_arrive(3, 2 * kB);
+            uint32_t pp[16], dd[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int q0 = 32 * c + 2 * e;
+              const float p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
+              const float p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
+              pp[e] = ptx::pack_bf16x2(p0, p1);
+              dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl[q0]),
+                                       p1 * (__uint_as_float(dp[2 * e + 1]) - dl[q0 + 1]));
+            }
+            if (c == 2) ptx::named_bar_sync(3, 2 * kB);
+            ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
+            ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
+            // dS^T row `row` (key) -> MN-major A of dQ: queries 32c..32c+31 are
+            // 16-byte chunks 4(c&1)..4(c&1)+3 of sub-tile c>>1, SW128-swizzled
+            const uint32_t sub = dsa + (c >> 1) * kTile + row * 128;
+#pragma unroll
+            for (int h4 = 0; h4 < 4; ++h4) {
+              const uint32_t chunk = 4 * (c & 1) + h4;
+              ptx::st_shared_v4(sub + ((chunk ^ (row & 7)) * 16), dd[4 * h4], dd[4 * h4 + 1], dd[4 * h4 + 2],
+                                dd[4 * h4 + 3]);
+            }
           }
-        ptx::tma_store_commit();
+          ptx::tmem_st_wait();
+          ptx::fence_proxy_async_smem();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&sm.p_full);
+        }
+        // dK (WG0) / dV (WG1) of key block kb
+        wait(&sm.kv_done, kvn & 1);
+        ++kvn;
+        ptx::tc_fence_after();
+        uint32_t a[2][32];
+        if (leader) ptx::tma_store_wait_read<0>();
+        ptx::named_bar_sync(bar_id, 128);
+        const uint32_t col = wg == 0 ? cDK : cDV;
+        ptx::tmem_ld32(tbase + lane_base + col, a[0]);
+        ptx::tmem_ld32(tbase + lane_base + col + 32, a[1]);
+        ptx::tmem_ld_wait();
+        stage_store(sm.stage[wg], a, wg == 0 ? p.scale : 1.0f);
+        ptx::tc_fence_before();
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(bar_id, 128);
+        if (leader) {
+          const int32_t tb = x.t0 + kb * kB;
+          const CUtensorMap* mo = wg == 0 ? &tm_dk : &tm_dv;
+          ptx::tma_store_5d(mo, sm.stage[wg], 0, x.j, x.gamma, tb, x.b);
+          for (int32_t gz = 0; gz < p.r; ++gz)
+            if (gz != x.gamma) {
+              ptx::tma_store_5d(mo, sm.zero, 0, x.j, gz, tb, x.b);
+              if (wg == 0) ptx::tma_store_5d(&tm_dq, sm.zero, 0, x.j, gz, tb, x.b);
+            }
+          ptx::tma_store_commit();
+        }
       }
-    }
-    // dQ blocks (TMEM lanes = query rows), alternating between the warpgroups
-    wait(&sm.q_done, 0);
-    ptx::tc_fence_after();
-    for (int qb = wg; qb < nb; qb += 2) {
-      uint32_t a[2][32];
-      if (leader) ptx::tma_store_wait_read<0>();
-      ptx::named_bar_sync(bar_id, 128);
-      ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb, a[0]);
-      ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb + 32, a[1]);
-      ptx::tmem_ld_wait();
-      stage_store(sm.stage[wg], a, p.scale);
-      ptx::fence_proxy_async_smem();
-      ptx::named_bar_sync(bar_id, 128);
-      if (leader) {
-        ptx::tma_store_5d(&tm_dq, sm.stage[wg], 0, j, gamma, t0 + qb * kB, b);
-        ptx::tma_store_commit();
+      // dQ blocks (TMEM lanes = query rows), alternating between the warpgroups
+      wait(&sm.q_done, it & 1);
+      ptx::tc_fence_after();
+      for (int qb = wg; qb < nb; qb += 2) {
+        uint32_t a[2][32];
+        if (leader) ptx::tma_store_wait_read<0>();
+        ptx::named_bar_sync(bar_id, 128);
+        ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb, a[0]);
+        ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb + 32, a[1]);
+        ptx::tmem_ld_wait();
+        stage_store(sm.stage[wg], a, p.scale);
+        ptx::tc_fence_before();
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(bar_id, 128);
+        if (leader) {
+          ptx::tma_store_5d(&tm_dq, sm.stage[wg], 0, x.j, x.gamma, x.t0 + qb * kB, x.b);
+          ptx::tma_store_commit();
+        }
       }
     }
     if (leader) ptx::tma_store_wait_all<0>();
@@ -343,6 +377,7 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
   p.h = (int32_t)g.h;
   p.n_seg = (int32_t)(g.N / g.w);
   p.nblk = p.m / kB;
+  p.n_units = (int32_t)(g.B * g.h * p.n_seg);
   p.scale = g.scale;
   p.c = g.scale * kLog2e;
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
@@ -357,7 +392,14 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
     *why = "cudaFuncSetAttribute failed";
     return 0;
   }
-  const unsigned grid = (unsigned)(g.B * g.h * p.n_seg);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(p.n_units, sms);  // persistent: one CTA per SM
   dfa_bwd_sm100_kernel<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mg, mdq, mdk, mdv, lse, delta, p);
   *err = cudaGetLastError();
   return 1;
