@@ -149,12 +149,25 @@ struct Sm100Params {
   int32_t offsets[kMaxHeads];
 };
 
+#ifndef DFA_HEAD_MAJOR
+#define DFA_HEAD_MAJOR 1
+#endif
+// Unit order.  Head-major (default): u = (b * n_pairs + pair) * h + j, so the
+// h CTAs running side by side read the h heads' 128-byte column blocks of the
+// SAME token rows -- one DRAM page opened once instead of h times.
 __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
   Unit x;
+#if DFA_HEAD_MAJOR
+  const int32_t bp = p.div_h.div(u);
+  x.j = u - bp * p.h;
+  x.b = p.div_pairs.div(bp);
+  const int32_t pair = bp - x.b * p.n_pairs;
+#else
   const int32_t bj = p.div_pairs.div(u);
   const int32_t pair = u - bj * p.n_pairs;
   x.b = p.div_h.div(bj);
   x.j = bj - x.b * p.h;
+#endif
   x.gamma = p.offsets[x.j];
   x.t0 = pair * kUnitRows;
   int32_t lo[2], hi[2];

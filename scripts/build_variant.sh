@@ -11,6 +11,6 @@ mkdir -p $OUT/build_$NAME
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr $DEFS"
 nvcc $FL -c $C/dfa_sm100.cu -o $OUT/build_$NAME/dfa_sm100.o
-nvcc $ARCH -shared -o $OUT/libdfa_$NAME.so $C/build/dfa_api.cpp.o $C/build/dfa_simt.cu.o $OUT/build_$NAME/dfa_sm100.o \
-  $C/build/dfa_combine.cu.o -lcudart_static -lrt -ldl -lpthread
+OTHERS=$(ls $C/build/*.o | grep -v dfa_sm100.cu.o)
+nvcc $ARCH -shared -o $OUT/libdfa_$NAME.so $OTHERS $OUT/build_$NAME/dfa_sm100.o -lcudart_static -lrt -ldl -lpthread
 echo built $OUT/libdfa_$NAME.so

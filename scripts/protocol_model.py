@@ -48,8 +48,8 @@ class Bar:
 
 
 def make_unit(p, u):
-    pair, bj = u % p["n_pairs"], u // p["n_pairs"]
-    j, b = bj % p["h"], bj // p["h"]
+    j, bp = u % p["h"], u // p["h"]  # head-major unit order (DFA_HEAD_MAJOR)
+    pair, b = bp % p["n_pairs"], bp // p["n_pairs"]
     t0 = pair * 2 * KBM
     lo, hi = [], []
     for s in range(2):
