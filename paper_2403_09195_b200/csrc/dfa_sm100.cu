@@ -64,8 +64,19 @@ constexpr int kBM = 128;               // query rows per slot (MMA M)
 constexpr int kBN = 128;               // keys per tile (MMA N of Q K^T, K of P V)
 constexpr int kUnitRows = 2 * kBM;     // t'-rows per work unit
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 bf16), SW128
+#ifndef DFA_K_STAGES
+#define DFA_K_STAGES 3
+#endif
+#ifndef DFA_V_STAGES
+#define DFA_V_STAGES 3
+#endif
+#ifndef DFA_O_STAGES
+#define DFA_O_STAGES 2
+#endif
 constexpr int kQStages = 2;
-constexpr int kKVStages = 3;
+constexpr int kKStages = DFA_K_STAGES;  // K ring depth (loads in flight ahead of Q K^T)
+constexpr int kVStages = DFA_V_STAGES;  // V ring depth
+constexpr int kOStages = DFA_O_STAGES;  // epilogue staging tiles (slot s uses s % kOStages)
 constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSBufs = 3;                                  // rotating S/P buffers
@@ -97,13 +108,13 @@ struct Unit {
 
 struct __align__(1024) SmemLayout {
   uint8_t q[kQStages][2][kTileBytes];  // contiguous: tile (stage, slot) at index stage * 2 + slot
-  uint8_t k[kKVStages][kTileBytes];
-  uint8_t v[kKVStages][kTileBytes];
-  uint8_t ostage[2][kTileBytes];
+  uint8_t k[kKStages][kTileBytes];
+  uint8_t v[kVStages][kTileBytes];
+  uint8_t ostage[kOStages][kTileBytes];
   uint8_t zero[kTileBytes];
   uint64_t q_full[kQStages], q_empty[kQStages];
-  uint64_t k_full[kKVStages], k_empty[kKVStages];  // K ring: freed when its last Q K^T completes
-  uint64_t v_full[kKVStages], v_empty[kKVStages];  // V ring: freed when its last P V completes
+  uint64_t k_full[kKStages], k_empty[kKStages];  // K ring: freed when its last Q K^T completes
+  uint64_t v_full[kVStages], v_empty[kVStages];  // V ring: freed when its last P V completes
   uint64_t s_full[2][kSBufs];  // MMA -> slot s: S ready in buffer b
   uint64_t p_full[kSBufs];     // slot -> P V issuer: P written in buffer b (128 arrivals)
   uint64_t s_free[kSBufs];     // P V issuer -> Q K^T issuer: P V of buffer b completed
@@ -149,6 +160,14 @@ struct Sm100Params {
   int32_t offsets[kMaxHeads];
 };
 
+// Profiling probes (variant builds only, results wrong): drop the
+// exponentials / the zero boxes to measure what each costs.
+#ifndef DFA_PROBE_NO_EXP
+#define DFA_PROBE_NO_EXP 0
+#endif
+#ifndef DFA_PROBE_NO_ZERO
+#define DFA_PROBE_NO_ZERO 0
+#endif
 #ifndef DFA_HEAD_MAJOR
 #define DFA_HEAD_MAJOR 1
 #endif
@@ -278,9 +297,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.q_full[s], 1);
       ptx::mbar_init(&sm.q_empty[s], 1);
     }
-    for (int s = 0; s < kKVStages; ++s) {
+    for (int s = 0; s < kKStages; ++s) {
       ptx::mbar_init(&sm.k_full[s], 1);
       ptx::mbar_init(&sm.k_empty[s], 1);
+    }
+    for (int s = 0; s < kVStages; ++s) {
       ptx::mbar_init(&sm.v_full[s], 1);
       ptx::mbar_init(&sm.v_empty[s], 1);
     }
@@ -330,9 +351,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_load_5d(sm.q[qs][0], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0, x.b, pol);
         ptx::tma_load_5d(sm.q[qs][1], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0 + kBM, x.b, pol);
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
-          const uint32_t st = g % kKVStages;
+          const uint32_t st = g % kKStages;
           DFA_TRACE(0, TR_KV_WAIT);
-          DFA_WAIT(&sm.k_empty[st], ((g / kKVStages) & 1) ^ 1, 3);
+          DFA_WAIT(&sm.k_empty[st], ((g / kKStages) & 1) ^ 1, 3);
           DFA_TRACE(0, TR_KV_ISSUE);
           ptx::mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
           ptx::tma_load_5d(sm.k[st], &tm_k, &sm.k_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
@@ -347,8 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Unit x = make_unit(p, u);
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
-          const uint32_t st = g % kKVStages;
-          DFA_WAIT(&sm.v_empty[st], ((g / kKVStages) & 1) ^ 1, 4);
+          const uint32_t st = g % kVStages;
+          DFA_WAIT(&sm.v_empty[st], ((g / kVStages) & 1) ^ 1, 4);
           ptx::mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
           ptx::tma_load_5d(sm.v[st], &tm_v, &sm.v_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
         }
@@ -402,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++steps;
           }
           ptx::tc_commit(&sm.k_empty[gs]);  // every Q K^T of this K tile issued
-          if (++gs == kKVStages) {
+          if (++gs == kKStages) {
             gs = 0;
             gpar ^= 1u;
           }
@@ -460,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             b = (b == kSBufs - 1) ? 0 : b + 1;
           }
           ptx::tc_commit(&sm.v_empty[gs]);  // every P V of this V tile issued
-          if (++gs == kKVStages) {
+          if (++gs == kVStages) {
             gs = 0;
             gpar ^= 1u;
           }
@@ -572,7 +593,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           xv[e] = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * e]), __uint_as_float(sr[c][2 * e + 1])), c2, n2);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          if ((kPolyMask >> e) & 1u) {
+          if (DFA_PROBE_NO_EXP) {
+            // profiling probe only (wrong results): no exponentials
+          } else if ((kPolyMask >> e) & 1u) {
             xv[e] = ptx::ex2_poly2(xv[e]);
           } else {
             xv[e].x = ptx::ex2(xv[e].x);
@@ -646,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (leader) {
             ptx::tma_store_wait_read<0>();  // staging no longer read by an earlier store
             ptx::mbar_arrive_expect_tx(&sm.oload_full[s], kTileBytes);
-            ptx::tma_load_5d(sm.ostage[s], &tm_o, &sm.oload_full[s], 0, x.j, x.gamma, ts0, x.b, pol_merge);
+            ptx::tma_load_5d(sm.ostage[s % kOStages], &tm_o, &sm.oload_full[s], 0, x.j, x.gamma, ts0, x.b, pol_merge);
           }
           if (lrow) lse_prev = lrow[x.gamma];
         }
@@ -666,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_arrive(&sm.stat_empty[s]);  // stats buffer `ph` may be reused
         ptx::mbar_arrive(&sm.o_empty[s]);     // O_s may be overwritten by the next unit
         const float lse_new = mref * p.scale + __logf(l);
-        const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s]);
+        const uint32_t stage_addr = ptx::smem_u32(sm.ostage[s % kOStages]);
         if (!p.merge) {
           const float inv = valid_q ? 1.0f / l : 0.0f;
           // the previous TMA store from this staging tile must have finished reading it
@@ -712,10 +735,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, kBM);
         if (leader) {
-          ptx::tma_store_5d(&tm_o, sm.ostage[s], 0, x.j, x.gamma, ts0, x.b);
+          ptx::tma_store_5d(&tm_o, sm.ostage[s % kOStages], 0, x.j, x.gamma, ts0, x.b);
           if (!p.merge)
             for (int32_t gz = 0; gz < p.r; ++gz)
-              if (gz != x.gamma) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
+              if (gz != x.gamma && !DFA_PROBE_NO_ZERO) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
           ptx::tma_store_commit();
         }
         DFA_TRACE(4, TR_STORE_ISSUED);
