@@ -626,7 +626,7 @@ dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtyp
   if (!gemm(M, D, D, att, wt->wo, x1, x, wt->bo)) return fail(DFA_ERR_CUDA, "encoder_block: wo: %s", why);
   launches += dfa_impl::launch_layer_norm(dtype, x1, wt->ln2_g, wt->ln2_b, ln, M, (int)D, s);
   if (!gemm(M, H, D, ln, wt->w1, hid, nullptr, wt->b1)) return fail(DFA_ERR_CUDA, "encoder_block: w1: %s", why);
-  launches += dfa_impl::launch_gelu(dtype, hid, M * H, s);
+  launches += dfa_impl::launch_gelu(dtype, hid, hid, M * H, s);
   if (!gemm(M, D, H, hid, wt->w2, out, x1, wt->b2)) return fail(DFA_ERR_CUDA, "encoder_block: w2: %s", why);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "encoder_block: %s", cudaGetErrorString(err));

@@ -58,7 +58,7 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
                   const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why);
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
                       cudaStream_t stream);
-int launch_gelu(int dtype, void* x, int64_t n, cudaStream_t stream);
+int launch_gelu(int dtype, const void* xin, void* x, int64_t n, cudaStream_t stream);  // x = GELU(xin); may alias
 // wq/wk/wv [h, D, d] -> packed [D, 3, h, d] (one QKV GEMM writes q|k|v per token).
 int launch_pack_qkv(int dtype, const void* wq, const void* wk, const void* wv, void* out, int64_t h, int64_t D,
                     int64_t d, cudaStream_t stream);

@@ -86,7 +86,7 @@ def main():
          "ln2_b": torch.zeros(D), "w1": s * torch.randn(D, hidden), "b1": torch.zeros(hidden),
          "w2": torch.randn(hidden, D) / hidden ** 0.5, "b2": torch.zeros(D)}
     p = {kk: vv.to("cuda", bf).contiguous() for kk, vv in p.items()}
-    wsb = torch.empty(7 * B * N * D * 2 + B * N * hidden * 2 + (40 << 20), dtype=torch.uint8, device="cuda")
+    wsb = torch.empty(7 * B * N * D * 2 + 2 * B * N * hidden * 2 + (40 << 20), dtype=torch.uint8, device="cuda")
     y = torch.empty_like(x)
     ms = time_ms(lambda: dfa.encoder_block_forward(x, p, cfg, out=y, workspace=wsb), iters=10)
     blk_flop = proj_flop + fwd_flop + 2 * 2 * B * N * D * hidden
