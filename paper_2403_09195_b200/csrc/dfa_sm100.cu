@@ -77,6 +77,12 @@ constexpr int kQStages = 2;
 constexpr int kKStages = DFA_K_STAGES;  // K ring depth (loads in flight ahead of Q K^T)
 constexpr int kVStages = DFA_V_STAGES;  // V ring depth
 constexpr int kOStages = DFA_O_STAGES;  // epilogue staging tiles (slot s uses s % kOStages)
+#ifndef DFA_ZERO_ROWS
+#define DFA_ZERO_ROWS 128
+#endif
+// Rows per zero box: a smaller zero tile (stored 128 / kZeroRows times per
+// class) frees shared memory for deeper load rings.
+constexpr int kZeroRows = DFA_ZERO_ROWS;
 constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSBufs = 3;                                  // rotating S/P buffers
@@ -111,7 +117,7 @@ struct __align__(1024) SmemLayout {
   uint8_t k[kKStages][kTileBytes];
   uint8_t v[kVStages][kTileBytes];
   uint8_t ostage[kOStages][kTileBytes];
-  uint8_t zero[kTileBytes];
+  uint8_t zero[kZeroRows * 128];
   uint64_t q_full[kQStages], q_empty[kQStages];
   uint64_t k_full[kKStages], k_empty[kKStages];  // K ring: freed when its last Q K^T completes
   uint64_t v_full[kVStages], v_empty[kVStages];  // V ring: freed when its last P V completes
@@ -278,7 +284,8 @@ template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
-                     float* __restrict__ lse, const __grid_constant__ Sm100Params p, uint64_t* __restrict__ trace,
+                     const __grid_constant__ CUtensorMap tm_z, float* __restrict__ lse,
+                     const __grid_constant__ Sm100Params p, uint64_t* __restrict__ trace,
                      unsigned long long* __restrict__ watchdog) {
   extern __shared__ uint8_t smem_raw[];
   SmemLayout& sm =
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = ptx::lane_id();
 
   // zero tile for the unselected offset classes
-  for (uint32_t i = threadIdx.x; i < kTileBytes / 16; i += kThreads)
+  for (uint32_t i = threadIdx.x; i < kZeroRows * 128 / 16; i += kThreads)
     ptx::st_shared_v4(ptx::smem_u32(sm.zero) + 16 * i, 0u, 0u, 0u, 0u);
   ptx::fence_proxy_async_smem();
 
@@ -324,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tma_prefetch_desc(&tm_k);
     ptx::tma_prefetch_desc(&tm_v);
     ptx::tma_prefetch_desc(&tm_o);
+    ptx::tma_prefetch_desc(&tm_z);
   } else if (warp == 2) {
     ptx::tmem_alloc<kTmemCols>(&sm.tmem_base);
   }
@@ -738,7 +746,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tma_store_5d(&tm_o, sm.ostage[s % kOStages], 0, x.j, x.gamma, ts0, x.b);
           if (!p.merge)
             for (int32_t gz = 0; gz < p.r; ++gz)
-              if (gz != x.gamma && !DFA_PROBE_NO_ZERO) ptx::tma_store_5d(&tm_o, sm.zero, 0, x.j, gz, ts0, x.b);
+              if (gz != x.gamma && !DFA_PROBE_NO_ZERO)
+                for (int32_t zr = 0; zr < kBM; zr += kZeroRows)
+                  ptx::tma_store_5d(&tm_z, sm.zero, 0, x.j, gz, ts0 + zr, x.b);
           ptx::tma_store_commit();
         }
         DFA_TRACE(4, TR_STORE_ISSUED);
@@ -778,12 +788,13 @@ EncodeTiledFn get_encode_fn() {
 // out-of-range rows are zero-filled on load and dropped on store.  `ld` is
 // the token stride in elements (h * 64 when contiguous; 3 * h * 64 when q,
 // k, v are column blocks of one fused-projection output).
-bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld) {
+bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld,
+              uint32_t box_rows = 128) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[5] = {(cuuint64_t)kD, (cuuint64_t)h, (cuuint64_t)r, (cuuint64_t)(N / r), (cuuint64_t)B};
   cuuint64_t strides[4] = {(cuuint64_t)kD * 2, (cuuint64_t)ld * 2, (cuuint64_t)r * ld * 2, (cuuint64_t)N * ld * 2};
-  cuuint32_t box[5] = {kD, 1, 1, 128, 1};
+  cuuint32_t box[5] = {kD, 1, 1, box_rows, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -829,9 +840,10 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
     *err = cudaErrorInvalidValue;
     return 0;
   }
-  CUtensorMap mq, mk, mv, mo;
+  CUtensorMap mq, mk, mv, mo, mz;
   if (!make_map(&mq, q, g.B, g.N, g.r, g.h, g.ldq) || !make_map(&mk, k, g.B, g.N, g.r, g.h, g.ldk) ||
-      !make_map(&mv, v, g.B, g.N, g.r, g.h, g.ldv) || !make_map(&mo, o, g.B, g.N, g.r, g.h, g.ldo)) {
+      !make_map(&mv, v, g.B, g.N, g.r, g.h, g.ldv) || !make_map(&mo, o, g.B, g.N, g.r, g.h, g.ldo) ||
+      !make_map(&mz, o, g.B, g.N, g.r, g.h, g.ldo, kZeroRows)) {
     *why = "cuTensorMapEncodeTiled failed";
     *err = cudaErrorInvalidValue;
     return 0;
@@ -866,9 +878,9 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   }
   const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
   if (trace)
-    dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, trace, watchdog);
+    dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, mz, lse, p, trace, watchdog);
   else
-    dfa_sm100_kernel<false><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, lse, p, nullptr, nullptr);
+    dfa_sm100_kernel<false><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, mz, lse, p, nullptr, nullptr);
   *err = cudaGetLastError();
   return 1;
 }
