@@ -64,6 +64,7 @@ struct __align__(1024) BwdSmem {
 
 struct BwdSm100Params {
   int32_t N, T, m, r, h, n_seg, nblk, n_units;
+  int32_t mseg;  // segment view rows when < 128: 128 / mseg segments packed per tile, block-diagonal mask
   float c, scale;
   int32_t offsets[kMaxHeads];
 };
@@ -233,8 +234,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int q0 = 32 * c + 2 * e;
-              const float p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
-              const float p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
+              float p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
+              float p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
+              if (p.mseg < kB) {  // packed short segments: no interaction across segments
+                const uint32_t kseg = row / p.mseg;
+                if ((uint32_t)q0 / p.mseg != kseg) p0 = 0.0f;
+                if ((uint32_t)(q0 + 1) / p.mseg != kseg) p1 = 0.0f;
+              }
               pp[e] = ptx::pack_bf16x2(p0, p1);
               dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl[q0]),
                                        p1 * (__uint_as_float(dp[2 * e + 1]) - dl[q0 + 1]));
@@ -314,6 +320,414 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ============================================================================
+// Long segments (m = w / r >= 512, m % 128 == 0): the accumulators of a whole
+// view no longer fit TMEM next to S / dP, so the backward splits FA2-style
+// into two tcgen05 kernels, each deterministic:
+//   dkdv_long: unit = (b, j, segment, key block kb); K_kb, V_kb resident, the
+//              view's (Q, dO) blocks streamed through a 2-stage ring;
+//              S^T, dP^T -> P^T, dS^T (TMEM, bf16) -> dV += P^T dO, dK += dS^T Q.
+//   dq_long:   unit = (b, j, segment, query block qb); Q_qb, dO_qb resident,
+//              (K, V) blocks streamed; S = Q K^T, dP = dO V^T (lanes = queries,
+//              so lse / Delta are per-thread scalars) -> dS (TMEM, bf16) ->
+//              dQ += dS K.
+// 7 GEMM-shaped products per (kb, qb) pair instead of the fused kernel's 5.
+struct LongParams {
+  int32_t N, m, r, h, n_seg, nblk, n_units;
+  float c, scale;
+  int32_t offsets[kMaxHeads];
+};
+
+struct LongView {
+  int32_t b, j, gamma, t0, blk;  // t0: first t' of the view; blk: kb or qb
+};
+__device__ __forceinline__ LongView long_view(const LongParams& p, int32_t u) {
+  LongView v;
+  v.blk = u % p.nblk;
+  const int32_t rest = u / p.nblk;
+  const int32_t seg = rest % p.n_seg, bj = rest / p.n_seg;
+  v.j = bj % p.h;
+  v.b = bj / p.h;
+  v.gamma = p.offsets[v.j];
+  v.t0 = seg * p.m;
+  return v;
+}
+
+struct __align__(1024) DkdvSmem {
+  uint8_t k[kTile], v[kTile];
+  uint8_t q[2][kTile], g[2][kTile];  // (Q, dO) ring
+  uint8_t stage[2][kTile];
+  uint8_t zero[kTile];
+  float lse2[2][kB], dlt[2][kB];     // per step, double-buffered (prefetched one step ahead)
+  uint64_t kv_full, kv_done, ring_full[2], ring_empty[2], s_full, p_full;
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    dfa_bwd_dkdv_long_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
+                             const __grid_constant__ CUtensorMap tm_dk, const __grid_constant__ CUtensorMap tm_dv,
+                             const float* __restrict__ lse, const float* __restrict__ delta,
+                             const __grid_constant__ LongParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  DkdvSmem& sm = *reinterpret_cast<DkdvSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int nq = p.nblk;
+  if (warp == 0 && lane == 0) {
+    ptx::mbar_init(&sm.kv_full, 1);
+    ptx::mbar_init(&sm.kv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&sm.ring_full[i], 1);
+      ptx::mbar_init(&sm.ring_empty[i], 1);
+    }
+    ptx::mbar_init(&sm.s_full, 1);
+    ptx::mbar_init(&sm.p_full, 2 * kB);
+    ptx::fence_barrier_init();
+  } else if (warp == 1) {
+    ptx::tmem_alloc<512>(&sm.tmem_base);
+  }
+  for (uint32_t i = threadIdx.x; i < kTile / 16; i += kThreads) ptx::st_shared_v4(ptx::smem_u32(sm.zero) + 16 * i, 0, 0, 0, 0);
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+  constexpr uint32_t cS = 0, cDP = 128, cDV = 256, cDK = 320;
+
+  if (warp == 3) {
+    // ------------------------------------------------------- TMA producer
+    if (ptx::elect_one()) {
+      const uint64_t pol = ptx::policy_evict_first();
+      uint32_t gstep = 0;
+      int it = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+        const LongView x = long_view(p, u);
+        if (it > 0) wait(&sm.kv_done, (it - 1) & 1);  // previous unit's MMAs finished with K / V
+        ptx::mbar_arrive_expect_tx(&sm.kv_full, 2 * kTile);
+        const int32_t tk = x.t0 + x.blk * kB;
+        ptx::tma_load_5d(sm.k, &tm_k, &sm.kv_full, 0, x.j, x.gamma, tk, x.b, pol);
+        ptx::tma_load_5d(sm.v, &tm_v, &sm.kv_full, 0, x.j, x.gamma, tk, x.b, pol);
+        for (int qb = 0; qb < nq; ++qb, ++gstep) {
+          const uint32_t st = gstep & 1;
+          wait(&sm.ring_empty[st], ((gstep >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&sm.ring_full[st], 2 * kTile);
+          const int32_t tq = x.t0 + qb * kB;
+          ptx::tma_load_5d(sm.q[st], &tm_q, &sm.ring_full[st], 0, x.j, x.gamma, tq, x.b, pol);
+          ptx::tma_load_5d(sm.g[st], &tm_g, &sm.ring_full[st], 0, x.j, x.gamma, tq, x.b, pol);
+        }
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------------------- MMA
+    if (ptx::elect_one()) {
+      constexpr uint32_t id_ss = ptx::idesc_bf16(kB, kB, 0, 0);
+      constexpr uint32_t id_ts = ptx::idesc_bf16(kB, kD, 0, 1);
+      const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k));
+      const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v));
+      uint32_t step = 0;
+      int it = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+        wait(&sm.kv_full, it & 1);
+        ptx::tc_fence_after();
+        for (int qb = 0; qb < nq; ++qb, ++step) {
+          const uint32_t st = step & 1;
+          wait(&sm.ring_full[st], (step >> 1) & 1);
+          ptx::tc_fence_after();
+          const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[st]));
+          const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[st]));
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            ptx::mma_ss(tbase + cS, kd + 2 * kk, qd + 2 * kk, id_ss, kk > 0);
+            ptx::mma_ss(tbase + cDP, vd + 2 * kk, gd + 2 * kk, id_ss, kk > 0);
+          }
+          ptx::tc_commit(&sm.s_full);
+          wait(&sm.p_full, step & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kB / 16; ++kk) {
+            ptx::mma_ts(tbase + cDV, tbase + cS + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_ts(tbase + cDK, tbase + cDP + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+          }
+          ptx::tc_commit(&sm.ring_empty[st]);
+        }
+        ptx::tc_commit(&sm.kv_done);
+      }
+    }
+  } else if (warp >= 4) {
+    // ----------------------------------------------- gradient warpgroups
+    const int wg = (warp - 4) / 4;
+    const uint32_t row = ((warp - 4) % 4) * 32 + lane;
+    const uint32_t lane_base = (((warp - 4) % 4) * 32) << 16;
+    const bool leader = warp % 4 == 0 && lane == 0;
+    const int t = threadIdx.x - 128;  // 0..255: entry t % 128 of lse (t < 128) or Delta
+    // this CTA's step sequence: (unit it, qb) -> lse / Delta of query block qb
+    auto fetch = [&](int32_t u, int qb) -> float {
+      const LongView x = long_view(p, u);
+      const int64_t n = (int64_t)(x.t0 + qb * kB + (t & 127)) * p.r + x.gamma;
+      const int64_t base = ((int64_t)x.b * p.h + x.j) * p.N;
+      return t < 128 ? lse[base + n] * kLog2e : delta[base + n];
+    };
+    auto put = [&](int buf, float val) {
+      if (t < 128) sm.lse2[buf][t] = val;
+      else sm.dlt[buf][t - 128] = val;
+    };
+    if ((int32_t)blockIdx.x < p.n_units) put(0, fetch(blockIdx.x, 0));
+    ptx::named_bar_sync(4, 2 * kB);
+    uint32_t step = 0;
+    int it = 0;
+    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+      const LongView x = long_view(p, u);
+      for (int qb = 0; qb < nq; ++qb, ++step) {
+        // prefetch the next step's lse / Delta (stored after this step's work)
+        int32_t nu = u;
+        int nqb = qb + 1;
+        if (nqb == nq) {
+          nqb = 0;
+          nu = u + gridDim.x;
+        }
+        const bool has_next = nu < p.n_units;
+        const float nxt = has_next ? fetch(nu, nqb) : 0.0f;
+        const int buf = step & 1;
+        wait(&sm.s_full, step & 1);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int c = 2 * wg; c < 2 * wg + 2; ++c) {
+          uint32_t sv[32], dp[32];
+          ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, sv);
+          ptx::tmem_ld32(tbase + lane_base + cDP + 32 * c, dp);
+          ptx::tmem_ld_wait();
+          if (c == 1) ptx::named_bar_arrive(3, 2 * kB);  // see dfa_bwd_sm100_kernel
+          uint32_t pp[16], dd[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int q0 = 32 * c + 2 * e;
+            const float p0 = ptx::ex2(__uint_as_float(sv[2 * e]) * p.c - sm.lse2[buf][q0]);
+            const float p1 = ptx::ex2(__uint_as_float(sv[2 * e + 1]) * p.c - sm.lse2[buf][q0 + 1]);
+            pp[e] = ptx::pack_bf16x2(p0, p1);
+            dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - sm.dlt[buf][q0]),
+                                     p1 * (__uint_as_float(dp[2 * e + 1]) - sm.dlt[buf][q0 + 1]));
+          }
+          if (c == 2) ptx::named_bar_sync(3, 2 * kB);
+          ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
+          ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.p_full);
+        if (has_next) put(buf ^ 1, nxt);
+        ptx::named_bar_sync(4, 2 * kB);
+      }
+      // dK (WG0, scaled) / dV (WG1) of this key block, + zero boxes of the other classes
+      wait(&sm.kv_done, it & 1);
+      ptx::tc_fence_after();
+      uint32_t a[2][32];
+      if (leader) ptx::tma_store_wait_read<0>();
+      ptx::named_bar_sync(1 + wg, 128);
+      const uint32_t col = wg == 0 ? cDK : cDV;
+      ptx::tmem_ld32(tbase + lane_base + col, a[0]);
+      ptx::tmem_ld32(tbase + lane_base + col + 32, a[1]);
+      ptx::tmem_ld_wait();
+      const float mul = wg == 0 ? p.scale : 1.0f;
+      const uint32_t a0 = ptx::smem_u32(sm.stage[wg]);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float* f = reinterpret_cast<const float*>(&a[c >> 2][(c & 3) * 8]);
+        ptx::st_shared_v4(a0 + row * 128 + ((c ^ (row & 7)) * 16), ptx::pack_bf16x2(f[0] * mul, f[1] * mul),
+                          ptx::pack_bf16x2(f[2] * mul, f[3] * mul), ptx::pack_bf16x2(f[4] * mul, f[5] * mul),
+                          ptx::pack_bf16x2(f[6] * mul, f[7] * mul));
+      }
+      ptx::tc_fence_before();
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1 + wg, 128);
+      if (leader) {
+        const int32_t tk = x.t0 + x.blk * kB;
+        const CUtensorMap* mo = wg == 0 ? &tm_dk : &tm_dv;
+        ptx::tma_store_5d(mo, sm.stage[wg], 0, x.j, x.gamma, tk, x.b);
+        for (int32_t gz = 0; gz < p.r; ++gz)
+          if (gz != x.gamma) ptx::tma_store_5d(mo, sm.zero, 0, x.j, gz, tk, x.b);
+        ptx::tma_store_commit();
+      }
+    }
+    if (leader) ptx::tma_store_wait_all<0>();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tbase);
+  }
+}
+
+struct __align__(1024) DqSmem {
+  uint8_t q[kTile], g[kTile];
+  uint8_t k[2][kTile], v[2][kTile];  // (K, V) ring
+  uint8_t stage[kTile];
+  uint8_t zero[kTile];
+  uint64_t qg_full, q_done, ring_full[2], ring_empty[2], s_full, p_full;
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    dfa_bwd_dq_long_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
+                           const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse,
+                           const float* __restrict__ delta, const __grid_constant__ LongParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  DqSmem& sm = *reinterpret_cast<DqSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  const int nk = p.nblk;
+  if (warp == 0 && lane == 0) {
+    ptx::mbar_init(&sm.qg_full, 1);
+    ptx::mbar_init(&sm.q_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&sm.ring_full[i], 1);
+      ptx::mbar_init(&sm.ring_empty[i], 1);
+    }
+    ptx::mbar_init(&sm.s_full, 1);
+    ptx::mbar_init(&sm.p_full, 2 * kB);
+    ptx::fence_barrier_init();
+  } else if (warp == 1) {
+    ptx::tmem_alloc<512>(&sm.tmem_base);
+  }
+  for (uint32_t i = threadIdx.x; i < kTile / 16; i += kThreads) ptx::st_shared_v4(ptx::smem_u32(sm.zero) + 16 * i, 0, 0, 0, 0);
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = sm.tmem_base;
+  constexpr uint32_t cS = 0, cDP = 128, cDQ = 256;
+
+  if (warp == 3) {
+    if (ptx::elect_one()) {
+      const uint64_t pol = ptx::policy_evict_first();
+      uint32_t gstep = 0;
+      int it = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+        const LongView x = long_view(p, u);
+        if (it > 0) wait(&sm.q_done, (it - 1) & 1);  // previous unit's MMAs finished with Q / dO
+        ptx::mbar_arrive_expect_tx(&sm.qg_full, 2 * kTile);
+        const int32_t tq = x.t0 + x.blk * kB;
+        ptx::tma_load_5d(sm.q, &tm_q, &sm.qg_full, 0, x.j, x.gamma, tq, x.b, pol);
+        ptx::tma_load_5d(sm.g, &tm_g, &sm.qg_full, 0, x.j, x.gamma, tq, x.b, pol);
+        for (int kb = 0; kb < nk; ++kb, ++gstep) {
+          const uint32_t st = gstep & 1;
+          wait(&sm.ring_empty[st], ((gstep >> 1) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&sm.ring_full[st], 2 * kTile);
+          const int32_t tk = x.t0 + kb * kB;
+          ptx::tma_load_5d(sm.k[st], &tm_k, &sm.ring_full[st], 0, x.j, x.gamma, tk, x.b, pol);
+          ptx::tma_load_5d(sm.v[st], &tm_v, &sm.ring_full[st], 0, x.j, x.gamma, tk, x.b, pol);
+        }
+      }
+    }
+  } else if (warp == 0) {
+    if (ptx::elect_one()) {
+      constexpr uint32_t id_ss = ptx::idesc_bf16(kB, kB, 0, 0);  // S = Q K^T, dP = dO V^T (K-major)
+      constexpr uint32_t id_ts = ptx::idesc_bf16(kB, kD, 0, 1);  // dQ += dS K (A TMEM, B = K MN-major)
+      const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q));
+      const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g));
+      uint32_t step = 0;
+      int it = 0;
+      for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+        wait(&sm.qg_full, it & 1);
+        ptx::tc_fence_after();
+        for (int kb = 0; kb < nk; ++kb, ++step) {
+          const uint32_t st = step & 1;
+          wait(&sm.ring_full[st], (step >> 1) & 1);
+          ptx::tc_fence_after();
+          const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k[st]));
+          const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v[st]));
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            ptx::mma_ss(tbase + cS, qd + 2 * kk, kd + 2 * kk, id_ss, kk > 0);
+            ptx::mma_ss(tbase + cDP, gd + 2 * kk, vd + 2 * kk, id_ss, kk > 0);
+          }
+          ptx::tc_commit(&sm.s_full);
+          wait(&sm.p_full, step & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kB / 16; ++kk)  // K-step of 16 keys: 8 packed dS columns, 16 rows of K
+            ptx::mma_ts(tbase + cDQ, tbase + cDP + kk * 8, kd + kk * 128, id_ts, (kb > 0 || kk > 0) ? 1u : 0u);
+          ptx::tc_commit(&sm.ring_empty[st]);
+        }
+        ptx::tc_commit(&sm.q_done);
+      }
+    }
+  } else if (warp >= 4) {
+    const int wg = (warp - 4) / 4;
+    const uint32_t row = ((warp - 4) % 4) * 32 + lane;  // query row (TMEM lane)
+    const uint32_t lane_base = (((warp - 4) % 4) * 32) << 16;
+    const bool leader = warp == 4 && lane == 0;
+    uint32_t step = 0;
+    int it = 0;
+    for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x, ++it) {
+      const LongView x = long_view(p, u);
+      const int32_t tq = x.t0 + x.blk * kB;
+      const int64_t n = (int64_t)(tq + row) * p.r + x.gamma;
+      const int64_t base = ((int64_t)x.b * p.h + x.j) * p.N;
+      const float l2 = lse[base + n] * kLog2e, dl = delta[base + n];
+      for (int kb = 0; kb < nk; ++kb, ++step) {
+        wait(&sm.s_full, step & 1);
+        ptx::tc_fence_after();
+#pragma unroll 1
+        for (int c = 2 * wg; c < 2 * wg + 2; ++c) {
+          uint32_t sv[32], dp[32];
+          ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, sv);
+          ptx::tmem_ld32(tbase + lane_base + cDP + 32 * c, dp);
+          ptx::tmem_ld_wait();
+          if (c == 1) ptx::named_bar_arrive(3, 2 * kB);
+          uint32_t dd[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float p0 = ptx::ex2(__uint_as_float(sv[2 * e]) * p.c - l2);
+            const float p1 = ptx::ex2(__uint_as_float(sv[2 * e + 1]) * p.c - l2);
+            dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl), p1 * (__uint_as_float(dp[2 * e + 1]) - dl));
+          }
+          if (c == 2) ptx::named_bar_sync(3, 2 * kB);
+          ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.p_full);
+      }
+      if (wg == 0) {  // dQ of this query block (scaled) + zero boxes of the other classes
+        wait(&sm.q_done, it & 1);
+        ptx::tc_fence_after();
+        uint32_t a[2][32];
+        if (leader) ptx::tma_store_wait_read<0>();
+        ptx::named_bar_sync(1, 128);
+        ptx::tmem_ld32(tbase + lane_base + cDQ, a[0]);
+        ptx::tmem_ld32(tbase + lane_base + cDQ + 32, a[1]);
+        ptx::tmem_ld_wait();
+        const uint32_t a0 = ptx::smem_u32(sm.stage);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float* f = reinterpret_cast<const float*>(&a[c >> 2][(c & 3) * 8]);
+          ptx::st_shared_v4(a0 + row * 128 + ((c ^ (row & 7)) * 16), ptx::pack_bf16x2(f[0] * p.scale, f[1] * p.scale),
+                            ptx::pack_bf16x2(f[2] * p.scale, f[3] * p.scale),
+                            ptx::pack_bf16x2(f[4] * p.scale, f[5] * p.scale),
+                            ptx::pack_bf16x2(f[6] * p.scale, f[7] * p.scale));
+        }
+        ptx::tc_fence_before();
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, 128);
+        if (leader) {
+          ptx::tma_store_5d(&tm_dq, sm.stage, 0, x.j, x.gamma, tq, x.b);
+          for (int32_t gz = 0; gz < p.r; ++gz)
+            if (gz != x.gamma) ptx::tma_store_5d(&tm_dq, sm.zero, 0, x.j, gz, tq, x.b);
+          ptx::tma_store_commit();
+        }
+      }
+    }
+    if (leader) ptx::tma_store_wait_all<0>();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tbase);
+  }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -352,7 +766,10 @@ bool bwd_sm100_supported(const Geometry& g, int dtype, const void* const* ptrs, 
   if (dtype != 1 || g.d != kD || g.dv != kD) return false;
   if (g.N % g.w != 0 || g.w % g.r != 0) return false;
   const int64_t m = g.w / g.r;
-  if (m != 128 && m != 256) return false;
+  // 128, 256: fused kernel; >= 512: the dkdv_long + dq_long pair; 16..64
+  // (dividing 128): fused kernel on 128-row tiles of packed segments
+  const bool packed = m < 128 && 128 % m == 0 && m >= 16 && (g.N / g.r) % 128 == 0;
+  if (m % 128 != 0 && !packed) return false;
   if (g.h > kMaxHeads || g.N > (int64_t)INT32_MAX / 2 || g.B * g.h * (g.N / g.w) > (int64_t)INT32_MAX) return false;
   for (int i = 0; i < n_ptrs; ++i)
     if (reinterpret_cast<uintptr_t>(ptrs[i]) & 15u) return false;
@@ -373,14 +790,54 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
   p.N = (int32_t)g.N;
   p.T = (int32_t)(g.N / g.r);
   p.m = (int32_t)(g.w / g.r);
+  p.mseg = p.m;
+  if (p.m < kB) p.m = kB;  // packed: a "view" is 128 t'-rows holding 128 / mseg segments
   p.r = (int32_t)g.r;
   p.h = (int32_t)g.h;
-  p.n_seg = (int32_t)(g.N / g.w);
+  p.n_seg = (int32_t)((g.N / g.r) / p.m);  // units of p.m t'-rows per (b, j) stream
   p.nblk = p.m / kB;
   p.n_units = (int32_t)(g.B * g.h * p.n_seg);
   p.scale = g.scale;
   p.c = g.scale * kLog2e;
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  if (p.nblk > kMaxBlk) {
+    LongParams lp;
+    lp.N = p.N;
+    lp.m = p.m;
+    lp.r = p.r;
+    lp.h = p.h;
+    lp.n_seg = p.n_seg;
+    lp.nblk = p.nblk;
+    lp.n_units = (int32_t)(g.B * g.h * p.n_seg * p.nblk);
+    lp.c = p.c;
+    lp.scale = p.scale;
+    for (int i = 0; i < kMaxHeads; ++i) lp.offsets[i] = p.offsets[i];
+    const size_t s1 = sizeof(DkdvSmem) + 1024, s2 = sizeof(DqSmem) + 1024;
+    static std::once_flag once_l;
+    static cudaError_t attr_l = cudaSuccess;
+    std::call_once(once_l, [&] {
+      attr_l = cudaFuncSetAttribute(dfa_bwd_dkdv_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+      if (attr_l == cudaSuccess)
+        attr_l = cudaFuncSetAttribute(dfa_bwd_dq_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+    });
+    if (attr_l != cudaSuccess) {
+      *err = attr_l;
+      *why = "cudaFuncSetAttribute failed";
+      return 0;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(lp.n_units, sms);
+    dfa_bwd_dkdv_long_kernel<<<grid, kThreads, s1, stream>>>(mq, mk, mv, mg, mdk, mdv, lse, delta, lp);
+    dfa_bwd_dq_long_kernel<<<grid, kThreads, s2, stream>>>(mq, mk, mv, mg, mdq, lse, delta, lp);
+    *err = cudaGetLastError();
+    return 2;
+  }
   const size_t smem = sizeof(BwdSmem) + 1024;
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
@@ -391,13 +848,6 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
     *err = attr;
     *why = "cudaFuncSetAttribute failed";
     return 0;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
   }
   const unsigned grid = (unsigned)std::min<int64_t>(p.n_units, sms);  // persistent: one CTA per SM
   dfa_bwd_sm100_kernel<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mg, mdq, mdk, mdv, lse, delta, p);

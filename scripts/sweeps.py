@@ -136,16 +136,41 @@ def config4(ncu=False):
     return {"config": "config4 (w,r) sweep B=64 h=6 bf16", "rows": rows, "lse_combined_set": combo}
 
 
+def config4_backward():
+    """dfa_backward over the config-4 (w, r) grid (B = 64, h = 6, bf16): the
+    tcgen05 kernels for m = w/r multiple of 128, SIMT otherwise.  FLOP = 2.5 x
+    the forward's (S, dP, dV, dK, dQ; the long-m pair recomputes S / dP, so its
+    executed FLOPs are 3.5 x)."""
+    N, h, d, B = 4096, 6, 64, 64
+    q, k, v, do = (torch.randn((B, N, h, d), device="cuda", dtype=torch.bfloat16) for _ in range(4))
+    L = torch.empty((B, h, N), device="cuda", dtype=torch.float32)
+    ws = torch.empty(B * h * N * 4 + 256, dtype=torch.uint8, device="cuda")
+    g = [torch.empty_like(q) for _ in range(3)]
+    rows = []
+    for w in (256, 512, 1024, 2048, 4096):
+        for r in (1, 2, 4, 8):
+            cfg = cfg_for(N, w, r, h)
+            o = dfa.dfa_forward(q, k, v, cfg, lse=L)
+            m = w // r
+            iters = 3 if m % 128 else 10
+            ms = time_ms(lambda: dfa.dfa_backward(q, k, v, o, L, do, cfg, *g, workspace=ws), iters=iters, warmup=1)
+            fl = 2.5 * 2 * dfa.flop_count(cfg).dilated_mults * B
+            rows.append({"w": w, "r": r, "m": m, "ms": ms, "tflops": fl / (ms / 1e3) / 1e12,
+                         "path": "tcgen05 fused" if m in (128, 256) else ("tcgen05 dkdv+dq" if m % 128 == 0 else (
+                             "tcgen05 fused (packed segments)" if 128 % m == 0 and m >= 16 else "simt"))})
+    return {"config": "config4 backward (w,r) sweep B=64 h=6 bf16", "rows": rows}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweeps.json"))
     ap.add_argument("--ncu", action="store_true")
-    ap.add_argument("--only", choices=["config1", "config3", "config4"], default=None)
+    ap.add_argument("--only", choices=["config1", "config3", "config4", "config4bwd"], default=None)
     a = ap.parse_args()
     if a.ncu:
         config4(ncu=True)
         return
-    fns = {"config1": config1, "config4": config4, "config3": config3}
+    fns = {"config1": config1, "config4": config4, "config3": config3, "config4bwd": config4_backward}
     res = {"gpu": torch.cuda.get_device_name(0)}
     for name, fn in fns.items():
         if a.only in (None, name):
@@ -159,6 +184,8 @@ def main():
               f"{r['frac_of_attainable']:.2f} of attainable ({r['bound']})")
     if "config4" in res:
         print("combined", res["config4"]["lse_combined_set"])
+    for r in res.get("config4bwd", {}).get("rows", []):
+        print(f"bwd w={r['w']:5d} r={r['r']} m={r['m']:4d} {r['ms']:.3f} ms {r['tflops']:7.1f} TF  {r['path']}")
     for r in res.get("config3", {}).get("rows", []):
         print(f"B={r['B']:4d} {r['ms_6_layers']:.3f} ms/6 layers {r['images_per_s']:9.0f} images/s {r['tflops']:.0f} TF")
 
