@@ -189,6 +189,15 @@ dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, 
                                     const void* wq, const void* wk, const void* wv, const void* wo, void* out,
                                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same on HOST buffers, synchronous (device staging in `ws`, sized by
+ * dfa_multi_head_host_workspace_bytes): the call include/dfa.hpp's
+ * reference-shaped dfa::multi_head_dilated makes. */
+dfa_status_t dfa_multi_head_host_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
+                                                 size_t* bytes);
+dfa_status_t dfa_multi_head_dilated_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,
+                                         const void* wq, const void* wk, const void* wv, const void* wo, void* out,
+                                         dfa_workspace_t* ws);
+
 /* One pre-norm encoder block (encoder.hpp:241-248; parameters as
  * init_encoder_params names them, :287-304): x1 = x + attention_mix(LN1(x))
  * (attention_mix = multi_head_dilated + bias bo, encoder.hpp:189-223);

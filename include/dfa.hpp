@@ -8,6 +8,8 @@
 //   attnkit::make_segment_view        -> dfa::make_segment_view    (:84-98)
 //   attnkit::dilated_attention(q,k,v,cfg,gamma,workers)
 //                                     -> dfa::dilated_attention    (:280-301)
+//   attnkit::multi_head_dilated(x,w,cfg,workers)
+//                                     -> dfa::multi_head_dilated   (:340-360)
 //   attnkit::flop_count / flop_csv_*  -> dfa::flop_count / ...     (:364-394)
 //   attnkit::fault::recompose_perturb -> dfa::fault::ScopedPerturb (:237-241)
 //
@@ -257,6 +259,58 @@ Tensor dilated_attention(const Tensor& q, const Tensor& k, const Tensor& v, cons
   Tensor out({q.rows(), v.cols()});
   check(dfa_forward_host(&c, DFA_F32, 1, q.data(), k.data(), v.data(), out.data(), nullptr,
                          thread_workspace().get(bytes), nullptr));
+  return out;
+}
+
+// attention.hpp:340-360 multi_head_dilated(x, weights, cfg, workers) on host
+// tensors: `Weights` has the reference's MultiHeadWeights members -- wq, wk,
+// wv (h tensors of D x d) and wo (D x D) -- so attnkit::MultiHeadWeights<float>
+// qualifies.  Same checks and error types: validate(true) (full coverage),
+// weight shapes (MultiHeadWeights::validate), x = [N x D].  fp32 device path.
+template <class Tensor, class Weights>
+Tensor multi_head_dilated(const Tensor& x, const Weights& weights, const AttentionConfig& cfg, int workers = 1) {
+  using Scalar = std::remove_cv_t<std::remove_pointer_t<decltype(x.data())>>;
+  static_assert(std::is_same_v<Scalar, float>, "dfa::multi_head_dilated runs the fp32 device path");
+  (void)workers;
+  cfg.validate(/*require_full_coverage=*/true);
+  const auto heads = static_cast<std::size_t>(cfg.num_heads);
+  if (weights.wq.size() != heads || weights.wk.size() != heads || weights.wv.size() != heads) {
+    std::ostringstream os;
+    os << "multi_head_dilated: expected " << cfg.num_heads << " per-head projections";
+    throw config_error(os.str());
+  }
+  const Index D = cfg.head_dim * cfg.num_heads, d = cfg.head_dim;
+  for (std::size_t j = 0; j < heads; ++j)
+    for (const auto* t : {&weights.wq[j], &weights.wk[j], &weights.wv[j]})
+      if (t->rows() != D || t->cols() != d) {
+        std::ostringstream os;
+        os << "multi_head_dilated: head " << j << " projection is [" << t->rows() << "x" << t->cols()
+           << "], expected [" << D << "x" << d << "]";
+        throw dimension_error(os.str());
+      }
+  if (weights.wo.rows() != D || weights.wo.cols() != D) throw dimension_error("multi_head_dilated: bad output projection");
+  detail::require_rank2(x, "multi_head_dilated");
+  if (x.rows() != cfg.seq_len || x.cols() != D) {
+    std::ostringstream os;
+    os << "multi_head_dilated: input [" << x.rows() << "x" << x.cols() << "], expected [" << cfg.seq_len << "x" << D
+       << "]";
+    throw dimension_error(os.str());
+  }
+  // stack the per-head projections as [h, D, d] (the C-ABI layout)
+  std::vector<float> wq(heads * D * d), wk(heads * D * d), wv(heads * D * d);
+  for (std::size_t j = 0; j < heads; ++j)
+    for (Index e = 0; e < D * d; ++e) {
+      wq[j * D * d + e] = weights.wq[j].data()[e];
+      wk[j * D * d + e] = weights.wk[j].data()[e];
+      wv[j * D * d + e] = weights.wv[j].data()[e];
+    }
+  std::vector<int64_t> offs;
+  dfa_config_t c = cfg.to_c(offs, 0);
+  std::size_t bytes = 0;
+  check(dfa_multi_head_host_workspace_bytes(&c, DFA_F32, 1, &bytes));
+  Tensor out({cfg.seq_len, D});
+  check(dfa_multi_head_dilated_host(&c, DFA_F32, 1, x.data(), wq.data(), wk.data(), wv.data(), weights.wo.data(),
+                                    out.data(), thread_workspace().get(bytes)));
   return out;
 }
 

@@ -56,6 +56,8 @@ EXPORTED = (
     "dfa_backward",
     "dfa_multi_head_workspace_bytes",
     "dfa_multi_head_dilated",
+    "dfa_multi_head_host_workspace_bytes",
+    "dfa_multi_head_dilated_host",
     "dfa_encoder_block_workspace_bytes",
     "dfa_encoder_block_forward",
     "dfa_tensor_header",
@@ -137,6 +139,8 @@ def _load() -> ctypes.CDLL:
         "dfa_backward": (c_i32, [p_cfg, c_i32, c_i64] + [c_vp] * 10 + [ctypes.c_size_t, c_vp]),
         "dfa_multi_head_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_multi_head_dilated": (c_i32, [p_cfg, c_i32, c_i64] + [c_vp] * 7 + [ctypes.c_size_t, c_vp]),
+        "dfa_multi_head_host_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
+        "dfa_multi_head_dilated_host": (c_i32, [p_cfg, c_i32, c_i64] + [c_vp] * 7),
         "dfa_encoder_block_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_encoder_block_forward": (c_i32, [p_cfg, c_i32, c_i64, c_vp, ctypes.POINTER(DfaBlockWeights), c_vp, c_vp,
                                               ctypes.c_size_t, c_vp]),

@@ -569,6 +569,48 @@ dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, 
   return DFA_OK;
 }
 
+// attention.hpp:340-360 on HOST buffers (synchronous; the reference-shaped
+// C++ adapter dfa::multi_head_dilated calls this).
+dfa_status_t dfa_multi_head_host_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
+                                                 size_t* bytes) {
+  size_t dev = 0;
+  dfa_status_t st = dfa_multi_head_workspace_bytes(cfg, dtype, batch, &dev);
+  if (st != DFA_OK) return st;
+  const size_t es = elem_size(dtype), D = (size_t)(cfg->num_heads * cfg->head_dim);
+  *bytes = dev + 2 * up256((size_t)(batch * cfg->seq_len) * D * es) + 4 * up256(D * D * es);
+  return DFA_OK;
+}
+
+dfa_status_t dfa_multi_head_dilated_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,
+                                         const void* wq, const void* wk, const void* wv, const void* wo, void* out,
+                                         dfa_workspace_t* ws) {
+  size_t need = 0, dev_need = 0;
+  dfa_status_t st = dfa_multi_head_host_workspace_bytes(cfg, dtype, batch, &need);
+  if (st != DFA_OK) return st;
+  dfa_multi_head_workspace_bytes(cfg, dtype, batch, &dev_need);
+  if (!ws || ws->bytes < need)
+    return fail(DFA_ERR_DIMENSION, "multi_head_dilated: workspace has %zu bytes, needs %zu", ws ? ws->bytes : 0,
+                need);
+  if (batch == 0) return DFA_OK;
+  if (!x || !wq || !wk || !wv || !wo || !out) return fail(DFA_ERR_DIMENSION, "multi_head_dilated: null pointer");
+  const size_t es = elem_size(dtype), D = (size_t)(cfg->num_heads * cfg->head_dim);
+  const size_t act = (size_t)(batch * cfg->seq_len) * D * es, wb = D * D * es;
+  char* base = static_cast<char*>(ws->dev);
+  char* dx = base + dev_need;
+  char* dout = dx + up256(act);
+  char* dw[4];
+  for (int i = 0; i < 4; ++i) dw[i] = dout + up256(act) + i * up256(wb);
+  const void* hw[4] = {wq, wk, wv, wo};
+  cudaError_t err = cudaMemcpy(dx, x, act, cudaMemcpyHostToDevice);
+  for (int i = 0; i < 4 && err == cudaSuccess; ++i) err = cudaMemcpy(dw[i], hw[i], wb, cudaMemcpyHostToDevice);
+  if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "multi_head_dilated: H2D: %s", cudaGetErrorString(err));
+  st = dfa_multi_head_dilated(cfg, dtype, batch, dx, dw[0], dw[1], dw[2], dw[3], dout, base, dev_need, nullptr);
+  if (st != DFA_OK) return st;
+  if ((err = cudaMemcpy(out, dout, act, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return fail(DFA_ERR_CUDA, "multi_head_dilated: D2H: %s", cudaGetErrorString(err));
+  return DFA_OK;
+}
+
 dfa_status_t dfa_encoder_block_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
                                                int64_t hidden, size_t* bytes) {
   dfa_impl::Geometry g;

@@ -120,6 +120,38 @@ static void gpu_checks(const std::string& dir) {
     Tensor p = dfa::dilated_attention(q, k, v, cfg, 1);
     CHECK(p.buf[0] != out.buf[0]);
   }
+
+  // multi_head_dilated (attention.hpp:340-360) with MultiHeadWeights' shape:
+  // N = 256, D = 128, h = 2 (d = 64), (w, r) = (64, 2); dumped for the test
+  struct Weights {
+    std::vector<Tensor> wq, wk, wv;
+    Tensor wo{{128, 128}};
+  } w;
+  const auto mcfg = basic_cfg(256, 64, 2, 2, 64);
+  for (int j = 0; j < 2; ++j) {
+    w.wq.push_back(randn(128, 64));
+    w.wk.push_back(randn(128, 64));
+    w.wv.push_back(randn(128, 64));
+  }
+  w.wo = randn(128, 128);
+  for (auto* t : {&w.wo}) for (auto& x : t->buf) x /= std::sqrt(128.0f);
+  for (auto& vec : {&w.wq, &w.wk, &w.wv})
+    for (auto& t : *vec) for (auto& x : t.buf) x /= std::sqrt(128.0f);
+  auto x = randn(256, 128);
+  Tensor y = dfa::multi_head_dilated(x, w, mcfg);
+  dump(dir + "/mh_x.f32", x);
+  for (int j = 0; j < 2; ++j) {
+    dump(dir + "/mh_wq" + std::to_string(j) + ".f32", w.wq[j]);
+    dump(dir + "/mh_wk" + std::to_string(j) + ".f32", w.wk[j]);
+    dump(dir + "/mh_wv" + std::to_string(j) + ".f32", w.wv[j]);
+  }
+  dump(dir + "/mh_wo.f32", w.wo);
+  dump(dir + "/mh_y.f32", y);
+  // full coverage is required, as in the reference (attention.hpp:343)
+  auto partial = basic_cfg(256, 64, 4, 2, 64);
+  CHECK_THROWS_AS(dfa::multi_head_dilated(x, w, partial), dfa::config_error);
+  Tensor badx({255, 128});
+  CHECK_THROWS_AS(dfa::multi_head_dilated(badx, w, mcfg), dfa::dimension_error);
 }
 
 int main(int argc, char** argv) {

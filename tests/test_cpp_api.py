@@ -33,3 +33,16 @@ def test_cpp_dilated_attention_on_gpu(binary, port, tmp_path):
     q, k, v, o = (np.fromfile(tmp_path / f"{n}.f32", dtype=np.float32).reshape(4096, 64) for n in "qkvo")
     want = port.dilated_attention(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64), 512, 2, 1)
     assert np.abs(o - want).max() <= 1e-4
+
+
+@pytest.mark.gpu
+def test_cpp_multi_head_dilated_vs_reference(binary, ref, tmp_path):
+    """dfa::multi_head_dilated (C++ adapter over dfa_multi_head_dilated_host)
+    vs the compiled reference's multi_head_dilated on the same fp32 inputs."""
+    r = subprocess.run([binary, "gpu", str(tmp_path)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    ld = lambda n, shape: np.fromfile(tmp_path / f"{n}.f32", dtype=np.float32).reshape(shape)  # noqa: E731
+    x, wo, y = ld("mh_x", (256, 128)), ld("mh_wo", (128, 128)), ld("mh_y", (256, 128))
+    wq, wk, wv = (np.stack([ld(f"mh_{n}{j}", (128, 64)) for j in range(2)]) for n in ("wq", "wk", "wv"))
+    want = ref.multi_head_dilated(x, wq, wk, wv, wo, 64, 2)
+    assert np.abs(y - want).max() <= 1e-4 * max(1.0, np.abs(want).max())
