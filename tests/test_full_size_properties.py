@@ -1,0 +1,75 @@
+"""Size-independent properties at BASELINE.json's full sizes (the oracle is
+too slow there): every config-4 (w, r) at B = 64, h = 6, N = 4096, and the
+config-5 batch decomposition.
+
+  * constant values: with every V row equal to c, softmax weights summing to
+    1 make each kept row c (bf16 tolerance) and every unselected row exactly 0;
+  * batch equivariance: permuting images permutes outputs bit for bit (no
+    cross-image interference, persistent-unit bookkeeping independent of
+    position);
+  * batch decomposition (config 5): one launch over 1024 images equals four
+    launches over 256-image chunks, bit for bit.
+"""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GRID = [(w, r) for w in (256, 512, 1024, 2048, 4096) for r in (1, 2, 4, 8)]
+
+
+def _cfg(dfa, w, r, h=6):
+    return dfa.AttentionConfig(4096, w, r, h, 64, dfa.AttentionConfig.spread_offsets(h, r))
+
+
+@pytest.fixture(scope="module")
+def qk():
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    return [torch.randn((64, 4096, 6, 64), device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(2)]
+
+
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("w,r", GRID)
+def test_constant_values_full_size(dfa, cuda, qk, w, r):
+    import torch
+
+    q, k = qk
+    c = torch.linspace(-2, 2, 64, device="cuda").to(torch.bfloat16)
+    v = c.view(1, 1, 1, 64).expand(64, 4096, 6, 64).contiguous()
+    o = dfa.dfa_forward(q, k, v, _cfg(dfa, w, r)).float()
+    torch.cuda.synchronize()
+    sel = torch.zeros((4096, 6), dtype=torch.bool, device="cuda")
+    for j in range(6):
+        sel[j % r::r, j] = True
+    kept = o[:, sel]        # [64, rows, 64]
+    assert (kept - c.float()).abs().max().item() <= 2e-2
+    assert (o[:, ~sel] == 0).all()
+
+
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("w,r", [(512, 2), (256, 8), (4096, 1), (1024, 4)])
+def test_batch_permutation_equivariance(dfa, cuda, qk, w, r):
+    import torch
+
+    q, k = qk
+    v = torch.randn_like(q)
+    cfg = _cfg(dfa, w, r)
+    perm = torch.randperm(64, device="cuda")
+    a = dfa.dfa_forward(q, k, v, cfg)
+    b = dfa.dfa_forward(q[perm].contiguous(), k[perm].contiguous(), v[perm].contiguous(), cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(a[perm], b)
+
+
+@pytest.mark.timeout(300)
+def test_config5_batch_decomposition(dfa, cuda):
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.randn((1024, 4096, 6, 64), device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
+    cfg = _cfg(dfa, 512, 2)
+    whole = dfa.dfa_forward(q, k, v, cfg)
+    parts = torch.cat([dfa.dfa_forward(q[i:i + 256], k[i:i + 256], v[i:i + 256], cfg) for i in range(0, 1024, 256)])
+    torch.cuda.synchronize()
+    assert torch.equal(whole, parts)
