@@ -47,6 +47,9 @@ constexpr int kTile = 128 * 128;       // 128 rows x 128 B (64 bf16), SW128
 constexpr int kMaxBlk = 2;             // m <= 256
 constexpr int kThreads = 384;          // warp 0: TMA + MMA, warp 1: TMEM alloc, warps 4-11: gradient WGs
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef DFA_BWD_LONG_FROM
+#define DFA_BWD_LONG_FROM 3  // view blocks (m / 128) from which the dkdv + dq pair replaces the fused kernel
+#endif
 
 struct __align__(1024) BwdSmem {
   uint8_t q[kMaxBlk][kTile];
@@ -807,7 +810,7 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  if (p.nblk > kMaxBlk) {
+  if (p.nblk > kMaxBlk || p.nblk >= DFA_BWD_LONG_FROM) {
     LongParams lp;
     lp.N = p.N;
     lp.m = p.m;
