@@ -210,6 +210,10 @@ class Reference:
             fn.argtypes = [tp, tp, tp, tp, tp, _i64, _i64, _i64, _i64, _i64, _i64p, tp]
         L.ref_dilated_backward_f64.restype = _i32
         L.ref_dilated_backward_f64.argtypes = [_d, _d, _d, _d, _i64, _i64, _i64, _i64, _i64, _i64, _d, _d, _d]
+        L.ref_bench_csv_header.restype = _i32
+        L.ref_bench_csv_header.argtypes = [ctypes.c_char_p, _i64]
+        L.ref_spearman.restype = _i32
+        L.ref_spearman.argtypes = [_d, _d, _i64, _d]
         L.ref_encoder_block_f64.restype = _i32
         L.ref_encoder_block_f64.argtypes = [_d, _i64, _i64, _i64, _i64, _i64, _i64] + [_d] * 14
 
@@ -330,6 +334,21 @@ class Reference:
         if st:
             raise OracleError(st, self.last_error())
         return gq, gk, gv
+
+    def bench_csv_header(self) -> str:
+        buf = ctypes.create_string_buffer(512)
+        st = self.lib.ref_bench_csv_header(buf, 512)
+        if st:
+            raise OracleError(st, self.last_error())
+        return buf.value.decode()
+
+    def spearman(self, a, b) -> float:
+        a, b = (np.ascontiguousarray(x, dtype=np.float64) for x in (a, b))
+        out = ctypes.c_double(0)
+        st = self.lib.ref_spearman(_ptr(a, _d), _ptr(b, _d), len(a), ctypes.byref(out))
+        if st:
+            raise OracleError(st, self.last_error())
+        return out.value
 
     def encoder_block(self, x, p, h, w, r):
         """One pre-norm block (encoder.hpp:241-248).  p: dict with ln1_g, ln1_b,

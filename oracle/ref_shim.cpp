@@ -11,6 +11,7 @@
 // legs may load it; the product path (paper_2403_09195_b200) never does.
 
 #include <atomic>
+#include <cstdio>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -20,6 +21,7 @@
 
 #include "attnkit/attention.hpp"
 #include "attnkit/autodiff.hpp"
+#include "attnkit/bench.hpp"
 #include "attnkit/encoder.hpp"
 #include "attnkit/oracles.hpp"
 #include "attnkit/tensor.hpp"
@@ -383,6 +385,19 @@ int ref_encoder_block_f64(const double* x, int64_t n, int64_t dm, int64_t h, int
     auto mixed = ag::add_rowvec(ag::matmul(hid, p.at(b + "mlp.w2")), p.at(b + "mlp.b2"));
     auto y = ag::add(x1, mixed);
     std::memcpy(out, y.value().data(), sizeof(double) * static_cast<size_t>(n * dm));
+  });
+}
+
+// bench.hpp:173-176 bench_csv_header and :235-276 spearman_rank_correlation.
+int ref_bench_csv_header(char* buf, int64_t cap) {
+  return guarded([&] {
+    const std::string h = bench_csv_header();
+    std::snprintf(buf, static_cast<size_t>(cap), "%s", h.c_str());
+  });
+}
+int ref_spearman(const double* a, const double* b, int64_t n, double* out) {
+  return guarded([&] {
+    *out = spearman_rank_correlation(std::vector<double>(a, a + n), std::vector<double>(b, b + n));
   });
 }
 
