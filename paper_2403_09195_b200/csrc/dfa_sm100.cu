@@ -96,6 +96,12 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define DFA_POLY_MASK 0x8888u
 #endif
 constexpr float kRescaleThreshold = DFA_RESCALE_THR;  // log2 units: p <= 2^8 between rescales
+#ifndef DFA_SUMCHECK
+#define DFA_SUMCHECK 0
+#endif
+// Sum-checked fast path (DFA_SUMCHECK): a tile whose row sum against the
+// running reference stays <= 2^thr needs no row max.
+constexpr float kSumBound = 256.0f;
 // bit e: pair e of each 16-pair (32-column) chunk uses the FMA-pipe exp2
 // polynomial instead of MUFU.EX2 (balances the MUFU and FMA/issue pipes;
 // measured: 4 of 16 beats 0, 2, 5, 6, 7 and 8 of 16)
@@ -551,76 +557,96 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (col < lo || col >= hi) sr[c][e] = __float_as_uint(-INFINITY);
           }
       }
-      float mx[8];
+      // Exponentiate the tile against `neg` = -reference * c: packed
+      // scale-subtract (FFMA2), exp2 (pairs in kPolyMask as an FMA-pipe
+      // polynomial, the rest on MUFU), packed sums (FADD2), bf16 packing and
+      // tcgen05.st of P over the consumed S columns.  Returns the row sum.
+      auto exp_pass = [&](float neg, bool clamp_hi) -> float {
+        float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+        const float2 c2 = make_float2(p.c, p.c), n2 = make_float2(neg, neg);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+        for (int c = 0; c < 4; ++c) {
+          float2 xv[16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+          for (int e = 0; e < 16; ++e)
+            xv[e] = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * e]), __uint_as_float(sr[c][2 * e + 1])), c2, n2);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(sr[c][e]));
-      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-      DFA_TRACE(2 + s, TR_MAX_DONE);
-      // Lazy rescale (warp-uniform: tcgen05.ld/st are warp collectives).  O_s
-      // must hold every earlier P V of this slot: wait for the slot's previous
-      // P V (pv_done phases are consumed exactly once per step, in order).
-      const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
-      const bool fix_o = move && mref != -INFINITY;
+          for (int e = 0; e < 16; ++e) {
+            if (DFA_PROBE_NO_EXP) {
+              // profiling probe only (wrong results): no exponentials
+            } else if ((kPolyMask >> e) & 1u) {
+              // the polynomial's exponent add wraps for x >= 128: clamp so an
+              // overflowing tile shows up in the row sum (MUFU gives +inf)
+              if (clamp_hi) xv[e] = make_float2(fminf(xv[e].x, 126.0f), fminf(xv[e].y, 126.0f));
+              xv[e] = ptx::ex2_poly2(xv[e]);
+            } else {
+              xv[e].x = ptx::ex2(xv[e].x);
+              xv[e].y = ptx::ex2(xv[e].y);
+            }
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            ls2[e & 1] = ptx::fadd2(ls2[e & 1], xv[e]);
+            pk[e] = ptx::pack_bf16x2(xv[e].x, xv[e].y);
+          }
+          ptx::tmem_st16(tS + 16 * c, pk);
+        }
+        const float2 lsum = ptx::fadd2(ls2[0], ls2[1]);
+        return lsum.x + lsum.y;
+      };
+      bool exact = true;
       bool waited = false;
-      if (__any_sync(0xffffffffu, fix_o)) {
-        if (steps > 0) {
-          DFA_WAIT(&sm.pv_done[s], pvc & 1, 11);
-          ++pvc;
-          waited = true;
-        }
-        ptx::tc_fence_after();
-        const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
-        l *= corr;
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          uint32_t orow[32];
-          ptx::tmem_ld32(tO + 32 * c, orow);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * corr);
-          ptx::tmem_st32(tO + 32 * c, orow);
-        }
+#if DFA_SUMCHECK
+      // Fast path (every row of the warp already has a reference from an
+      // earlier tile of this unit): no row max.  The tile's row sum bounds
+      // each p, so sum <= 2^thr keeps every p within the lazy-rescale bound;
+      // otherwise (or on inf / NaN) the tile is redone on the exact path and
+      // P is simply re-stored over the same columns.
+      if (__all_sync(0xffffffffu, mref != -INFINITY)) {
+        const float fs = exp_pass(-mref * p.c, true);
+        exact = __any_sync(0xffffffffu, !(fs <= kSumBound));
+        if (!exact) l += fs;
       }
-      if (move) mref = tmax;
-      const float neg = (mref == -INFINITY) ? 0.0f : -mref * p.c;
-      float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
-      const float2 c2 = make_float2(p.c, p.c), n2 = make_float2(neg, neg);
+#endif
+      if (exact) {
+        float mx[8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        // per 32-column chunk: packed scale-subtract (FFMA2), exponentiate
-        // (pairs in kPolyMask as an FMA-pipe polynomial, the rest on MUFU), packed
-        // sums (FADD2) and bf16 packing
-        float2 xv[16];
+        for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          xv[e] = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * e]), __uint_as_float(sr[c][2 * e + 1])), c2, n2);
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          if (DFA_PROBE_NO_EXP) {
-            // profiling probe only (wrong results): no exponentials
-          } else if ((kPolyMask >> e) & 1u) {
-            xv[e] = ptx::ex2_poly2(xv[e]);
-          } else {
-            xv[e].x = ptx::ex2(xv[e].x);
-            xv[e].y = ptx::ex2(xv[e].y);
+          for (int e = 0; e < 32; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(sr[c][e]));
+        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        DFA_TRACE(2 + s, TR_MAX_DONE);
+        // Lazy rescale (warp-uniform: tcgen05.ld/st are warp collectives).  O_s
+        // must hold every earlier P V of this slot: wait for the slot's previous
+        // P V (pv_done phases are consumed exactly once per step, in order).
+        const bool move = tmax > mref && (mref == -INFINITY || (tmax - mref) * p.c > kRescaleThreshold);
+        const bool fix_o = move && mref != -INFINITY;
+        if (__any_sync(0xffffffffu, fix_o)) {
+          if (steps > 0) {
+            DFA_WAIT(&sm.pv_done[s], pvc & 1, 11);
+            ++pvc;
+            waited = true;
+          }
+          ptx::tc_fence_after();
+          const float corr = fix_o ? ptx::ex2((mref - tmax) * p.c) : 1.0f;
+          l *= corr;
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            uint32_t orow[32];
+            ptx::tmem_ld32(tO + 32 * c, orow);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) orow[e] = __float_as_uint(__uint_as_float(orow[e]) * corr);
+            ptx::tmem_st32(tO + 32 * c, orow);
           }
         }
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          ls2[e & 1] = ptx::fadd2(ls2[e & 1], xv[e]);
-          pk[e] = ptx::pack_bf16x2(xv[e].x, xv[e].y);
-        }
-        ptx::tmem_st16(tS + 16 * c, pk);
+        if (move) mref = tmax;
+        l += exp_pass((mref == -INFINITY) ? 0.0f : -mref * p.c, false);
       }
-      const float2 lsum = ptx::fadd2(ls2[0], ls2[1]);
-      float ls[4] = {lsum.x, lsum.y, 0.0f, 0.0f};
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       DFA_TRACE(2 + s, TR_EXP_DONE);
       // keep the pv_done phases in lockstep with the steps
       if (!waited && steps > 0) {
