@@ -50,3 +50,44 @@ def gather_to_rank0(shard, total_shape0: int, group=None) -> Optional["object"]:
     for req in dist.batch_isend_irecv([dist.P2POp(dist.isend, shard.contiguous(), 0, group)]):
         req.wait()
     return None
+
+
+# ------------------------------------------------- batch-1 latency (§8e)
+def segment_shard(n: int, w: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous token rows [start, stop) owned by `rank` when a single image
+    is split across ranks: whole segments only (segments are independent --
+    attention.hpp:280-301 never mixes rows of different segments), so each
+    rank runs the unchanged kernel on an (stop - start)-token problem.  The
+    last rank may own the tail segment (w does not divide N)."""
+    n_seg = (n + w - 1) // w
+    a, b = shard_range(n_seg, rank, world)
+    return min(a * w, n), min(b * w, n)
+
+
+def segment_parallel_forward(q, k, v, cfg, group=None, stream=None):
+    """Batch-1 latency path: every rank computes the dilated
+    attention of its contiguous block of segments and one all-gather
+    assembles the [B, N, h, d_v] output on every rank.  The partition keeps
+    the segment grid (the local problem has N' = stop - start rows, the same
+    w, r and offsets), so the result is bit-identical to the one-GPU call."""
+    import dataclasses
+
+    import torch
+    import torch.distributed as dist
+
+    from . import dfa_forward
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = cfg.seq_len
+    a, b = segment_shard(n, cfg.segment_len, rank, world)
+    local = dataclasses.replace(cfg, seq_len=b - a)
+    parts_rows = [segment_shard(n, cfg.segment_len, r, world) for r in range(world)]
+    width = max(hi - lo for lo, hi in parts_rows)
+    mine = torch.zeros((q.shape[0], width) + tuple(v.shape[2:]), dtype=v.dtype, device=v.device)
+    if b > a:  # padded to the widest shard so the all-gather sees equal sizes
+        mine[:, : b - a] = dfa_forward(q[:, a:b].contiguous(), k[:, a:b].contiguous(), v[:, a:b].contiguous(),
+                                       local, stream=stream)
+    gathered = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(gathered, mine, group=group)
+    return torch.cat([g[:, : hi - lo] for g, (lo, hi) in zip(gathered, parts_rows)], dim=1)

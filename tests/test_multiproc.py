@@ -61,3 +61,56 @@ def test_gather_world2_gloo(total):
     t = torch.tensor(got)
     assert t.shape == (total, 3, 2)
     assert torch.equal(t[:, 0, 0], torch.arange(total, dtype=torch.float32))
+
+
+def test_segment_shards_cover_whole_segments():
+    from paper_2403_09195_b200.dist import segment_shard
+
+    for n, w in ((4096, 512), (4096, 4096), (1000, 300), (130, 64)):
+        for world in (1, 2, 3, 4, 8):
+            rows = []
+            for r in range(world):
+                a, b = segment_shard(n, w, r, world)
+                assert a == b or (a % w == 0 and (b % w == 0 or b == n))  # whole segments only
+                rows.extend(range(a, b))
+            assert rows == list(range(n))
+
+
+def _seg_worker(rank, world, port, q):
+    """segment_parallel_forward's plumbing on gloo with a CPU stand-in for the
+    kernel (the real one needs a GPU): each rank "computes" its rows and the
+    all-gather must reassemble the full sequence in order."""
+    import dataclasses
+
+    import paper_2403_09195_b200 as dfa_pkg
+    from paper_2403_09195_b200 import dist as ddist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def fake_forward(qq, kk, vv, cfg, out=None, stream=None):
+        assert qq.shape[1] == cfg.seq_len  # the local problem keeps the segment grid
+        return vv * 2
+
+    dfa_pkg.dfa_forward = fake_forward
+    cfg = dfa_pkg.AttentionConfig(1000, 300, 2, 1, 4, [0])
+    v = torch.arange(1000, dtype=torch.float32).view(1, 1000, 1, 1).expand(1, 1000, 1, 4).contiguous()
+    out = ddist.segment_parallel_forward(v, v, v, dataclasses.replace(cfg))
+    q.put((rank, out[0, :, 0, 0].tolist()))
+    dist.destroy_process_group()
+
+
+def test_segment_parallel_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seg_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, rows in res:
+        assert rows == [2.0 * i for i in range(1000)]
