@@ -73,3 +73,28 @@ def test_config5_batch_decomposition(dfa, cuda):
     parts = torch.cat([dfa.dfa_forward(q[i:i + 256], k[i:i + 256], v[i:i + 256], cfg) for i in range(0, 1024, 256)])
     torch.cuda.synchronize()
     assert torch.equal(whole, parts)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_segment_sharded_forward_is_bit_identical(dfa, cuda, world):
+    """dist.segment_parallel_forward's partition (whole segments per rank, the
+    unchanged kernel on each N' = stop - start problem) reproduces the
+    one-GPU output bit for bit -- computed here shard by shard on one GPU."""
+    import dataclasses
+
+    import torch
+    from paper_2403_09195_b200.dist import segment_shard
+
+    g = torch.Generator(device="cuda").manual_seed(world)
+    q, k, v = (torch.randn((2, 4096, 6, 64), device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
+    cfg = _cfg(dfa, 512, 2)
+    full = dfa.dfa_forward(q, k, v, cfg)
+    parts = []
+    for rank in range(world):
+        a, b = segment_shard(4096, 512, rank, world)
+        if b > a:
+            local = dataclasses.replace(cfg, seq_len=b - a)
+            parts.append(dfa.dfa_forward(q[:, a:b].contiguous(), k[:, a:b].contiguous(), v[:, a:b].contiguous(),
+                                         local))
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, dim=1), full)
