@@ -123,9 +123,13 @@ dfa_status_t dfa_dilated_attention_host(const dfa_config_t* cfg, dfa_dtype_t dty
                                         const void* v, int64_t head_offset, int32_t workers, void* out,
                                         dfa_workspace_t* ws);
 
-/* Batched forward on HOST buffers (the end-to-end call): H2D copy of q, k, v,
- * dfa_forward, D2H copy of o (and lse if non-NULL), stream synchronize.  Pinned
- * host buffers give full PCIe bandwidth; pageable ones work, slower. */
+/* Batched forward on HOST buffers (the end-to-end call): q, k, v reach the
+ * device, dfa_forward runs, o (and lse if non-NULL) come back, then a stream
+ * synchronize -- pipelined over image chunks on two copy streams.  When q, k, v
+ * are pinned (mapped) host memory and the call takes the tcgen05 path, the
+ * kernel TMA-reads only the kept rows straight from host memory over PCIe
+ * (no staging copy; dfa_host_transfer_bytes reports the bytes); otherwise
+ * they are copied in.  Pageable buffers work, slower. */
 dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
                               const void* k, const void* v, void* o, float* lse, dfa_workspace_t* ws,
                               void* stream);
@@ -134,6 +138,14 @@ dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_
  * adds 1e-3 to output element 0 so the parity harness demonstrably fails. */
 void dfa_set_fault_perturb(int32_t armed);
 int32_t dfa_get_fault_perturb(void);
+
+/* Zero-copy input mode of dfa_forward_host (default on; 0 forces the copy-in
+ * pipeline).  Process-wide. */
+void dfa_set_host_zero_copy(int32_t enabled);
+/* Bytes dfa_forward_host moves host->device (h2d) and device->host (d2h) for
+ * these buffers: kept rows of q, k, v in zero-copy mode, whole tensors otherwise. */
+dfa_status_t dfa_host_transfer_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                                     const void* k, const void* v, int32_t with_lse, size_t* h2d, size_t* d2h);
 
 /* Bytes a dfa_forward_host call needs in its workspace. */
 dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t with_lse,

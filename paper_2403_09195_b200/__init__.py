@@ -371,6 +371,27 @@ def dfa_forward_host(q, k, v, out, cfg: AttentionConfig, ws: Workspace, dtype: s
     return out
 
 
+@contextlib.contextmanager
+def host_zero_copy(enabled: bool):
+    """Scope dfa_forward_host's zero-copy input mode (default on)."""
+    lib.dfa_set_host_zero_copy(1 if enabled else 0)
+    try:
+        yield
+    finally:
+        lib.dfa_set_host_zero_copy(1)
+
+
+def host_transfer_bytes(q, k, v, cfg: AttentionConfig, dtype: str = "bf16", with_lse: bool = False):
+    """(h2d, d2h) bytes dfa_forward_host moves for these host tensors."""
+    c = cfg._c()
+    c.value_dim = v.shape[-1]
+    h2d, d2h = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(lib.dfa_host_transfer_bytes(ctypes.byref(c), _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16,
+                                       q.shape[0], q.data_ptr(), k.data_ptr(), v.data_ptr(), 1 if with_lse else 0,
+                                       ctypes.byref(h2d), ctypes.byref(d2h)))
+    return h2d.value, d2h.value
+
+
 def dfa_forward_multibranch(q, k, v, cfg: AttentionConfig, branches, out=None, lse=None, stream=None,
                             workspace=None):
     """EXTENSION: LSE-weighted combine of several (w, r) branches (include/dfa.h).

@@ -21,6 +21,7 @@ thread_local std::string g_last_error;
 thread_local int32_t g_launches = 0;
 std::atomic<int32_t> g_fault{0};
 std::atomic<int32_t> g_path_override{0};
+std::atomic<int32_t> g_host_zero_copy{1};
 
 dfa_status_t fail(dfa_status_t st, const char* fmt, ...) {
   char buf[512];
@@ -102,6 +103,16 @@ int pick_path(const dfa_impl::Geometry& g, dfa_dtype_t dtype, const void* q, con
 
 size_t elem_size(dfa_dtype_t t) { return t == DFA_F32 ? 4 : 2; }
 
+// Device address of pinned, mapped host memory (nullptr for pageable or device memory).
+const void* mapped_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
+}
+
 }  // namespace
 
 namespace dfa_impl {
@@ -118,7 +129,10 @@ dfa_status_t fail_msg(dfa_status_t st, const char* fmt, ...) {
 
 // Device staging for the host-buffer entry points, plus the copy streams and
 // events of the chunked H2D -> kernel -> D2H pipeline (created on first use).
-constexpr int kHostChunks = 8;
+#ifndef DFA_HOST_CHUNKS
+#define DFA_HOST_CHUNKS 16
+#endif
+constexpr int kHostChunks = DFA_HOST_CHUNKS;
 struct dfa_workspace {
   void* dev = nullptr;
   size_t bytes = 0;
@@ -135,6 +149,35 @@ int32_t dfa_last_launch_count(void) { return g_launches; }
 void dfa_set_fault_perturb(int32_t armed) { g_fault.store(armed ? 1 : 0); }
 int32_t dfa_get_fault_perturb(void) { return g_fault.load(); }
 void dfa_set_path_override(int32_t path) { g_path_override.store(path); }
+void dfa_set_host_zero_copy(int32_t enabled) { g_host_zero_copy.store(enabled ? 1 : 0); }
+
+dfa_status_t dfa_host_transfer_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
+                                     const void* k, const void* v, int32_t with_lse, size_t* h2d, size_t* d2h) {
+  dfa_impl::Geometry g;
+  dfa_status_t st = resolve(cfg, batch, &g);
+  if (st != DFA_OK) return st;
+  if (!h2d || !d2h) return fail(DFA_ERR_DIMENSION, "dfa_host_transfer_bytes: null output");
+  const size_t es = elem_size(dtype);
+  *d2h = (size_t)(g.B * g.N * g.h * g.dv) * es + (with_lse ? (size_t)(g.B * g.h * g.N) * 4 : 0);
+  const void* zq = g_host_zero_copy.load() ? mapped_host(q) : nullptr;
+  const bool zero_copy = zq && mapped_host(k) && mapped_host(v) &&
+                         pick_path(g, dtype, mapped_host(q), mapped_host(k), mapped_host(v), zq) ==
+                             DFA_PATH_SM100_TCGEN05;
+  if (!zero_copy) {
+    *h2d = (size_t)(g.B * g.N * g.h) * (2 * g.d + g.dv) * es;
+    return DFA_OK;
+  }
+  // kept rows only: sum over heads and segments of the view sizes
+  size_t rows = 0;
+  for (int64_t j = 0; j < g.h; ++j)
+    for (int64_t i = 0; i < g.n_seg; ++i) {
+      int64_t m = 0;
+      dfa_segment_view(g.N, g.w, g.r, i, g.offsets[j], nullptr, 0, &m);
+      rows += (size_t)m;
+    }
+  *h2d = (size_t)g.B * rows * (size_t)(2 * g.d + g.dv) * es;
+  return DFA_OK;
+}
 
 dfa_status_t dfa_validate(const dfa_config_t* cfg, int32_t require_full_coverage) {
   return validate(cfg, require_full_coverage);
@@ -331,6 +374,14 @@ dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_
     if (!ok) return fail(DFA_ERR_CUDA, "dfa_forward_host: stream/event creation failed");
     ws->pipe = true;
   }
+  // Zero-copy inputs: when q, k, v are pinned host memory mapped into the
+  // device address space and the call takes the tcgen05 path, the kernel's
+  // TMA boxes read the kept rows straight over PCIe -- half (r = 2) or less
+  // of the tensors' bytes ever cross the bus, and no staging copy exists.
+  const void* zq = g_host_zero_copy.load() ? mapped_host(q) : nullptr;
+  const void* zk = zq ? mapped_host(k) : nullptr;
+  const void* zv = zk ? mapped_host(v) : nullptr;
+  const bool zero_copy = zv && pick_path(g, dtype, zq, zk, zv, dout) == DFA_PATH_SM100_TCGEN05;
   // Pipeline over image chunks: H2D of chunk c+1 (copy engine 1) overlaps
   // the kernel of chunk c and the D2H of chunk c-1 (copy engine 2), so the
   // call costs ~max(H2D, D2H) instead of their sum.
@@ -345,6 +396,12 @@ dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_
     const int64_t b0 = c * per, nb = std::min<int64_t>(per, g.B - b0);
     if (nb <= 0) break;
     const size_t oqk = (size_t)b0 * img_qk, ov = (size_t)b0 * img_v, ol = (size_t)b0 * img_l;
+    if (zero_copy) {
+      st = dfa_forward(cfg, dtype, nb, static_cast<const char*>(zq) + oqk, static_cast<const char*>(zk) + oqk,
+                       static_cast<const char*>(zv) + ov, dout + ov, dl ? dl + ol / 4 : nullptr, stream);
+      if (st != DFA_OK) return st;
+      launches += g_launches;
+    } else {
     if ((err = cudaMemcpyAsync(dq + oqk, static_cast<const char*>(q) + oqk, nb * img_qk, cudaMemcpyHostToDevice,
                                ws->in_s)) != cudaSuccess ||
         (err = cudaMemcpyAsync(dk + oqk, static_cast<const char*>(k) + oqk, nb * img_qk, cudaMemcpyHostToDevice,
@@ -357,6 +414,7 @@ dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_
     st = dfa_forward(cfg, dtype, nb, dq + oqk, dk + oqk, dv + ov, dout + ov, dl ? dl + ol / 4 : nullptr, stream);
     if (st != DFA_OK) return st;
     launches += g_launches;
+    }
     if ((err = cudaEventRecord(ws->fwd_done[c], s)) != cudaSuccess ||
         (err = cudaStreamWaitEvent(ws->out_s, ws->fwd_done[c], 0)) != cudaSuccess ||
         (err = cudaMemcpyAsync(static_cast<char*>(o) + ov, dout + ov, nb * img_v, cudaMemcpyDeviceToHost,
