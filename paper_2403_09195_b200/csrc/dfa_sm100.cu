@@ -61,9 +61,14 @@ namespace {
 
 constexpr int kD = 64;                 // head_dim handled by this kernel
 constexpr int kBM = 128;               // query rows per slot (MMA M)
-constexpr int kBN = 128;               // keys per tile (MMA N of Q K^T, K of P V)
+#ifndef DFA_BN
+#define DFA_BN 128
+#endif
+constexpr int kBN = DFA_BN;            // keys per tile (MMA N of Q K^T, K of P V): 128 or 64
+constexpr int kSC = kBN / 32;          // 32-column chunks of an S tile
 constexpr int kUnitRows = 2 * kBM;     // t'-rows per work unit
 constexpr int kTileBytes = 128 * 128;  // 128 rows x 128 B (64 bf16), SW128
+constexpr int kKVTileBytes = kBN * 128;  // key / value tile: kBN rows x 128 B
 #ifndef DFA_K_STAGES
 #define DFA_K_STAGES 3
 #endif
@@ -85,8 +90,8 @@ constexpr int kOStages = DFA_O_STAGES;  // epilogue staging tiles (slot s uses s
 constexpr int kZeroRows = DFA_ZERO_ROWS;
 constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
-constexpr int kSBufs = 3;                                  // rotating S/P buffers
-__host__ __device__ constexpr uint32_t col_s(int buf) { return 128u * buf; }          // S_0..S_2 (P aliases)
+constexpr int kSBufs = 384 / kBN;                          // rotating S/P buffers (3 x 128 or 6 x 64 columns)
+__host__ __device__ constexpr uint32_t col_s(int buf) { return (uint32_t)kBN * buf; }  // S buffers (P aliases)
 __host__ __device__ constexpr uint32_t col_o(int slot) { return 384u + 64u * slot; }  // O_A, O_B
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef DFA_RESCALE_THR
@@ -120,8 +125,8 @@ struct Unit {
 
 struct __align__(1024) SmemLayout {
   uint8_t q[kQStages][2][kTileBytes];  // contiguous: tile (stage, slot) at index stage * 2 + slot
-  uint8_t k[kKStages][kTileBytes];
-  uint8_t v[kVStages][kTileBytes];
+  uint8_t k[kKStages][kKVTileBytes];
+  uint8_t v[kVStages][kKVTileBytes];
   uint8_t ostage[kOStages][kTileBytes];
   uint8_t zero[kZeroRows * 128];
   uint64_t q_full[kQStages], q_empty[kQStages];
@@ -369,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           DFA_TRACE(0, TR_KV_WAIT);
           DFA_WAIT(&sm.k_empty[st], ((g / kKStages) & 1) ^ 1, 3);
           DFA_TRACE(0, TR_KV_ISSUE);
-          ptx::mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
+          ptx::mbar_arrive_expect_tx(&sm.k_full[st], kKVTileBytes);
           ptx::tma_load_5d(sm.k[st], &tm_k, &sm.k_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
         }
       }
@@ -384,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
           const uint32_t st = g % kVStages;
           DFA_WAIT(&sm.v_empty[st], ((g / kVStages) & 1) ^ 1, 4);
-          ptx::mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
+          ptx::mbar_arrive_expect_tx(&sm.v_full[st], kKVTileBytes);
           ptx::tma_load_5d(sm.v[st], &tm_v, &sm.v_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
         }
       }
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           DFA_WAIT(&sm.k_full[gs], gpar, 6);
           ptx::tc_fence_after();
           DFA_TRACE(1, TR_QK_GOT);
-          const uint64_t kd = kdesc0 + (uint64_t)(gs * (kTileBytes >> 4));
+          const uint64_t kd = kdesc0 + (uint64_t)(gs * (kKVTileBytes >> 4));
 #pragma unroll 1
           for (int sl = 0; sl < 2; ++sl) {
             if (!uses(x, sl, kt)) continue;
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Unit x = make_unit(p, u);
         for (int32_t kt = 0; kt < x.n_kv; ++kt) {
           bool have_v = false;
-          const uint64_t vdesc = vdesc0 + (uint64_t)(gs * (kTileBytes >> 4));
+          const uint64_t vdesc = vdesc0 + (uint64_t)(gs * (kKVTileBytes >> 4));
 #pragma unroll 1
           for (int sl = 0; sl < 2; ++sl) {
             if (!uses(x, sl, kt)) continue;
@@ -541,16 +546,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       use_par ^= 1u << b;
       ptx::tc_fence_after();
       const uint32_t tS = tbase + lane_base + col_s(b);
-      uint32_t sr[4][32];
+      uint32_t sr[kSC][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) ptx::tmem_ld32(tS + 32 * c, sr[c]);
+      for (int c = 0; c < kSC; ++c) ptx::tmem_ld32(tS + 32 * c, sr[c]);
       ptx::tmem_ld_wait();
       const int32_t k0 = x.kv_lo + kt * kBN;
       const int32_t lo = min(max(seg_lo - k0, 0), kBN);
       const int32_t hi = min(max(seg_hi - k0, 0), kBN);
       if (!(lo == 0 && hi == kBN)) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < kSC; ++c)
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             const int col = 32 * c + e;
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
         const float2 c2 = make_float2(p.c, p.c), n2 = make_float2(neg, neg);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < kSC; ++c) {
           float2 xv[16];
 #pragma unroll
           for (int e = 0; e < 16; ++e)
@@ -614,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < kSC; ++c)
 #pragma unroll
           for (int e = 0; e < 32; ++e) mx[e & 7] = fmaxf(mx[e & 7], __uint_as_float(sr[c][e]));
         const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
@@ -867,8 +872,8 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
     return 0;
   }
   CUtensorMap mq, mk, mv, mo, mz;
-  if (!make_map(&mq, q, g.B, g.N, g.r, g.h, g.ldq) || !make_map(&mk, k, g.B, g.N, g.r, g.h, g.ldk) ||
-      !make_map(&mv, v, g.B, g.N, g.r, g.h, g.ldv) || !make_map(&mo, o, g.B, g.N, g.r, g.h, g.ldo) ||
+  if (!make_map(&mq, q, g.B, g.N, g.r, g.h, g.ldq) || !make_map(&mk, k, g.B, g.N, g.r, g.h, g.ldk, kBN) ||
+      !make_map(&mv, v, g.B, g.N, g.r, g.h, g.ldv, kBN) || !make_map(&mo, o, g.B, g.N, g.r, g.h, g.ldo) ||
       !make_map(&mz, o, g.B, g.N, g.r, g.h, g.ldo, kZeroRows)) {
     *why = "cuTensorMapEncodeTiled failed";
     *err = cudaErrorInvalidValue;
