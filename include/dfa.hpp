@@ -229,8 +229,8 @@ template <class Tensor>
 Tensor dilated_attention(const Tensor& q, const Tensor& k, const Tensor& v, const AttentionConfig& cfg,
                          Index head_offset, int workers = 1) {
   using Scalar = std::remove_cv_t<std::remove_pointer_t<decltype(q.data())>>;
-  static_assert(std::is_same_v<Scalar, float>,
-                "dfa::dilated_attention runs the fp32 device path; convert double tensors to float");
+  static_assert(std::is_same_v<Scalar, float> || std::is_same_v<Scalar, double>,
+                "dfa::dilated_attention takes float or double tensors");
   (void)workers;
   cfg.validate();
   detail::require_rank2(q, "dilated_attention");
@@ -257,8 +257,24 @@ Tensor dilated_attention(const Tensor& q, const Tensor& k, const Tensor& v, cons
   std::size_t bytes = 0;
   check(dfa_workspace_bytes(&c, DFA_F32, 1, 0, &bytes));
   Tensor out({q.rows(), v.cols()});
-  check(dfa_forward_host(&c, DFA_F32, 1, q.data(), k.data(), v.data(), out.data(), nullptr,
-                         thread_workspace().get(bytes), nullptr));
+  if constexpr (std::is_same_v<Scalar, float>) {
+    check(dfa_forward_host(&c, DFA_F32, 1, q.data(), k.data(), v.data(), out.data(), nullptr,
+                           thread_workspace().get(bytes), nullptr));
+  } else {
+    // double tensors (the reference's f64 mode) run the fp32 device path:
+    // inputs rounded to float, the result widened back (~1e-7 relative)
+    auto narrow = [](const Tensor& t) {
+      const std::size_t n = static_cast<std::size_t>(t.rows() * t.cols());
+      std::vector<float> f(n);
+      for (std::size_t i = 0; i < n; ++i) f[i] = static_cast<float>(t.data()[i]);
+      return f;
+    };
+    const auto fq = narrow(q), fk = narrow(k), fv = narrow(v);
+    std::vector<float> fo(static_cast<std::size_t>(q.rows() * v.cols()));
+    check(dfa_forward_host(&c, DFA_F32, 1, fq.data(), fk.data(), fv.data(), fo.data(), nullptr,
+                           thread_workspace().get(bytes), nullptr));
+    for (std::size_t i = 0; i < fo.size(); ++i) out.data()[i] = static_cast<double>(fo[i]);
+  }
   return out;
 }
 

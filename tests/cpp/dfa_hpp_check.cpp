@@ -12,6 +12,17 @@
 
 #include "dfa.hpp"
 
+// Minimal stand-in with attnkit::Tensor<double>'s rank-2 surface (f64 mode).
+struct TensorD {
+  std::vector<dfa::Index> shape;
+  std::vector<double> buf;
+  explicit TensorD(std::vector<dfa::Index> s) : shape(std::move(s)), buf(static_cast<size_t>(shape[0] * shape[1])) {}
+  dfa::Index rows() const { return shape[0]; }
+  dfa::Index cols() const { return shape[1]; }
+  double* data() { return buf.data(); }
+  const double* data() const { return buf.data(); }
+};
+
 // Minimal stand-in with attnkit::Tensor's rank-2 surface.
 struct Tensor {
   std::vector<dfa::Index> shape;
@@ -110,6 +121,19 @@ static void gpu_checks(const std::string& dir) {
   // rows of the other offset class are exact zeros (attention.hpp:243-245)
   for (dfa::Index i = 0; i < 4096; i += 2)
     for (dfa::Index c = 0; c < 64; ++c) CHECK(out.buf[static_cast<size_t>(i * 64 + c)] == 0.0f);
+  // f64 tensors (the reference's double mode) run the fp32 path and match it
+  {
+    TensorD qd({4096, 64}), kd({4096, 64}), vd({4096, 64});
+    for (size_t i = 0; i < qd.buf.size(); ++i) {
+      qd.buf[i] = q.buf[i];
+      kd.buf[i] = k.buf[i];
+      vd.buf[i] = v.buf[i];
+    }
+    TensorD od = dfa::dilated_attention(qd, kd, vd, cfg, 1);
+    double worst = 0;
+    for (size_t i = 0; i < od.buf.size(); ++i) worst = std::fmax(worst, std::fabs(od.buf[i] - out.buf[i]));
+    CHECK(worst == 0.0);
+  }
   // error paths keep the reference's exception types
   CHECK_THROWS_AS(dfa::dilated_attention(q, k, v, cfg, 2), std::out_of_range);
   Tensor bad({4095, 64});
