@@ -76,3 +76,48 @@ def test_workspace_bytes(dfa):
     cfg = dfa.AttentionConfig(4096, 512, 2, 6, 64, [0, 1, 0, 1, 0, 1])
     n = dfa.Workspace.bytes_for(cfg, "bf16", 2)
     assert n == 4 * 2 * 4096 * 6 * 64 * 2
+
+
+def test_entry_points_validate_before_touching_memory(dfa):
+    """Every C-ABI entry validates geometry / sizes / workspaces and returns the
+    reference-mapped status before any device access (fake pointers here)."""
+    import ctypes
+
+    from paper_2403_09195_b200 import _lib
+
+    L = dfa.lib
+    cfg = dfa.AttentionConfig(4096, 512, 2, 6, 64, [0, 1, 0, 1, 0, 1])
+    c = cfg._c()
+    fake = ctypes.c_void_p(0x1000)
+    # token strides below h*d
+    assert L.dfa_forward_strided(ctypes.byref(c), 1, 1, fake, 10, fake, 384, fake, 384, fake, 384, None,
+                                 None) == _lib.DFA_ERR_DIMENSION
+    # backward workspace too small
+    assert L.dfa_backward(ctypes.byref(c), 1, 1, *([fake] * 10), 16, None) == _lib.DFA_ERR_DIMENSION
+    # multibranch: 9 branches is over the limit
+    br = (_lib.DfaBranch * 9)()
+    need = ctypes.c_size_t(0)
+    assert L.dfa_multibranch_workspace_bytes(ctypes.byref(c), 9, 1, 1, ctypes.byref(need)) == _lib.DFA_ERR_CONFIG
+    assert L.dfa_forward_multibranch(ctypes.byref(c), 9, br, 1, 1, fake, fake, fake, fake, None, fake, 1 << 40,
+                                     None) == _lib.DFA_ERR_CONFIG
+    # multi-head needs full coverage; encoder block needs a positive MLP width
+    partial = dfa.AttentionConfig(4096, 512, 4, 2, 64, [0, 1])._c()
+    assert L.dfa_multi_head_workspace_bytes(ctypes.byref(partial), 1, 1, ctypes.byref(need)) == _lib.DFA_ERR_CONFIG
+    assert "covered by no head" in L.dfa_last_error().decode()
+    assert L.dfa_encoder_block_workspace_bytes(ctypes.byref(c), 1, 1, 0, ctypes.byref(need)) == _lib.DFA_ERR_CONFIG
+    # bad dtype code
+    assert L.dfa_forward(ctypes.byref(c), 7, 1, fake, fake, fake, fake, None, None) == _lib.DFA_ERR_CONFIG
+    # batch 0 is a no-op success
+    assert L.dfa_forward(ctypes.byref(c), 1, 0, fake, fake, fake, fake, None, None) == _lib.DFA_OK
+    # null tensor pointers
+    assert L.dfa_forward(ctypes.byref(c), 1, 1, None, fake, fake, fake, None, None) == _lib.DFA_ERR_DIMENSION
+
+
+def test_host_transfer_bytes_for_pageable_memory(dfa):
+    """Pageable host buffers cannot be read in place: the whole tensors are copied."""
+    import torch
+
+    cfg = dfa.AttentionConfig(1024, 256, 2, 2, 64, [0, 1])
+    q, k, v = (torch.zeros((2, 1024, 2, 64), dtype=torch.bfloat16) for _ in range(3))
+    h2d, d2h = dfa.host_transfer_bytes(q, k, v, cfg)
+    assert (h2d, d2h) == (3 * q.numel() * 2, q.numel() * 2)
