@@ -168,7 +168,8 @@ struct Sm100Params {
   int32_t N, T;      // T = N / r (t'-stream length per (b, j))
   int32_t m;         // t'-rows per full segment (w / r)
   int32_t r, h;
-  int32_t n_pairs;   // ceil(T / 256) work units per (b, j) stream
+  int32_t n_pairs;   // ceil(T / unit_rows) work units per (b, j) stream
+  int32_t unit_rows; // 256 (slots A + B) or 128 (slot A only: twice the units for small grids)
   int32_t n_units;   // B * h * n_pairs
   float c;           // scale * log2(e)
   float scale;
@@ -205,12 +206,13 @@ __device__ __forceinline__ Unit make_unit(const Sm100Params& p, int32_t u) {
   x.j = bj - x.b * p.h;
 #endif
   x.gamma = p.offsets[x.j];
-  x.t0 = pair * kUnitRows;
+  x.t0 = pair * p.unit_rows;
   int32_t lo[2], hi[2];
 #pragma unroll
   for (int s = 0; s < 2; ++s) {
     const int32_t r0 = x.t0 + s * kBM;
-    const int32_t r1 = min(r0 + kBM, p.T);
+    // half units (small grids): slot B stays empty, every CTA gets one 128-row tile
+    const int32_t r1 = (s == 1 && p.unit_rows == kBM) ? r0 : min(r0 + kBM, p.T);
     if (r0 < r1) {
       lo[s] = p.div_m.div(r0) * p.m;
       hi[s] = min((p.div_m.div(r1 - 1) + 1) * p.m, p.T);
@@ -885,7 +887,13 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.m = (int32_t)(g.w / g.r);
   p.r = (int32_t)g.r;
   p.h = (int32_t)g.h;
+  p.unit_rows = kUnitRows;
   p.n_pairs = (p.T + kUnitRows - 1) / kUnitRows;
+  // small grids: 128-row half units when twice the units still fit one wave
+  if ((int64_t)g.B * g.h * ((p.T + kBM - 1) / kBM) <= num_sms()) {
+    p.unit_rows = kBM;
+    p.n_pairs = (p.T + kBM - 1) / kBM;
+  }
   p.n_units = (int32_t)(g.B * g.h * p.n_pairs);
   p.scale = g.scale;
   p.c = g.scale * kLog2e;

@@ -50,10 +50,12 @@ class Bar:
 def make_unit(p, u):
     j, bp = u % p["h"], u // p["h"]  # head-major unit order (DFA_HEAD_MAJOR)
     pair, b = bp % p["n_pairs"], bp // p["n_pairs"]
-    t0 = pair * 2 * KBM
+    unit = p.get("unit_rows", 2 * KBM)
+    t0 = pair * unit
     lo, hi = [], []
     for s in range(2):
-        r0, r1 = t0 + s * KBM, min(t0 + s * KBM + KBM, p["T"])
+        r0 = t0 + s * KBM
+        r1 = r0 if (s == 1 and unit == KBM) else min(r0 + KBM, p["T"])  # half units: slot B empty
         if r0 < r1:
             lo.append((r0 // p["m"]) * p["m"])
             hi.append(min(((r1 - 1) // p["m"] + 1) * p["m"], p["T"]))
@@ -254,10 +256,15 @@ def run(p, cta, seed=0):
             return {n: (w[1].name, w[2], w[1].phase) for n, w in blocked.items() if w is not None}
 
 
-def params(N, w, r, h, Bt, grid):
+def params(N, w, r, h, Bt, grid, sms=148):
+    """Mirror of launch_sm100's unit geometry (half units when the grid is small)."""
     T, m = N // r, w // r
-    n_pairs = -(-T // 256)
-    return dict(T=T, m=m, h=h, n_pairs=n_pairs, n_units=Bt * h * n_pairs, grid=grid)
+    unit = 2 * KBM
+    n_pairs = -(-T // unit)
+    if Bt * h * -(-T // KBM) <= sms:
+        unit = KBM
+        n_pairs = -(-T // unit)
+    return dict(T=T, m=m, h=h, n_pairs=n_pairs, n_units=Bt * h * n_pairs, grid=grid, unit_rows=unit)
 
 
 if __name__ == "__main__":
