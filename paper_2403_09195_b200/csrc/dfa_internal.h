@@ -36,6 +36,12 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr,
                  unsigned long long* watchdog = nullptr, bool merge = false);
 
+// Four-slot variant of the tcgen05 kernel (dfa_sm100_v2.cu): same coverage
+// as launch_sm100 without merge mode; 512-row work units.
+int launch_sm100_v2(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
+                    cudaStream_t stream, cudaError_t* err, const char** why);
+int64_t sm100_v2_units(const Geometry& g);
+
 // LSE-weighted combine of nb <= 8 branch outputs (dfa_combine.cu).
 int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int nb, const void* const* o,
                    const float* const* lse, void* out, float* lse_out, cudaStream_t stream, cudaError_t* err);
