@@ -23,6 +23,7 @@
 #include <mutex>
 
 #include "dfa_internal.h"
+#include "sm100_ptx.cuh"
 
 namespace dfa_impl {
 namespace {
@@ -113,6 +114,85 @@ __global__ void __launch_bounds__(256) layer_norm_vec_kernel(const T* __restrict
   }
 }
 
+// bf16 production form of layer_norm_vec_kernel: the same two-pass fp32
+// statistics with the row kept as packed float pairs (FADD2 / FFMA2 / FMUL2),
+// bf16 unpacked by shifts.  Each warp walks rows (grid-stride) with its lanes'
+// g / b columns unpacked once.  ~4 instructions per element (the generic
+// form spends ~33 on per-element bf16 insert / extract), so the pass runs at
+// HBM speed.  kVec = 16-byte vectors per lane (D <= 256 * kVec).
+template <int kVec>
+__global__ void __launch_bounds__(256) layer_norm_bf16_kernel(const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ g,
+                                                              const __nv_bfloat16* __restrict__ b,
+                                                              __nv_bfloat16* __restrict__ y, int64_t rows, int cols) {
+  const int lane = threadIdx.x & 31;
+  const int nv = cols / 8;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  float2 gg[kVec][4], bb[kVec][4];
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    const int vi = lane + 32 * i;
+    const uint4 gr = vi < nv ? reinterpret_cast<const uint4*>(g)[vi] : make_uint4(0, 0, 0, 0);
+    const uint4 br = vi < nv ? reinterpret_cast<const uint4*>(b)[vi] : make_uint4(0, 0, 0, 0);
+    const uint32_t gw[4] = {gr.x, gr.y, gr.z, gr.w}, bw[4] = {br.x, br.y, br.z, br.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      gg[i][e] = ptx::bf16x2_to_float2(gw[e]);
+      bb[i][e] = ptx::bf16x2_to_float2(bw[e]);
+    }
+  }
+  const float rc = 1.0f / (float)cols;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+    float2 v[kVec][4];
+    float2 s2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i < kVec; ++i) {
+      const int vi = lane + 32 * i;
+      const uint4 r = vi < nv ? xr[vi] : make_uint4(0, 0, 0, 0);
+      const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[i][e] = ptx::bf16x2_to_float2(w[e]);
+        s2 = ptx::fadd2(s2, v[i][e]);
+      }
+    }
+    float sum = s2.x + s2.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum * rc;
+    const float2 nm = make_float2(-mean, -mean);
+    float2 q2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int i = 0; i < kVec; ++i) {
+      if (lane + 32 * i >= nv) continue;  // padded lanes hold zeros, not x - mean
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[i][e] = ptx::fadd2(v[i][e], nm);
+        q2 = ptx::ffma2(v[i][e], v[i][e], q2);
+      }
+    }
+    float var = q2.x + q2.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+    const float inv = 1.0f / sqrtf(var * rc + 1e-5f);
+    const float2 inv2 = make_float2(inv, inv);
+    uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+#pragma unroll
+    for (int i = 0; i < kVec; ++i) {
+      const int vi = lane + 32 * i;
+      if (vi >= nv) continue;
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 t = ptx::ffma2(ptx::fmul2(v[i][e], inv2), gg[i][e], bb[i][e]);
+        o[e] = ptx::pack_bf16x2(t.x, t.y);
+      }
+      yr[vi] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
 // Scalar fallback (any D <= 1024, any alignment).
 template <typename T>
 __global__ void __launch_bounds__(256) layer_norm_kernel(const T* __restrict__ x, const T* __restrict__ g,
@@ -193,6 +273,32 @@ __global__ void __launch_bounds__(256) gelu_kernel(const T* __restrict__ xin, T*
   for (int64_t i = done + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const float v = ldf(xin + i);
     x[i] = stf<T>(v * 0.5f * (1.0f + erff(v * 0.70710678118654752f)));
+  }
+}
+
+// bf16 production GELU: x * Phi(x) with Phi(x) = (1 + tanh(x (a + b x^2))) / 2,
+// a, b refitted to the erf form (max |error| 2.7e-4 over all x, plus
+// tanh.approx's 2^-11 relative) -- below bf16's resolution of the result, on
+// one MUFU.TANH and ~4 packed ops per element instead of erf's two MUFU ops
+// and ~30 scalar ones.  The fp32 validation mode keeps erf_fast.
+__global__ void __launch_bounds__(256) gelu_bf16_kernel(const uint4* __restrict__ xin, uint4* __restrict__ x,
+                                                        int64_t nv) {
+  const float2 a2 = make_float2(0.80015708f, 0.80015708f), b2 = make_float2(0.03470089f, 0.03470089f);
+  const float2 h2 = make_float2(0.5f, 0.5f);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    const uint4 r = xin[i];
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 v = ptx::bf16x2_to_float2(w[e]);
+      const float2 u = ptx::fmul2(v, ptx::ffma2(ptx::fmul2(v, v), b2, a2));
+      const float2 hv = ptx::fmul2(v, h2);
+      const float2 t = ptx::ffma2(hv, make_float2(ptx::tanh_approx(u.x), ptx::tanh_approx(u.y)), hv);
+      o[e] = ptx::pack_bf16x2(t.x, t.y);
+    }
+    x[i] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -361,8 +467,12 @@ int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, vo
                                                          (float*)y, rows, cols);
   } else {
     using B = __nv_bfloat16;
-    if (al && cols % 8 == 0 && cols <= 8 * 32 * 4)
-      layer_norm_vec_kernel<B, 4><<<grid_vec, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
+    // packed form: 4 rows per warp on a grid of 148 x 16 blocks at most
+    const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, 148 * 16));
+    if (al && cols % 8 == 0 && cols <= 8 * 32 * 2)
+      layer_norm_bf16_kernel<2><<<grid_b, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
+    else if (al && cols % 8 == 0 && cols <= 8 * 32 * 4)
+      layer_norm_bf16_kernel<4><<<grid_b, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
     else
       layer_norm_kernel<B><<<grid, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
   }
@@ -387,6 +497,8 @@ int launch_gelu(int dtype, const void* xin, void* x, int64_t n, cudaStream_t str
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n / per + 255) / 256, 148 * 64));
   if (dtype == 0)
     gelu_kernel<float><<<grid, 256, 0, stream>>>((const float*)xin, (float*)x, n, vec);
+  else if (vec && n % 8 == 0)
+    gelu_bf16_kernel<<<grid, 256, 0, stream>>>((const uint4*)xin, (uint4*)x, n / 8);
   else
     gelu_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)xin, (__nv_bfloat16*)x, n, vec);
   return 1;

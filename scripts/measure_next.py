@@ -61,7 +61,7 @@ def main():
     by = 5 * kept + B * h * (N // r) * 4 + 3 * B * N * h * d * 2
     res["backward"] = {"ms": ms, "tflops": 2.5 * fwd_flop / ms / 1e9, "GBps": by / ms / 1e6,
                        "forward_ms": time_ms(lambda: dfa.dfa_forward(q, k, v, cfg, out=o, lse=L)),
-                       "path": "SIMT fp32-math kernels (delta, dK/dV, dQ)"}
+                       "path": "delta kernel + fused tcgen05 backward (m = w / r = %d)" % (w // r)}
     del q, k, v, do, o, dq, dk, dv, L
     if a.only == "backward":
         print(json.dumps(res, indent=1))
