@@ -115,42 +115,47 @@ __global__ void __launch_bounds__(256) layer_norm_vec_kernel(const T* __restrict
 }
 
 // bf16 production form of layer_norm_vec_kernel: the same two-pass fp32
-// statistics with the row kept as packed float pairs (FADD2 / FFMA2 / FMUL2),
-// bf16 unpacked by shifts.  Each warp walks rows (grid-stride) with its lanes'
-// g / b columns unpacked once.  ~4 instructions per element (the generic
-// form spends ~33 on per-element bf16 insert / extract), so the pass runs at
-// HBM speed.  kVec = 16-byte vectors per lane (D <= 256 * kVec).
-template <int kVec>
+// statistics with rows kept as packed float pairs (FADD2 / FFMA2 / FMUL2) and
+// bf16 unpacked by shifts (~6 instructions per element instead of the
+// generic form's ~33 on per-element bf16 insert / extract).  Each warp owns
+// kRows consecutive rows and issues all their 16-byte loads before any math,
+// so kRows x D x 2 bytes per warp are in flight (one row per warp left the
+// pass latency-bound at ~2.8 TB/s).  kVec = 16-byte vectors per lane.
+template <int kVec, int kRows>
 __global__ void __launch_bounds__(256) layer_norm_bf16_kernel(const __nv_bfloat16* __restrict__ x,
                                                               const __nv_bfloat16* __restrict__ g,
                                                               const __nv_bfloat16* __restrict__ b,
                                                               __nv_bfloat16* __restrict__ y, int64_t rows, int cols) {
   const int lane = threadIdx.x & 31;
+  const int64_t row0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRows;
+  if (row0 >= rows) return;
   const int nv = cols / 8;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  float2 gg[kVec][4], bb[kVec][4];
+  const float rc = 1.0f / (float)cols;
+  uint4 raw[kRows][kVec];
+#pragma unroll
+  for (int rr = 0; rr < kRows; ++rr) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (row0 + rr) * cols);
+#pragma unroll
+    for (int i = 0; i < kVec; ++i) {
+      const int vi = lane + 32 * i;
+      raw[rr][i] = (vi < nv && row0 + rr < rows) ? xr[vi] : make_uint4(0, 0, 0, 0);
+    }
+  }
+  uint4 graw[kVec], braw[kVec];
 #pragma unroll
   for (int i = 0; i < kVec; ++i) {
     const int vi = lane + 32 * i;
-    const uint4 gr = vi < nv ? reinterpret_cast<const uint4*>(g)[vi] : make_uint4(0, 0, 0, 0);
-    const uint4 br = vi < nv ? reinterpret_cast<const uint4*>(b)[vi] : make_uint4(0, 0, 0, 0);
-    const uint32_t gw[4] = {gr.x, gr.y, gr.z, gr.w}, bw[4] = {br.x, br.y, br.z, br.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      gg[i][e] = ptx::bf16x2_to_float2(gw[e]);
-      bb[i][e] = ptx::bf16x2_to_float2(bw[e]);
-    }
+    graw[i] = vi < nv ? reinterpret_cast<const uint4*>(g)[vi] : make_uint4(0, 0, 0, 0);
+    braw[i] = vi < nv ? reinterpret_cast<const uint4*>(b)[vi] : make_uint4(0, 0, 0, 0);
   }
-  const float rc = 1.0f / (float)cols;
-  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
-    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+#pragma unroll
+  for (int rr = 0; rr < kRows; ++rr) {
+    if (row0 + rr >= rows) break;
     float2 v[kVec][4];
     float2 s2 = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int i = 0; i < kVec; ++i) {
-      const int vi = lane + 32 * i;
-      const uint4 r = vi < nv ? xr[vi] : make_uint4(0, 0, 0, 0);
-      const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+      const uint32_t w[4] = {raw[rr][i].x, raw[rr][i].y, raw[rr][i].z, raw[rr][i].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         v[i][e] = ptx::bf16x2_to_float2(w[e]);
@@ -177,15 +182,18 @@ __global__ void __launch_bounds__(256) layer_norm_bf16_kernel(const __nv_bfloat1
     for (int o = 16; o > 0; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
     const float inv = 1.0f / sqrtf(var * rc + 1e-5f);
     const float2 inv2 = make_float2(inv, inv);
-    uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+    uint4* yr = reinterpret_cast<uint4*>(y + (row0 + rr) * cols);
 #pragma unroll
     for (int i = 0; i < kVec; ++i) {
       const int vi = lane + 32 * i;
       if (vi >= nv) continue;
+      const uint32_t gw[4] = {graw[i].x, graw[i].y, graw[i].z, graw[i].w};
+      const uint32_t bw[4] = {braw[i].x, braw[i].y, braw[i].z, braw[i].w};
       uint32_t o[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float2 t = ptx::ffma2(ptx::fmul2(v[i][e], inv2), gg[i][e], bb[i][e]);
+        const float2 t =
+            ptx::ffma2(ptx::fmul2(v[i][e], inv2), ptx::bf16x2_to_float2(gw[e]), ptx::bf16x2_to_float2(bw[e]));
         o[e] = ptx::pack_bf16x2(t.x, t.y);
       }
       yr[vi] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -467,12 +475,13 @@ int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, vo
                                                          (float*)y, rows, cols);
   } else {
     using B = __nv_bfloat16;
-    // packed form: 4 rows per warp on a grid of 148 x 16 blocks at most
-    const unsigned grid_b = (unsigned)std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, 148 * 16));
+    const unsigned grid_r = (unsigned)((rows + 31) / 32);  // 8 warps x 4 rows per block
     if (al && cols % 8 == 0 && cols <= 8 * 32 * 2)
-      layer_norm_bf16_kernel<2><<<grid_b, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
+      layer_norm_bf16_kernel<2, 4><<<grid_r, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows,
+                                                              cols);
     else if (al && cols % 8 == 0 && cols <= 8 * 32 * 4)
-      layer_norm_bf16_kernel<4><<<grid_b, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
+      layer_norm_bf16_kernel<4, 2><<<(unsigned)((rows + 15) / 16), 256, 0, stream>>>((const B*)x, (const B*)g,
+                                                                                      (const B*)b, (B*)y, rows, cols);
     else
       layer_norm_kernel<B><<<grid, 256, 0, stream>>>((const B*)x, (const B*)g, (const B*)b, (B*)y, rows, cols);
   }
