@@ -122,6 +122,56 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ o, con
   }
 }
 
+// Delta on the tcgen05 path (bf16, dv = 64, w % r == 0): only the rows a
+// view keeps (n % r == gamma_j) -- every other row of O is exactly zero and
+// its Delta is never read -- so half (r = 2) to 1/8 of the O / dO bytes of
+// delta_kernel.  Eight lanes share a 128-byte row (fully coalesced 16-byte
+// loads: a thread-per-row form at a 1.5 KB row stride ran at ~2 TB/s), a
+// warp covers 4 rows per load and 16 rows per iteration with all 8 loads in
+// flight; the dot product reduces over the 8 lanes with shuffles.
+__global__ void __launch_bounds__(256) delta_kept_kernel(const uint4* __restrict__ o, const uint4* __restrict__ dout,
+                                                         float* __restrict__ delta, int64_t B, int64_t N, int64_t r,
+                                                         int64_t h, const __grid_constant__ BwdParams p) {
+  const int64_t T = N / r, total = B * h * T;
+  const int lane = threadIdx.x & 31, sub = lane >> 3, ch = lane & 7;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 16; base < total; base += warps * 16) {
+    uint4 x[4], y[4];
+    int64_t out[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      // kept row, order (b, t', j): the h heads' 128-byte chunks of the same
+      // token rows are read together (DRAM page locality)
+      const int64_t idx = base + 4 * u + sub;
+      out[u] = -1;
+      x[u] = y[u] = make_uint4(0, 0, 0, 0);
+      if (idx < total) {
+        const int64_t j = idx % h, bt = idx / h;
+        const int64_t t = bt % T, b = bt / T;
+        const int64_t n = t * r + p.offsets[j];
+        const int64_t at = ((b * N + n) * h + j) * 8 + ch;
+        x[u] = o[at];
+        y[u] = dout[at];
+        out[u] = (b * h + j) * N + n;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t xa[4] = {x[u].x, x[u].y, x[u].z, x[u].w}, ya[4] = {y[u].x, y[u].y, y[u].z, y[u].w};
+      float acc = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc = fmaf(__uint_as_float(xa[e] << 16), __uint_as_float(ya[e] << 16), acc);
+        acc = fmaf(__uint_as_float(xa[e] & 0xffff0000u), __uint_as_float(ya[e] & 0xffff0000u), acc);
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      if (ch == 0 && out[u] >= 0) delta[out[u]] = acc;
+    }
+  }
+}
+
 template <typename T, int DMAX, int PARTS, int QT>
 __global__ void __launch_bounds__(128) dkdv_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                    const T* __restrict__ v, const T* __restrict__ dout,
@@ -341,9 +391,17 @@ int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, 
                     cudaStream_t stream, cudaError_t* err, bool allow_sm100, const char** why) {
   const void* ptrs[] = {q, k, v, dout, dq, dk, dv};
   if (allow_sm100 && bwd_sm100_supported(g, dtype, ptrs, 7)) {
-    const int64_t rows = g.B * g.N * g.h;
-    delta_kernel<__nv_bfloat16><<<(unsigned)std::min<int64_t>((rows + 255) / 256, 148 * 32), 256, 0, stream>>>(
-        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, delta, rows, g.N, g.h, g.dv);
+    if ((reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+      BwdParams bp{};
+      for (int j = 0; j < kMaxHeads; ++j) bp.offsets[j] = g.offsets[j];
+      const int64_t kept = g.B * g.h * (g.N / g.r);
+      delta_kept_kernel<<<(unsigned)std::min<int64_t>((kept + 127) / 128, 148 * 16), 256, 0, stream>>>(
+          (const uint4*)o, (const uint4*)dout, delta, g.B, g.N, g.r, g.h, bp);
+    } else {
+      const int64_t rows = g.B * g.N * g.h;
+      delta_kernel<__nv_bfloat16><<<(unsigned)std::min<int64_t>((rows + 255) / 256, 148 * 32), 256, 0, stream>>>(
+          (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, delta, rows, g.N, g.h, g.dv);
+    }
     const int n = launch_bwd_sm100(g, q, k, v, dout, lse, delta, dq, dk, dv, stream, err, why);
     return n ? n + 1 : 0;
   }
