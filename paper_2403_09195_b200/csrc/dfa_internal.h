@@ -61,7 +61,8 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
 // batch; LayerNorm (eps 1e-5) and erf-GELU kernels.  Return 0 on failure.
 int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
                   int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
-                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why);
+                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why,
+                  bool gelu = false);  // gelu: D = GELU(A B + bias), cuBLASLt's (tanh-form) GELU epilogue
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
                       cudaStream_t stream);
 int launch_gelu(int dtype, const void* xin, void* x, int64_t n, cudaStream_t stream);  // x = GELU(xin); may alias

@@ -398,7 +398,8 @@ cublasLtHandle_t lt_handle() {
 // Column-major cuBLASLt sees D^T = B^T A^T: m = N, n = M.
 int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
                   int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
-                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why) {
+                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why,
+                  bool gelu) {
   cublasLtHandle_t h = lt_handle();
   const Lt& L = lt();
   if (!h) {
@@ -412,7 +413,8 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
   int ok = 0;
   do {
     if (L.cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS) break;
-    cublasLtEpilogue_t epi = bias ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT;
+    cublasLtEpilogue_t epi = gelu ? (bias ? CUBLASLT_EPILOGUE_GELU_BIAS : CUBLASLT_EPILOGUE_GELU)
+                                  : (bias ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT);
     L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi));
     if (bias) {
       L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
