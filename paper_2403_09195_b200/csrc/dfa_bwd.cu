@@ -132,27 +132,29 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ o, con
 __global__ void __launch_bounds__(256) delta_kept_kernel(const uint4* __restrict__ o, const uint4* __restrict__ dout,
                                                          float* __restrict__ delta, int64_t B, int64_t N, int64_t r,
                                                          int64_t h, const __grid_constant__ BwdParams p) {
-  const int64_t T = N / r, total = B * h * T;
+  // 32-bit index decode (the launcher guarantees B * h * N < 2^31): int64
+  // division is a long emulated sequence and made this pass issue-bound
+  const uint32_t T = (uint32_t)(N / r), total = (uint32_t)(B * h * T), hh = (uint32_t)h;
   const int lane = threadIdx.x & 31, sub = lane >> 3, ch = lane & 7;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t base = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 16; base < total; base += warps * 16) {
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 16; base < total; base += warps * 16) {
     uint4 x[4], y[4];
     int64_t out[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       // kept row, order (b, t', j): the h heads' 128-byte chunks of the same
       // token rows are read together (DRAM page locality)
-      const int64_t idx = base + 4 * u + sub;
+      const uint32_t idx = base + 4 * u + sub;
       out[u] = -1;
       x[u] = y[u] = make_uint4(0, 0, 0, 0);
       if (idx < total) {
-        const int64_t j = idx % h, bt = idx / h;
-        const int64_t t = bt % T, b = bt / T;
-        const int64_t n = t * r + p.offsets[j];
-        const int64_t at = ((b * N + n) * h + j) * 8 + ch;
+        const uint32_t bt = idx / hh, j = idx - bt * hh;
+        const uint32_t b = bt / T, t = bt - b * T;
+        const uint32_t n = t * (uint32_t)r + (uint32_t)p.offsets[j];
+        const int64_t at = (((int64_t)b * N + n) * h + j) * 8 + ch;
         x[u] = o[at];
         y[u] = dout[at];
-        out[u] = (b * h + j) * N + n;
+        out[u] = ((int64_t)b * h + j) * N + n;
       }
     }
 #pragma unroll
@@ -391,7 +393,7 @@ int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, 
                     cudaStream_t stream, cudaError_t* err, bool allow_sm100, const char** why) {
   const void* ptrs[] = {q, k, v, dout, dq, dk, dv};
   if (allow_sm100 && bwd_sm100_supported(g, dtype, ptrs, 7)) {
-    if ((reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+    if ((reinterpret_cast<uintptr_t>(o) & 15u) == 0 && g.B * g.h * g.N < ((int64_t)1 << 31)) {
       BwdParams bp{};
       for (int j = 0; j < kMaxHeads; ++j) bp.offsets[j] = g.offsets[j];
       const int64_t kept = g.B * g.h * (g.N / g.r);
