@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 namespace dfa_impl {
@@ -18,6 +19,30 @@ struct Geometry {
   int64_t ldq, ldk, ldv, ldo;  // token (row) strides in elements; h*d / h*dv when contiguous
   int32_t offsets[kMaxHeads];
 };
+
+// Launch with the programmatic-stream-serialization attribute (PDL): the
+// kernel's prologue may overlap the previous kernel in the stream; kernels
+// launched this way call griddepcontrol.wait before touching global memory.
+// DFA_PDL=0 in the environment turns it off (measurement).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t stream,
+                              Args... args) {
+  static const bool on = [] {
+    const char* e = getenv("DFA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = on ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 // Generic SIMT kernel: any geometry, f32 (validation mode) or bf16 I/O,
 // fp32 arithmetic, online softmax over key tiles.  Returns launches issued.

@@ -352,6 +352,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = sm.tmem_base;
+  // Programmatic dependent launch: the setup above (barriers, TMEM, zero
+  // tile, descriptor prefetch) overlaps the previous kernel's tail; no global
+  // memory is touched before the previous grid has completed.  Dependents
+  // may start their own setup right away (they wait the same way).
+  ptx::griddep_wait();
+  ptx::griddep_launch_dependents();
 
   // Registers: 512 x 128 at launch; rebalanced per warpgroup to
   // producer/MMA 40, softmax 2 x 192, epilogue 80 (sum 64512 <= 65536).  192
@@ -917,11 +923,13 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
     return 0;
   }
   const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
+  cudaError_t le = cudaSuccess;
   if (trace)
     dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, mz, lse, p, trace, watchdog);
   else
-    dfa_sm100_kernel<false><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, mz, lse, p, nullptr, nullptr);
-  *err = cudaGetLastError();
+    le = launch_pdl(dfa_sm100_kernel<false>, grid, kThreads, smem, stream, mq, mk, mv, mo, mz, lse, p,
+                    (uint64_t*)nullptr, (unsigned long long*)nullptr);
+  *err = le != cudaSuccess ? le : cudaGetLastError();
   return 1;
 }
 
