@@ -199,20 +199,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                           ptx::pack_bf16x2(f[6] * mul, f[7] * mul));
       }
     };
+    // The view's lse (log2 units) and Delta, one query row per thread (nb * 128
+    // <= 256 rows): fetched into registers one unit ahead -- the next unit's
+    // loads go out after this unit's last step, so their latency hides behind
+    // the dK / dV / dQ epilogues -- and copied to shared memory (both
+    // warpgroups read all of it) at the start of the unit.
+    const int t_row = threadIdx.x - 128;
+    float pre_l = 0.0f, pre_d = 0.0f;
+    auto fetch_stats = [&](int32_t uu) {
+      const View y = view(uu);
+      if (t_row < nb * kB) {
+        const int64_t n = (int64_t)(y.t0 + t_row) * p.r + y.gamma;
+        const int64_t off = ((int64_t)y.b * p.h + y.j) * p.N + n;
+        pre_l = lse[off] * kLog2e;
+        pre_d = delta[off];
+      }
+    };
+    fetch_stats(blockIdx.x);
     int it = 0;
     for (int32_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
       const View x = view(u);
-      // the view's lse (log2 units) and Delta; both warpgroups read all of it
       ptx::named_bar_sync(4, 2 * kB);  // previous unit's steps are done with lse2 / dlt
-      {
-        const int t = threadIdx.x - 128;
-        const float* lb = lse + ((int64_t)x.b * p.h + x.j) * p.N;
-        const float* db = delta + ((int64_t)x.b * p.h + x.j) * p.N;
-        for (int tt = t; tt < nb * kB; tt += 2 * kB) {
-          const int64_t n = (int64_t)(x.t0 + tt) * p.r + x.gamma;
-          sm.lse2[tt] = lb[n] * kLog2e;
-          sm.dlt[tt] = db[n];
-        }
+      if (t_row < nb * kB) {
+        sm.lse2[t_row] = pre_l;
+        sm.dlt[t_row] = pre_d;
       }
       ptx::named_bar_sync(4, 2 * kB);
       for (int kb = 0; kb < nb; ++kb) {
@@ -266,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tc_fence_before();
           ptx::mbar_arrive(&sm.p_full);
         }
+        if (kb == nb - 1 && u + (int32_t)gridDim.x < n_units) fetch_stats(u + gridDim.x);  // next unit's stats
         // dK (WG0) / dV (WG1) of key block kb
         wait(&sm.kv_done, kvn & 1);
         ++kvn;

@@ -64,6 +64,8 @@ def main():
                        "path": "delta kernel + fused tcgen05 backward (m = w / r = %d)" % (w // r)}
     del q, k, v, do, o, dq, dk, dv, L
     if a.only == "backward":
+        os.makedirs(os.path.dirname(a.out), exist_ok=True)
+        json.dump(res, open(a.out, "w"), indent=1)
         print(json.dumps(res, indent=1))
         return
 
