@@ -61,7 +61,7 @@ struct __align__(1024) BwdSmem {
   uint8_t zero[kTile];
   float lse2[kMaxBlk * kB];       // lse * log2(e) of the view's query rows
   float dlt[kMaxBlk * kB];        // Delta of the view's query rows
-  uint64_t load_full, s_full, p_full, kv_done, q_done;
+  uint64_t load_full[kMaxBlk], s_full, p_full, kv_done, q_done;  // load_full[blk]: Q, K, V, dO of 128-row block blk
   uint32_t tmem_base;
 };
 
@@ -102,18 +102,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto issue_loads = [&](int32_t u) {
     const View x = view(u);
     const uint64_t pol = ptx::policy_evict_first();
-    ptx::mbar_arrive_expect_tx(&sm.load_full, 4 * nb * kTile);
-    for (int blk = 0; blk < nb; ++blk) {
+    for (int blk = 0; blk < nb; ++blk) {  // block 0 first: the unit's first step needs only it
       const int32_t tb = x.t0 + blk * kB;
-      ptx::tma_load_5d(sm.q[blk], &tm_q, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
-      ptx::tma_load_5d(sm.k[blk], &tm_k, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
-      ptx::tma_load_5d(sm.v[blk], &tm_v, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
-      ptx::tma_load_5d(sm.g[blk], &tm_g, &sm.load_full, 0, x.j, x.gamma, tb, x.b, pol);
+      uint64_t* bar = &sm.load_full[blk];
+      ptx::mbar_arrive_expect_tx(bar, 4 * kTile);
+      ptx::tma_load_5d(sm.q[blk], &tm_q, bar, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.k[blk], &tm_k, bar, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.v[blk], &tm_v, bar, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.g[blk], &tm_g, bar, 0, x.j, x.gamma, tb, x.b, pol);
     }
   };
 
   if (warp == 0 && lane == 0) {
-    ptx::mbar_init(&sm.load_full, 1);
+    for (int blk = 0; blk < kMaxBlk; ++blk) ptx::mbar_init(&sm.load_full[blk], 1);
     ptx::mbar_init(&sm.s_full, 1);
     ptx::mbar_init(&sm.p_full, 2 * kB);
     ptx::mbar_init(&sm.kv_done, 1);
@@ -141,12 +142,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t step = 0;
       int it = 0;
       for (int32_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-        wait(&sm.load_full, it & 1);
+        wait(&sm.load_full[0], it & 1);
         ptx::tc_fence_after();
         for (int kb = 0; kb < nb; ++kb) {
           const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k[kb]));
           const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v[kb]));
           for (int qb = 0; qb < nb; ++qb, ++step) {
+            if (kb == 0 && qb == 1) {  // first step touching block 1 (Q1, dO1; K1, V1 follow)
+              wait(&sm.load_full[1], it & 1);
+              ptx::tc_fence_after();
+            }
             const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[qb]));
             const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[qb]));
 #pragma unroll
