@@ -47,6 +47,12 @@ constexpr int kTile = 128 * 128;       // 128 rows x 128 B (64 bf16), SW128
 constexpr int kMaxBlk = 2;             // m <= 256
 constexpr int kThreads = 384;          // warp 0: TMA + MMA, warp 1: TMEM alloc, warps 4-11: gradient WGs
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef DFA_BWD_POLY_MASK
+#define DFA_BWD_POLY_MASK 0x8080u
+#endif
+// bit e: pair e of each 16-pair (32-query) chunk of the gradient warpgroups
+// takes the FMA-pipe exp2 polynomial (ptx::ex2_poly2) instead of MUFU.EX2
+constexpr uint32_t kBwdPolyMask = DFA_BWD_POLY_MASK;
 #ifndef DFA_BWD_LONG_FROM
 #define DFA_BWD_LONG_FROM 3  // view blocks (m / 128) from which the dkdv + dq pair replaces the fused kernel
 #endif
@@ -252,8 +258,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int q0 = 32 * c + 2 * e;
-              float p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
-              float p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
+              float p0, p1;
+              if ((kBwdPolyMask >> e) & 1u) {  // FMA-pipe exp2 for a share of the pairs (MUFU-bound otherwise)
+                const float2 ex = ptx::ex2_poly2(make_float2(__uint_as_float(s[2 * e]) * p.c - l2[q0],
+                                                             __uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]));
+                p0 = ex.x;
+                p1 = ex.y;
+              } else {
+                p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
+                p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
+              }
               if (p.mseg < kB) {  // packed short segments: no interaction across segments
                 const uint32_t kseg = row / p.mseg;
                 if ((uint32_t)q0 / p.mseg != kseg) p0 = 0.0f;
