@@ -67,7 +67,8 @@ struct __align__(1024) BwdSmem {
   uint8_t zero[kTile];
   float lse2[kMaxBlk * kB];       // lse * log2(e) of the view's query rows
   float dlt[kMaxBlk * kB];        // Delta of the view's query rows
-  uint64_t load_full[kMaxBlk], s_full, p_full, kv_done, q_done;  // load_full[blk]: Q, K, V, dO of 128-row block blk
+  uint64_t load_full[kMaxBlk], kv_done, q_done;  // load_full[blk]: Q, K, V, dO of 128-row block blk
+  uint64_t s_full[2], p_full[2];                 // per query half: S^T / dP^T ready, P^T / dS^T written
   uint32_t tmem_base;
 };
 
@@ -121,8 +122,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int blk = 0; blk < kMaxBlk; ++blk) ptx::mbar_init(&sm.load_full[blk], 1);
-    ptx::mbar_init(&sm.s_full, 1);
-    ptx::mbar_init(&sm.p_full, 2 * kB);
+    for (int hf = 0; hf < 2; ++hf) {
+      ptx::mbar_init(&sm.s_full[hf], 1);
+      ptx::mbar_init(&sm.p_full[hf], kB);
+    }
     ptx::mbar_init(&sm.kv_done, 1);
     ptx::mbar_init(&sm.q_done, 1);
     ptx::fence_barrier_init();
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (ptx::elect_one()) {
       // ------------------------------------------------------------ MMA
-      constexpr uint32_t id_ss = ptx::idesc_bf16(kB, kB, 0, 0);   // S^T, dP^T: K-major A and B
+      constexpr uint32_t id_sh = ptx::idesc_bf16(kB, kB / 2, 0, 0);  // S^T, dP^T per query half: K-major A and B
       constexpr uint32_t id_ts = ptx::idesc_bf16(kB, kD, 0, 1);   // dV, dK: A from TMEM, B MN-major
       constexpr uint32_t id_dq = ptx::idesc_bf16(kB, kD, 1, 1);   // dQ: A (dS) MN-major, B (K) MN-major
       const uint64_t dsd = ptx::sdesc_sw128(ptx::smem_u32(sm.ds[0]), 1024, kTile);  // LBO: next 64 queries
@@ -160,19 +163,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[qb]));
             const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[qb]));
+            // S^T / dP^T in two query halves (N = 64; the half's Q / dO rows
+            // start 64 x 128 B into the tile): gradient warpgroup hf starts
+            // on its half while the other half's products are still running
 #pragma unroll
-            for (int kk = 0; kk < kD / 16; ++kk) {
-              ptx::mma_ss(tbase + cS, kd + 2 * kk, qd + 2 * kk, id_ss, kk > 0);
-              ptx::mma_ss(tbase + cDP, vd + 2 * kk, gd + 2 * kk, id_ss, kk > 0);
+            for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+              for (int kk = 0; kk < kD / 16; ++kk) {
+                ptx::mma_ss(tbase + cS + 64 * hf, kd + 2 * kk, qd + 512 * hf + 2 * kk, id_sh, kk > 0);
+                ptx::mma_ss(tbase + cDP + 64 * hf, vd + 2 * kk, gd + 512 * hf + 2 * kk, id_sh, kk > 0);
+              }
+              ptx::tc_commit(&sm.s_full[hf]);
             }
-            ptx::tc_commit(&sm.s_full);
-            wait(&sm.p_full, step & 1);
-            ptx::tc_fence_after();
+            // dV / dK per half as soon as that warpgroup has written P^T / dS^T
 #pragma unroll
-            for (int kk = 0; kk < kB / 16; ++kk) {
-              // K-step of 16 queries: 8 packed TMEM columns of P^T / dS^T, 16 rows (2048 B) of dO / Q
-              ptx::mma_ts(tbase + cDV, tbase + cS + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
-              ptx::mma_ts(tbase + cDK, tbase + cDP + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+            for (int hf = 0; hf < 2; ++hf) {
+              wait(&sm.p_full[hf], step & 1);
+              ptx::tc_fence_after();
+#pragma unroll
+              for (int kk = 4 * hf; kk < 4 * hf + 4; ++kk) {
+                // K-step of 16 queries: 8 packed TMEM columns of P^T / dS^T, 16 rows (2048 B) of dO / Q
+                ptx::mma_ts(tbase + cDV, tbase + cS + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+                ptx::mma_ts(tbase + cDK, tbase + cDP + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+              }
             }
 #pragma unroll
             for (int kk = 0; kk < kB / 16; ++kk)  // K-step of 16 keys: 16 rows of dS / K
@@ -238,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::named_bar_sync(4, 2 * kB);
       for (int kb = 0; kb < nb; ++kb) {
         for (int qb = 0; qb < nb; ++qb, ++step) {
-          wait(&sm.s_full, step & 1);
+          wait(&sm.s_full[wg], step & 1);
           ptx::tc_fence_after();
           const float* l2 = sm.lse2 + qb * kB;
           const float* dl = sm.dlt + qb * kB;
@@ -293,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_st_wait();
           ptx::fence_proxy_async_smem();
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&sm.p_full);
+          ptx::mbar_arrive(&sm.p_full[wg]);
         }
         if (kb == nb - 1 && u + (int32_t)gridDim.x < n_units) fetch_stats(u + gridDim.x);  // next unit's stats
         // dK (WG0) / dV (WG1) of key block kb
