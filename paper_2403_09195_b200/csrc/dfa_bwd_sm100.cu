@@ -65,8 +65,8 @@ struct __align__(1024) BwdSmem {
   uint8_t ds[2][kTile];           // dS^T as the MN-major A operand: queries [0,64) | [64,128)
   uint8_t stage[2][kTile];        // output staging (dK | dV, then dQ blocks)
   uint8_t zero[kTile];
-  float lse2[kMaxBlk * kB];       // lse * log2(e) of the view's query rows
-  float dlt[kMaxBlk * kB];        // Delta of the view's query rows
+  float lse2[kMaxBlk * kB];       // -lse * log2(e) of the view's query rows
+  float dlt[kMaxBlk * kB];        // -Delta of the view's query rows
   uint64_t load_full[kMaxBlk], kv_done, q_done;  // load_full[blk]: Q, K, V, dO of 128-row block blk
   uint64_t s_full[2], p_full[2];                 // per query half: S^T / dP^T ready, P^T / dS^T written
   uint32_t tmem_base;
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t_row < nb * kB) {
         const int64_t n = (int64_t)(y.t0 + t_row) * p.r + y.gamma;
         const int64_t off = ((int64_t)y.b * p.h + y.j) * p.N + n;
-        pre_l = lse[off] * kLog2e;
-        pre_d = delta[off];
+        pre_l = -lse[off] * kLog2e;  // negated: the gradient loop adds them with packed FFMA2 / FADD2
+        pre_d = -delta[off];
       }
     };
     fetch_stats(blockIdx.x);
@@ -269,26 +269,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (c == 1) ptx::named_bar_arrive(3, 2 * kB);
             uint32_t pp[16], dd[16];
 #pragma unroll
+            const float2 c2 = make_float2(p.c, p.c);
             for (int e = 0; e < 16; ++e) {
               const int q0 = 32 * c + 2 * e;
-              float p0, p1;
+              // packed pairs: x = s c - lse log2e (FFMA2), dS = P (dP - Delta) (FADD2, FMUL2)
+              const float2 nl = *reinterpret_cast<const float2*>(l2 + q0);
+              const float2 nd = *reinterpret_cast<const float2*>(dl + q0);
+              const float2 x = ptx::ffma2(make_float2(__uint_as_float(s[2 * e]), __uint_as_float(s[2 * e + 1])), c2, nl);
+              float2 pr;
               if ((kBwdPolyMask >> e) & 1u) {  // FMA-pipe exp2 for a share of the pairs (MUFU-bound otherwise)
-                const float2 ex = ptx::ex2_poly2(make_float2(__uint_as_float(s[2 * e]) * p.c - l2[q0],
-                                                             __uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]));
-                p0 = ex.x;
-                p1 = ex.y;
+                pr = ptx::ex2_poly2(x);
               } else {
-                p0 = ptx::ex2(__uint_as_float(s[2 * e]) * p.c - l2[q0]);
-                p1 = ptx::ex2(__uint_as_float(s[2 * e + 1]) * p.c - l2[q0 + 1]);
+                pr = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
               }
               if (p.mseg < kB) {  // packed short segments: no interaction across segments
                 const uint32_t kseg = row / p.mseg;
-                if ((uint32_t)q0 / p.mseg != kseg) p0 = 0.0f;
-                if ((uint32_t)(q0 + 1) / p.mseg != kseg) p1 = 0.0f;
+                if ((uint32_t)q0 / p.mseg != kseg) pr.x = 0.0f;
+                if ((uint32_t)(q0 + 1) / p.mseg != kseg) pr.y = 0.0f;
               }
-              pp[e] = ptx::pack_bf16x2(p0, p1);
-              dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl[q0]),
-                                       p1 * (__uint_as_float(dp[2 * e + 1]) - dl[q0 + 1]));
+              const float2 dsv =
+                  ptx::fmul2(pr, ptx::fadd2(make_float2(__uint_as_float(dp[2 * e]), __uint_as_float(dp[2 * e + 1])), nd));
+              pp[e] = ptx::pack_bf16x2(pr.x, pr.y);
+              dd[e] = ptx::pack_bf16x2(dsv.x, dsv.y);
             }
             if (c == 2) ptx::named_bar_sync(3, 2 * kB);
             ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
