@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const LongView x = long_view(p, u);
       const int64_t n = (int64_t)(x.t0 + qb * kB + (t & 127)) * p.r + x.gamma;
       const int64_t base = ((int64_t)x.b * p.h + x.j) * p.N;
-      return t < 128 ? lse[base + n] * kLog2e : delta[base + n];
+      return t < 128 ? -lse[base + n] * kLog2e : -delta[base + n];  // negated for packed FFMA2 / FADD2
     };
     auto put = [&](int buf, float val) {
       if (t < 128) sm.lse2[buf][t] = val;
@@ -546,14 +546,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld_wait();
           if (c == 1) ptx::named_bar_arrive(3, 2 * kB);  // see dfa_bwd_sm100_kernel
           uint32_t pp[16], dd[16];
+          const float2 c2 = make_float2(p.c, p.c);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          for (int e = 0; e < 16; ++e) {  // packed pairs, as dfa_bwd_sm100_kernel
             const int q0 = 32 * c + 2 * e;
-            const float p0 = ptx::ex2(__uint_as_float(sv[2 * e]) * p.c - sm.lse2[buf][q0]);
-            const float p1 = ptx::ex2(__uint_as_float(sv[2 * e + 1]) * p.c - sm.lse2[buf][q0 + 1]);
-            pp[e] = ptx::pack_bf16x2(p0, p1);
-            dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - sm.dlt[buf][q0]),
-                                     p1 * (__uint_as_float(dp[2 * e + 1]) - sm.dlt[buf][q0 + 1]));
+            const float2 nl = *reinterpret_cast<const float2*>(&sm.lse2[buf][q0]);
+            const float2 nd = *reinterpret_cast<const float2*>(&sm.dlt[buf][q0]);
+            const float2 x =
+                ptx::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), c2, nl);
+            const float2 pr = ((kBwdPolyMask >> e) & 1u) ? ptx::ex2_poly2(x) : make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+            const float2 dsv =
+                ptx::fmul2(pr, ptx::fadd2(make_float2(__uint_as_float(dp[2 * e]), __uint_as_float(dp[2 * e + 1])), nd));
+            pp[e] = ptx::pack_bf16x2(pr.x, pr.y);
+            dd[e] = ptx::pack_bf16x2(dsv.x, dsv.y);
           }
           if (c == 2) ptx::named_bar_sync(3, 2 * kB);
           ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
@@ -724,11 +729,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_ld_wait();
           if (c == 1) ptx::named_bar_arrive(3, 2 * kB);
           uint32_t dd[16];
+          const float2 c2 = make_float2(p.c, p.c), nl = make_float2(-l2, -l2), nd = make_float2(-dl, -dl);
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float p0 = ptx::ex2(__uint_as_float(sv[2 * e]) * p.c - l2);
-            const float p1 = ptx::ex2(__uint_as_float(sv[2 * e + 1]) * p.c - l2);
-            dd[e] = ptx::pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dl), p1 * (__uint_as_float(dp[2 * e + 1]) - dl));
+          for (int e = 0; e < 16; ++e) {  // packed pairs, as dfa_bwd_sm100_kernel
+            const float2 x =
+                ptx::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), c2, nl);
+            const float2 pr = ((kBwdPolyMask >> e) & 1u) ? ptx::ex2_poly2(x) : make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
+            const float2 dsv =
+                ptx::fmul2(pr, ptx::fadd2(make_float2(__uint_as_float(dp[2 * e]), __uint_as_float(dp[2 * e + 1])), nd));
+            dd[e] = ptx::pack_bf16x2(dsv.x, dsv.y);
           }
           if (c == 2) ptx::named_bar_sync(3, 2 * kB);
           ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
