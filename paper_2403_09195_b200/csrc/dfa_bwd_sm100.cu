@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (t_row < nb * kB) {
         const int64_t n = (int64_t)(y.t0 + t_row) * p.r + y.gamma;
         const int64_t off = ((int64_t)y.b * p.h + y.j) * p.N + n;
-        pre_l = -lse[off] * kLog2e;  // negated: the gradient loop adds them with packed FFMA2 / FADD2
-        pre_d = -delta[off];
+        pre_l = lse[off];  // raw: scaled / negated at the smem store, so nothing waits on the load here
+        pre_d = delta[off];
       }
     };
     fetch_stats(blockIdx.x);
@@ -245,8 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const View x = view(u);
       ptx::named_bar_sync(4, 2 * kB);  // previous unit's steps are done with lse2 / dlt
       if (t_row < nb * kB) {
-        sm.lse2[t_row] = pre_l;
-        sm.dlt[t_row] = pre_d;
+        sm.lse2[t_row] = -pre_l * kLog2e;  // negated: the gradient loop adds them with packed FFMA2 / FADD2
+        sm.dlt[t_row] = -pre_d;
       }
       ptx::named_bar_sync(4, 2 * kB);
       for (int kb = 0; kb < nb; ++kb) {
