@@ -186,6 +186,9 @@ struct Sm100Params {
 #ifndef DFA_PROBE_NO_ZERO
 #define DFA_PROBE_NO_ZERO 0
 #endif
+#ifndef DFA_L2_PROMO
+#define DFA_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_NONE  // TMA L2 sector promotion of the t'-stream maps
+#endif
 #ifndef DFA_HEAD_MAJOR
 #define DFA_HEAD_MAJOR 1
 #endif
@@ -837,7 +840,7 @@ bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t 
   cuuint32_t box[5] = {kD, 1, 1, box_rows, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult res = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)DFA_L2_PROMO,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return res == CUDA_SUCCESS;
 }
