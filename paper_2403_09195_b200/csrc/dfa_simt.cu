@@ -282,12 +282,26 @@ int launch_t(const Geometry& g, const void* q, const void* k, const void* v, voi
   bool launched = false;
   if constexpr (DMAX <= 64) {
     if ((int64_t)grid.x * grid.y * grid.z < 2 * 148) {
-      // small grid: 4 lanes per query row -> 4x the CTAs
+      // small grid: 4 lanes per query row -> 4x the CTAs; 8 lanes when even
+      // that leaves SMs idle (config 1: 64 -> 128 CTAs)
       p.n_chunks = (g.m_max + 128 / kSplit - 1) / (128 / kSplit);
       if (p.n_chunks < 1) p.n_chunks = 1;
-      dim3 g2((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
-      simt_split_kernel<T, DMAX, KT, kSplit><<<g2, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o,
-                                                                     lse, p);
+      const int64_t c8 = std::max<int64_t>(1, (g.m_max + 15) / 16);
+      if ((int64_t)g.n_seg * c8 * g.h * g.B < 148 && KT % 16 == 0) {  // 16 lanes per row
+        p.n_chunks = std::max<int64_t>(1, (g.m_max + 7) / 8);
+        dim3 g16((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
+        simt_split_kernel<T, DMAX, KT, 16><<<g16, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o,
+                                                                   lse, p);
+      } else if ((int64_t)g.n_seg * p.n_chunks * g.h * g.B < 148 && KT % 8 == 0) {
+        p.n_chunks = c8;
+        dim3 g8((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
+        simt_split_kernel<T, DMAX, KT, 8><<<g8, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o,
+                                                                 lse, p);
+      } else {
+        dim3 g2((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
+        simt_split_kernel<T, DMAX, KT, kSplit><<<g2, 128, 0, stream>>>((const T*)q, (const T*)k, (const T*)v,
+                                                                       (T*)o, lse, p);
+      }
       launched = true;
     }
   }
