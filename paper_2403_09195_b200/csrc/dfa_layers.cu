@@ -316,11 +316,16 @@ template <typename T>
 __global__ void __launch_bounds__(256) pack_qkv_kernel(const T* __restrict__ wq, const T* __restrict__ wk,
                                                        const T* __restrict__ wv, T* __restrict__ out, int64_t h,
                                                        int64_t D, int64_t d) {
-  const int64_t n = 3 * D * h * d;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = i % d, j = (i / d) % h, which = (i / (d * h)) % 3, c = i / (3 * h * d);
+  // 32-bit index decode (weights are far below 2^31 elements; int64 division
+  // made this tiny pass take ~13 us)
+  const uint32_t ud = (uint32_t)d, uh = (uint32_t)h, uD = (uint32_t)D;
+  const uint32_t n = 3u * uD * uh * ud;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t i1 = i / ud, e = i - i1 * ud;
+    const uint32_t i2 = i1 / uh, j = i1 - i2 * uh;
+    const uint32_t c = i2 / 3u, which = i2 - c * 3u;
     const T* src = which == 0 ? wq : (which == 1 ? wk : wv);
-    out[i] = src[(j * D + c) * d + e];
+    out[i] = src[((size_t)j * uD + c) * ud + e];
   }
 }
 
