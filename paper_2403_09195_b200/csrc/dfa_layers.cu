@@ -20,7 +20,9 @@
 #include <math.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "dfa_internal.h"
 #include "sm100_ptx.cuh"
@@ -401,6 +403,34 @@ cublasLtHandle_t lt_handle() {
 // Row-major D[M, N] (ldd) = A[M, K] (lda) * B[K, N] (ldb) (+ bias[N]) (+ beta * C[M, N] (ldc)),
 // `batch` problems at element strides sa / sb / sc / sd (sa may be 0).
 // Column-major cuBLASLt sees D^T = B^T A^T: m = N, n = M.
+// Per-shape cuBLASLt algorithm cache (see gemm_rowmajor).
+struct GemmKey {
+  int dtype;
+  int64_t M, N, K, lda, ldb, ldd;
+  bool c, bias, gelu;
+  int batch;
+  bool operator<(const GemmKey& o) const {
+    return std::tie(dtype, M, N, K, lda, ldb, ldd, c, bias, gelu, batch) <
+           std::tie(o.dtype, o.M, o.N, o.K, o.lda, o.ldb, o.ldd, o.c, o.bias, o.gelu, o.batch);
+  }
+};
+static std::mutex g_algo_mu;
+static std::map<GemmKey, cublasLtMatmulAlgo_t>& algo_cache() {
+  static std::map<GemmKey, cublasLtMatmulAlgo_t> m;
+  return m;
+}
+static bool cached_algo(const GemmKey& k, cublasLtMatmulAlgo_t* a) {
+  std::lock_guard<std::mutex> lk(g_algo_mu);
+  auto it = algo_cache().find(k);
+  if (it == algo_cache().end()) return false;
+  *a = it->second;
+  return true;
+}
+static void store_algo(const GemmKey& k, const cublasLtMatmulAlgo_t& a) {
+  std::lock_guard<std::mutex> lk(g_algo_mu);
+  algo_cache()[k] = a;
+}
+
 int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
                   int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
                   const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why,
@@ -442,16 +472,59 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
     }
     if (L.cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS) break;
     L.cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes, sizeof(ws_bytes));
-    cublasLtMatmulHeuristicResult_t res;
-    int found = 0;
-    if (L.cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, ld, pref, 1, &res, &found) != CUBLAS_STATUS_SUCCESS ||
-        found == 0) {
-      *why = "no cuBLASLt algorithm for this GEMM";
-      break;
-    }
     const float alpha = 1.0f;
     const float b2 = C ? beta : 0.0f;
-    if (L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res.algo, ws, ws_bytes, stream) !=
+    // Algorithm: cached per GEMM shape / epilogue.  First sight of a shape
+    // times up to kTune heuristic candidates on the caller's stream and keeps
+    // the fastest (cuBLASLt's first pick is not the fastest on several of the
+    // encoder-block shapes); skipped while the stream is being captured, when
+    // C aliases D, or with DFA_GEMM_AUTOTUNE=0.
+    const GemmKey key{dtype, M, N, K, lda, ldb, ldd, C != nullptr, bias != nullptr, gelu, batch};
+    cublasLtMatmulAlgo_t algo;
+    if (!cached_algo(key, &algo)) {
+      constexpr int kTune = 8;
+      cublasLtMatmulHeuristicResult_t res[kTune];
+      int found = 0;
+      if (L.cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, ld, pref, kTune, res, &found) != CUBLAS_STATUS_SUCCESS ||
+          found == 0) {
+        *why = "no cuBLASLt algorithm for this GEMM";
+        break;
+      }
+      int best = 0;
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(stream, &cap);
+      const char* e = getenv("DFA_GEMM_AUTOTUNE");
+      if (found > 1 && cap == cudaStreamCaptureStatusNone && C != D && !(e && e[0] == '0')) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        float best_ms = 1e30f;
+        for (int i = 0; i < found; ++i) {
+          if (res[i].state != CUBLAS_STATUS_SUCCESS) continue;
+          bool good = L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res[i].algo, ws,
+                                       ws_bytes, stream) == CUBLAS_STATUS_SUCCESS;  // warm-up
+          cudaEventRecord(e0, stream);
+          for (int r = 0; good && r < 2; ++r)
+            good = L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res[i].algo, ws,
+                                    ws_bytes, stream) == CUBLAS_STATUS_SUCCESS;
+          cudaEventRecord(e1, stream);
+          cudaEventSynchronize(e1);
+          float ms = 0.0f;
+          if (good && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess && ms < best_ms) {
+            best_ms = ms;
+            best = i;
+          }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGetLastError();
+        store_algo(key, res[best].algo);
+      } else if (cap == cudaStreamCaptureStatusNone) {
+        store_algo(key, res[0].algo);
+      }
+      algo = res[best].algo;
+    }
+    if (L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &algo, ws, ws_bytes, stream) !=
         CUBLAS_STATUS_SUCCESS) {
       *why = "cublasLtMatmul failed";
       break;
