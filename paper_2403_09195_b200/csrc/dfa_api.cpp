@@ -11,6 +11,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "../../include/dfa.h"
 #include "dfa_internal.h"
@@ -611,6 +612,70 @@ static dfa_status_t fused_qkv_attention(const dfa_config_t* cfg, dfa_dtype_t dty
   return DFA_OK;
 }
 
+// Offset-class split of a multi-head layer (bf16, r > 1, r | N, r | w): head j
+// only ever reads rows n = gamma_j (mod r) of its q / k / v, and its attention
+// output is zero on every other row.  Grouping heads by gamma, each class g runs
+//   qkv_g = x[rows = g mod r] W_qkv[class g columns]   (M / r rows)
+//   att_g = core(qkv_g) on the class's t'-streams       (N / r, w / r, r = 1)
+//   out[rows = g mod r] = att_g Wo[class g rows] (+ bias, + C)
+// -- the same result as the dense layer with 1/r of the projection FLOPs and
+// bytes and no zero rows materialised.  qkv holds the classes back to back;
+// the class-major Wo copy sits behind them in the same region (the dense
+// layout needs 3 M D elements there, this one 3 M D / r + D D).
+static bool class_split_ok(const dfa_impl::Geometry& g, dfa_dtype_t dtype) {
+  if (dtype != DFA_BF16 || g.r < 2 || g.N % g.r != 0 || g.w % g.r != 0 || g_path_override.load() == DFA_PATH_SIMT)
+    return false;
+  // the class-major Wo copy must fit behind the classes' qkv in the dense
+  // layout's 3 M D region (not the case for tiny M against a wide model)
+  const size_t es = elem_size(dtype), M = (size_t)(g.B * g.N), D = (size_t)(g.h * g.d);
+  return up256(3 * (M / (size_t)g.r) * D * es) + D * D * es <= 3 * up256(M * D * es);
+}
+
+static dfa_status_t class_split_layer(const dfa_config_t* cfg, dfa_dtype_t dtype, const dfa_impl::Geometry& g,
+                                      const void* x, const void* wq, const void* wk, const void* wv, const void* wo,
+                                      const void* bias, const void* resid, void* out, char* qkv, char* att,
+                                      char* wpack, void* lt, cudaStream_t s, int* launches, const char* who) {
+  const int64_t M = g.B * g.N, D = g.h * g.d, r = g.r, Mr = M / r;
+  const size_t es = elem_size(dtype);
+  char* wopack = qkv + up256((size_t)(3 * Mr * D) * es);
+  *launches += dfa_impl::launch_pack_class(dtype, wq, wk, wv, wo, wpack, wopack, g.h, D, g.d, g.offsets, s);
+  const char* why = "";
+  int64_t start = 0;  // first class-major head position of the class
+  for (int64_t gc = 0; gc < r; ++gc) {
+    int64_t cnt = 0;
+    for (int64_t j = 0; j < g.h; ++j) cnt += g.offsets[j] == gc ? 1 : 0;
+    if (cnt == 0) continue;  // full coverage (validated) makes every class non-empty
+    const int64_t hd = cnt * g.d;
+    char* q_g = qkv + (size_t)(3 * Mr * start * g.d) * es;
+    char* a_g = att + (size_t)(Mr * start * g.d) * es;
+    if (!dfa_impl::gemm_rowmajor(dtype, Mr, 3 * hd, D, static_cast<const char*>(x) + gc * D * es, r * D, 0,
+                                 wpack + (size_t)(3 * start * g.d) * es, 3 * D, 0, q_g, 3 * hd, 0, nullptr, 0, 0.0f,
+                                 nullptr, 1, lt, kLtWorkspace, s, &why))
+      return fail(DFA_ERR_CUDA, "%s: QKV projection (class %lld): %s", who, (long long)gc, why);
+    ++*launches;
+    std::vector<int64_t> zero_offs((size_t)cnt, 0);
+    dfa_config_t cc = *cfg;
+    cc.seq_len = g.N / r;
+    cc.segment_len = g.w / r;
+    cc.interval = 1;
+    cc.num_heads = cnt;
+    cc.head_offsets = zero_offs.data();
+    const int64_t ld[4] = {3 * hd, 3 * hd, 3 * hd, hd};
+    dfa_status_t st = forward_impl(&cc, dtype, g.B, q_g, q_g + hd * es, q_g + 2 * hd * es, a_g, nullptr,
+                                   reinterpret_cast<void*>(s), nullptr, nullptr, false, ld);
+    if (st != DFA_OK) return st;
+    *launches += g_launches;
+    const void* c_g = resid ? static_cast<const char*>(resid) + gc * D * es : nullptr;
+    if (!dfa_impl::gemm_rowmajor(dtype, Mr, D, hd, a_g, hd, 0, wopack + (size_t)(start * g.d * D) * es, D, 0,
+                                 static_cast<char*>(out) + gc * D * es, r * D, 0, c_g, r * D, c_g ? 1.0f : 0.0f,
+                                 bias, 1, lt, kLtWorkspace, s, &why))
+      return fail(DFA_ERR_CUDA, "%s: output projection (class %lld): %s", who, (long long)gc, why);
+    ++*launches;
+    start += cnt;
+  }
+  return DFA_OK;
+}
+
 dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,
                                     const void* wq, const void* wk, const void* wv, const void* wo, void* out,
                                     void* workspace, size_t ws_bytes, void* stream) {
@@ -633,14 +698,21 @@ dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, 
   void* lt = wpack + up256((size_t)(3 * D * D) * es);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int launches = 0;
-  st = fused_qkv_attention(cfg, dtype, g, x, wq, wk, wv, qkv, wpack, att, lt, s, &launches, "multi_head_dilated");
-  if (st != DFA_OK) return st;
-  const char* why = "";
-  if (!dfa_impl::gemm_rowmajor(dtype, M, D, D, att, D, 0, wo, D, 0, out, D, 0, nullptr, 0, 0.0f, nullptr, 1, lt,
-                               kLtWorkspace, s, &why))
-    return fail(DFA_ERR_CUDA, "multi_head_dilated: output projection: %s", why);
+  if (class_split_ok(g, dtype)) {
+    st = class_split_layer(cfg, dtype, g, x, wq, wk, wv, wo, nullptr, nullptr, out, qkv, static_cast<char*>(att),
+                           wpack, lt, s, &launches, "multi_head_dilated");
+    if (st != DFA_OK) return st;
+  } else {
+    st = fused_qkv_attention(cfg, dtype, g, x, wq, wk, wv, qkv, wpack, att, lt, s, &launches, "multi_head_dilated");
+    if (st != DFA_OK) return st;
+    const char* why = "";
+    if (!dfa_impl::gemm_rowmajor(dtype, M, D, D, att, D, 0, wo, D, 0, out, D, 0, nullptr, 0, 0.0f, nullptr, 1, lt,
+                                 kLtWorkspace, s, &why))
+      return fail(DFA_ERR_CUDA, "multi_head_dilated: output projection: %s", why);
+    ++launches;
+  }
   if (g_fault.load()) launches += dfa_impl::launch_perturb(dtype, out, s);
-  g_launches = launches + 1;
+  g_launches = launches;
   return DFA_OK;
 }
 
@@ -737,10 +809,16 @@ dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtyp
                                    kLtWorkspace, s, &why, gelu);
   };
   launches += dfa_impl::launch_layer_norm(dtype, x, wt->ln1_g, wt->ln1_b, ln, M, (int)D, s);
-  st = fused_qkv_attention(cfg, dtype, g, ln, wt->wq, wt->wk, wt->wv, qkv, wpack, att, lt, s, &launches,
-                           "encoder_block");
-  if (st != DFA_OK) return st;
-  if (!gemm(M, D, D, att, wt->wo, x1, x, wt->bo)) return fail(DFA_ERR_CUDA, "encoder_block: wo: %s", why);
+  if (class_split_ok(g, dtype)) {  // x1 = x + attention_mix(LN1 x) Wo + bo, per offset class
+    st = class_split_layer(cfg, dtype, g, ln, wt->wq, wt->wk, wt->wv, wt->wo, wt->bo, x, x1, qkv,
+                           static_cast<char*>(att), wpack, lt, s, &launches, "encoder_block");
+    if (st != DFA_OK) return st;
+  } else {
+    st = fused_qkv_attention(cfg, dtype, g, ln, wt->wq, wt->wk, wt->wv, qkv, wpack, att, lt, s, &launches,
+                             "encoder_block");
+    if (st != DFA_OK) return st;
+    if (!gemm(M, D, D, att, wt->wo, x1, x, wt->bo)) return fail(DFA_ERR_CUDA, "encoder_block: wo: %s", why);
+  }
   launches += dfa_impl::launch_layer_norm(dtype, x1, wt->ln2_g, wt->ln2_b, ln, M, (int)D, s);
   // bf16: GELU (tanh form, within bf16's resolution of the erf form, like
   // gelu_bf16_kernel) in the w1 GEMM's epilogue -- saves a 1.6 GB pass over

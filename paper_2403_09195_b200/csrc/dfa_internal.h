@@ -92,6 +92,10 @@ int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, vo
                       cudaStream_t stream);
 int launch_gelu(int dtype, const void* xin, void* x, int64_t n, cudaStream_t stream);  // x = GELU(xin); may alias
 // wq/wk/wv [h, D, d] -> packed [D, 3, h, d] (one QKV GEMM writes q|k|v per token).
+// Offset-class packing for the class-split multi-head path: q/k/v columns and
+// wo rows in class-major head order (heads grouped by offset).  Returns launches.
+int launch_pack_class(int dtype, const void* wq, const void* wk, const void* wv, const void* wo, void* qkv_out,
+                      void* wo_out, int64_t h, int64_t D, int64_t d, const int32_t* offsets, cudaStream_t stream);
 int launch_pack_qkv(int dtype, const void* wq, const void* wk, const void* wv, void* out, int64_t h, int64_t D,
                     int64_t d, cudaStream_t stream);
 

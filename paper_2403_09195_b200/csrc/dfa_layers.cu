@@ -331,6 +331,47 @@ __global__ void __launch_bounds__(256) pack_qkv_kernel(const T* __restrict__ wq,
   }
 }
 
+// Offset-class packing (multi-head layers with r > 1, see class_split in
+// dfa_api.cpp): heads grouped by gamma_j, class-major.  pos[j] = head j's
+// position in that order, cls[j] its class, start[g] / cnt[g] the classes'
+// first position / size.
+struct ClassPack {
+  int32_t pos[kMaxHeads], cls[kMaxHeads], start[kMaxHeads], cnt[kMaxHeads];
+};
+
+// wq/wk/wv [h, D, d] -> [D, 3 D] with class g's columns [3 d start_g, 3 d (start_g + cnt_g))
+// laid out [3][cnt_g][d]: one GEMM per class writes that class's q | k | v.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_qkv_class_kernel(const T* __restrict__ wq, const T* __restrict__ wk,
+                                                             const T* __restrict__ wv, T* __restrict__ out,
+                                                             uint32_t h, uint32_t D, uint32_t d,
+                                                             const __grid_constant__ ClassPack cp) {
+  const uint32_t n = 3u * D * h * d;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    // source order (c, which, j, e) -- i = ((c * 3 + which) * h + j) * d + e
+    const uint32_t i1 = i / d, e = i - i1 * d;
+    const uint32_t i2 = i1 / h, j = i1 - i2 * h;
+    const uint32_t c = i2 / 3u, which = i2 - c * 3u;
+    const T* src = which == 0 ? wq : (which == 1 ? wk : wv);
+    const uint32_t g = (uint32_t)cp.cls[j], jr = (uint32_t)(cp.pos[j] - cp.start[g]);
+    const uint32_t col = 3u * d * (uint32_t)cp.start[g] + (which * (uint32_t)cp.cnt[g] + jr) * d + e;
+    out[(size_t)c * 3u * D + col] = src[((size_t)j * D + c) * d + e];
+  }
+}
+
+// wo [h d, D] -> rows in class-major head order (row pos_j d + e <- j d + e).
+template <typename T>
+__global__ void __launch_bounds__(256) pack_wo_class_kernel(const T* __restrict__ wo, T* __restrict__ out,
+                                                            uint32_t h, uint32_t D, uint32_t d,
+                                                            const __grid_constant__ ClassPack cp) {
+  const uint32_t n = h * d * D;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t r = i / D, c = i - r * D;
+    const uint32_t j = r / d, e = r - j * d;
+    out[((size_t)cp.pos[j] * d + e) * D + c] = wo[i];
+  }
+}
+
 // cuBLASLt is bound at run time, not linked: if the process already holds a
 // libcublasLt.so.12 (e.g. PyTorch's wheel copy) that one is used, otherwise
 // the CUDA toolkit's is loaded.  Linking it would pin a second copy under the
@@ -578,6 +619,37 @@ int launch_pack_qkv(int dtype, const void* wq, const void* wk, const void* wv, v
     pack_qkv_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)wq, (const __nv_bfloat16*)wk,
                                                              (const __nv_bfloat16*)wv, (__nv_bfloat16*)out, h, D, d);
   return 1;
+}
+
+int launch_pack_class(int dtype, const void* wq, const void* wk, const void* wv, const void* wo, void* qkv_out,
+                      void* wo_out, int64_t h, int64_t D, int64_t d, const int32_t* offsets, cudaStream_t stream) {
+  ClassPack cp{};
+  int32_t r_max = 0;
+  for (int j = 0; j < h; ++j) r_max = std::max(r_max, offsets[j] + 1);
+  int32_t at = 0;
+  for (int32_t g = 0; g < r_max; ++g) {
+    cp.start[g] = at;
+    for (int j = 0; j < h; ++j)
+      if (offsets[j] == g) {
+        cp.pos[j] = at++;
+        cp.cls[j] = g;
+      }
+    cp.cnt[g] = at - cp.start[g];
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>((3 * D * D + 255) / 256, 148 * 8);
+  if (dtype == 0) {
+    pack_qkv_class_kernel<float><<<grid, 256, 0, stream>>>((const float*)wq, (const float*)wk, (const float*)wv,
+                                                           (float*)qkv_out, (uint32_t)h, (uint32_t)D, (uint32_t)d, cp);
+    pack_wo_class_kernel<float><<<grid, 256, 0, stream>>>((const float*)wo, (float*)wo_out, (uint32_t)h, (uint32_t)D,
+                                                          (uint32_t)d, cp);
+  } else {
+    using B = __nv_bfloat16;
+    pack_qkv_class_kernel<B><<<grid, 256, 0, stream>>>((const B*)wq, (const B*)wk, (const B*)wv, (B*)qkv_out,
+                                                       (uint32_t)h, (uint32_t)D, (uint32_t)d, cp);
+    pack_wo_class_kernel<B><<<grid, 256, 0, stream>>>((const B*)wo, (B*)wo_out, (uint32_t)h, (uint32_t)D,
+                                                      (uint32_t)d, cp);
+  }
+  return 2;
 }
 
 int launch_gelu(int dtype, const void* xin, void* x, int64_t n, cudaStream_t stream) {

@@ -105,3 +105,32 @@ def test_encoder_block_vs_reference(dfa, ref, cuda, n, h, d, w, r, B, dtype):
     for b in range(B):
         want = ref.encoder_block(x[b], p, h, w, r)
         _check(got[b], want, dtype)
+
+
+@pytest.mark.parametrize("n,h,w,r,offsets", [
+    (512, 4, 128, 2, [1, 0, 0, 1]),          # classes not in head order
+    (512, 3, 128, 2, [0, 0, 1]),             # uneven classes (2 + 1 heads)
+    (1024, 8, 512, 4, [3, 2, 1, 0, 0, 1, 2, 3]),
+    (768, 6, 256, 2, [0, 1, 0, 1, 0, 1]),
+])
+def test_multi_head_offset_classes_bf16(dfa, ref, cuda, n, h, w, r, offsets):
+    """The bf16 layer runs per offset class (heads grouped by gamma_j, 1/r of
+    the projection work, csrc/dfa_api.cpp class_split_layer): any assignment
+    of heads to classes with full coverage matches the reference."""
+    import torch
+
+    d, B = 64, 2
+    D = h * d
+    x = rand((B, n, D), 61)
+    ws = [rand((h, D, d), 62 + i) / np.sqrt(D) for i in range(3)]
+    wo = rand((D, D), 65) / np.sqrt(D)
+    td = torch.bfloat16
+    x, wo = _round(x, td), _round(wo, td)
+    ws = [_round(a, td) for a in ws]
+    cfg = dfa.AttentionConfig(n, w, r, h, d, offsets)
+    out = dfa.multi_head_dilated(_dev(x, td), *[_dev(a, td) for a in ws], _dev(wo, td), cfg)
+    torch.cuda.synchronize()
+    got = out.double().cpu().numpy()
+    for b in range(B):
+        want = ref.multi_head_dilated(x[b], ws[0], ws[1], ws[2], wo, w, r, offsets)
+        _check(got[b], want, "bf16")
