@@ -98,7 +98,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define DFA_RESCALE_THR 8.0f
 #endif
 #ifndef DFA_POLY_MASK
-#define DFA_POLY_MASK 0x8888u
+#define DFA_POLY_MASK 0x0888u
 #endif
 constexpr float kRescaleThreshold = DFA_RESCALE_THR;  // log2 units: p <= 2^8 between rescales
 #ifndef DFA_SUMCHECK
@@ -109,7 +109,8 @@ constexpr float kRescaleThreshold = DFA_RESCALE_THR;  // log2 units: p <= 2^8 be
 constexpr float kSumBound = 256.0f;
 // bit e: pair e of each 16-pair (32-column) chunk uses the FMA-pipe exp2
 // polynomial instead of MUFU.EX2 (balances the MUFU and FMA/issue pipes;
-// measured: 4 of 16 beats 0, 2, 5, 6, 7 and 8 of 16)
+// measured with the 192-register softmax: 3 of 16 (pairs 3, 7, 11) beats
+// 2 and 4 of 16 by 1-3% and 6 of 16 by 5-8%)
 constexpr uint32_t kPolyMask = DFA_POLY_MASK;
 
 // Geometry of one work unit, identical in every role.
