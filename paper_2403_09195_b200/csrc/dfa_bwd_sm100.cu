@@ -213,6 +213,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = warp % 4 == 0 && lane == 0;
     const uint32_t bar_id = 1 + wg;
     uint32_t step = 0, kvn = 0;
+    // The leader's last bulk-store group was zero boxes only (they read the
+    // zero tile, not the staging tile): a staging reuse then needs all but
+    // that one group to have finished reading.
+    bool zeros_last = false;
+    auto wait_stage = [&]() {
+      if (leader) {
+        if (zeros_last) ptx::tma_store_wait_read<1>();
+        else ptx::tma_store_wait_read<0>();
+      }
+    };
     auto stage_store = [&](uint8_t* st, const uint32_t (&v)[2][32], float mul) {
       const uint32_t a0 = ptx::smem_u32(st);
 #pragma unroll
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++kvn;
         ptx::tc_fence_after();
         uint32_t a[2][32];
-        if (leader) ptx::tma_store_wait_read<0>();
+        wait_stage();
         ptx::named_bar_sync(bar_id, 128);
         const uint32_t col = wg == 0 ? cDK : cDV;
         ptx::tmem_ld32(tbase + lane_base + col, a[0]);
@@ -330,20 +340,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int32_t tb = x.t0 + kb * kB;
           const CUtensorMap* mo = wg == 0 ? &tm_dk : &tm_dv;
           ptx::tma_store_5d(mo, sm.stage[wg], 0, x.j, x.gamma, tb, x.b);
-          for (int32_t gz = 0; gz < p.r; ++gz)
-            if (gz != x.gamma) {
-              ptx::tma_store_5d(mo, sm.zero, 0, x.j, gz, tb, x.b);
-              if (wg == 0) ptx::tma_store_5d(&tm_dq, sm.zero, 0, x.j, gz, tb, x.b);
-            }
-          ptx::tma_store_commit();
+          ptx::tma_store_commit();  // the staging tile's group
+          if (p.r > 1) {
+            for (int32_t gz = 0; gz < p.r; ++gz)
+              if (gz != x.gamma) {
+                ptx::tma_store_5d(mo, sm.zero, 0, x.j, gz, tb, x.b);
+                if (wg == 0) ptx::tma_store_5d(&tm_dq, sm.zero, 0, x.j, gz, tb, x.b);
+              }
+            ptx::tma_store_commit();  // zero boxes
+          }
         }
+        zeros_last = p.r > 1;
       }
       // dQ blocks (TMEM lanes = query rows), alternating between the warpgroups
       wait(&sm.q_done, it & 1);
       ptx::tc_fence_after();
       for (int qb = wg; qb < nb; qb += 2) {
         uint32_t a[2][32];
-        if (leader) ptx::tma_store_wait_read<0>();
+        wait_stage();
         ptx::named_bar_sync(bar_id, 128);
         ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb, a[0]);
         ptx::tmem_ld32(tbase + lane_base + cDQ + 64 * qb + 32, a[1]);
@@ -356,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tma_store_5d(&tm_dq, sm.stage[wg], 0, x.j, x.gamma, x.t0 + qb * kB, x.b);
           ptx::tma_store_commit();
         }
+        zeros_last = false;
       }
     }
     if (leader) ptx::tma_store_wait_all<0>();
