@@ -851,6 +851,7 @@ bool bwd_sm100_supported(const Geometry& g, int dtype, const void* const* ptrs, 
 int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void* v, const void* dout,
                      const float* lse, const float* delta, void* dq, void* dk, void* dv, cudaStream_t stream,
                      cudaError_t* err, const char** why) {
+  ensure_context();
   CUtensorMap mq, mk, mv, mg, mdq, mdk, mdv;
   if (!map5(&mq, q, g) || !map5(&mk, k, g) || !map5(&mv, v, g) || !map5(&mg, dout, g) || !map5(&mdq, dq, g) ||
       !map5(&mdk, dk, g) || !map5(&mdv, dv, g)) {

@@ -20,6 +20,18 @@ struct Geometry {
   int32_t offsets[kMaxHeads];
 };
 
+// Bind the device's primary context to the calling thread (once per thread)
+// before driver-API calls such as cuTensorMapEncodeTiled: a thread whose first
+// CUDA call is one of those (e.g. PyTorch's autograd worker running a
+// backward) has no current context otherwise.
+inline void ensure_context() {
+  static thread_local bool bound = false;
+  if (!bound) {
+    cudaFree(nullptr);
+    bound = true;
+  }
+}
+
 // Launch with the programmatic-stream-serialization attribute (PDL): the
 // kernel's prologue may overlap the previous kernel in the stream; kernels
 // launched this way call griddepcontrol.wait before touching global memory.

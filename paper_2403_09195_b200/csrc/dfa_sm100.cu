@@ -879,6 +879,7 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace,
                  unsigned long long* watchdog, bool merge) {
+  ensure_context();
   if (merge && !lse) {
     *why = "merge mode needs the running lse buffer";
     *err = cudaErrorInvalidValue;

@@ -543,6 +543,7 @@ int64_t sm100_v2_units(const Geometry& g) {
 
 int launch_sm100_v2(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                     cudaStream_t stream, cudaError_t* err, const char** why) {
+  ensure_context();
   CUtensorMap mq, mk, mv, mo;
   if (!map5(&mq, q, g, g.ldq, kBM) || !map5(&mk, k, g, g.ldk, kBN) || !map5(&mv, v, g, g.ldv, kBN) ||
       !map5(&mo, o, g, g.ldo, kBM)) {

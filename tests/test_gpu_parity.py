@@ -465,3 +465,36 @@ def test_v2_four_slot_kernel_vs_oracle(dfa, port, cuda, n, w, r, h, monkeypatch)
     monkeypatch.setenv("DFA_FWD_KERNEL", "v2")
     mx, rel = _bf16_case(dfa, port, 2, n, w, r, h, 3 * n + w)
     assert mx <= BF16_MAX_ABS and rel <= BF16_MEAN_REL, (mx, rel)
+
+
+def test_forward_and_backward_from_a_fresh_thread(dfa, cuda):
+    """The tcgen05 launchers encode TMA descriptors with the driver API; a
+    thread whose first CUDA call that is (e.g. PyTorch's autograd worker)
+    must still get the device's context (ensure_context)."""
+    import threading
+
+    torch = _torch()
+    cfg = make_cfg(dfa, 1024, 256, 2, 2, 64)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v, do = (torch.randn((1, 1024, 2, 64), generator=g, device="cuda", dtype=torch.bfloat16) for _ in range(4))
+    L = torch.empty((1, 2, 1024), dtype=torch.float32, device="cuda")
+    ref = dfa.dfa_forward(q, k, v, cfg, lse=L)
+    ref_g = dfa.dfa_backward(q, k, v, ref, L, do, cfg)
+    torch.cuda.synchronize()
+    out = {}
+
+    def work():
+        try:
+            out["o"] = dfa.dfa_forward(q, k, v, cfg)
+            out["g"] = dfa.dfa_backward(q, k, v, ref, L, do, cfg)
+            torch.cuda.synchronize()
+        except Exception as e:  # surfaced below
+            out["err"] = e
+
+    t = threading.Thread(target=work)
+    t.start()
+    t.join()
+    assert "err" not in out, out.get("err")
+    assert torch.equal(out["o"], ref)
+    for a, b in zip(out["g"], ref_g):
+        assert torch.equal(a, b)
