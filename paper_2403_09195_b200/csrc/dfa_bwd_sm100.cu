@@ -105,18 +105,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     v.t0 = seg * p.m;  // first t' of the view
     return v;
   };
-  // Q, K, V, dO of unit u (the forward's t'-stream boxes) -> smem, one barrier
-  auto issue_loads = [&](int32_t u) {
+  // Q, K, V, dO of unit u (the forward's t'-stream boxes) -> smem, one
+  // barrier per 128-row block.  Views of one block (m <= 128, nb = 1) leave
+  // the second block's tiles free: units alternate between the two (slot
+  // `sl`), so the next unit's loads go out while this unit computes.
+  auto issue_loads = [&](int32_t u, int sl) {
     const View x = view(u);
     const uint64_t pol = ptx::policy_evict_first();
     for (int blk = 0; blk < nb; ++blk) {  // block 0 first: the unit's first step needs only it
       const int32_t tb = x.t0 + blk * kB;
-      uint64_t* bar = &sm.load_full[blk];
+      const int t = blk + sl;
+      uint64_t* bar = &sm.load_full[t];
       ptx::mbar_arrive_expect_tx(bar, 4 * kTile);
-      ptx::tma_load_5d(sm.q[blk], &tm_q, bar, 0, x.j, x.gamma, tb, x.b, pol);
-      ptx::tma_load_5d(sm.k[blk], &tm_k, bar, 0, x.j, x.gamma, tb, x.b, pol);
-      ptx::tma_load_5d(sm.v[blk], &tm_v, bar, 0, x.j, x.gamma, tb, x.b, pol);
-      ptx::tma_load_5d(sm.g[blk], &tm_g, bar, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.q[t], &tm_q, bar, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.k[t], &tm_k, bar, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.v[t], &tm_v, bar, 0, x.j, x.gamma, tb, x.b, pol);
+      ptx::tma_load_5d(sm.g[t], &tm_g, bar, 0, x.j, x.gamma, tb, x.b, pol);
     }
   };
 
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(&sm.kv_done, 1);
     ptx::mbar_init(&sm.q_done, 1);
     ptx::fence_barrier_init();
-    issue_loads(blockIdx.x);  // the first unit's loads go out before anything else
+    issue_loads(blockIdx.x, 0);  // the first unit's loads go out before anything else
   } else if (warp == 1) {
     ptx::tmem_alloc<512>(&sm.tmem_base);
   }
@@ -150,19 +154,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dsd = ptx::sdesc_sw128(ptx::smem_u32(sm.ds[0]), 1024, kTile);  // LBO: next 64 queries
       uint32_t step = 0;
       int it = 0;
+      // One-block views: operands double-buffered across units.  Measured: -16%
+      // at r = 2; at r >= 4 the units are dominated by the zero-box stores and
+      // the extra loads in flight cost 2-8%, so they keep the single buffer.
+      const bool dbl = nb == 1 && p.r <= 2;
       for (int32_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-        wait(&sm.load_full[0], it & 1);
+        const int sl = dbl ? (it & 1) : 0;
+        wait(&sm.load_full[sl], dbl ? ((it >> 1) & 1) : (it & 1));
         ptx::tc_fence_after();
+        if (dbl && u + (int32_t)gridDim.x < n_units) {
+          // the other slot held unit it-1, whose MMAs are done once q_done(it-1) fired
+          if (it > 0) wait(&sm.q_done, (it - 1) & 1);
+          issue_loads(u + gridDim.x, sl ^ 1);
+        }
         for (int kb = 0; kb < nb; ++kb) {
-          const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k[kb]));
-          const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v[kb]));
+          const uint64_t kd = ptx::sdesc_sw128(ptx::smem_u32(sm.k[kb + sl]));
+          const uint64_t vd = ptx::sdesc_sw128(ptx::smem_u32(sm.v[kb + sl]));
           for (int qb = 0; qb < nb; ++qb, ++step) {
             if (kb == 0 && qb == 1) {  // first step touching block 1 (Q1, dO1; K1, V1 follow)
               wait(&sm.load_full[1], it & 1);
               ptx::tc_fence_after();
             }
-            const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[qb]));
-            const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[qb]));
+            const uint64_t qd = ptx::sdesc_sw128(ptx::smem_u32(sm.q[qb + sl]));
+            const uint64_t gd = ptx::sdesc_sw128(ptx::smem_u32(sm.g[qb + sl]));
             // S^T / dP^T in two query halves (N = 64; the half's Q / dO rows
             // start 64 x 128 B into the tile): gradient warpgroup hf starts
             // on its half while the other half's products are still running
@@ -196,9 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_commit(&sm.q_done);
         // the unit's operands are free once its MMAs complete: the next
         // unit's loads overlap this unit's dQ epilogue and output stores
-        if (u + (int32_t)gridDim.x < n_units) {
+        if (!dbl && u + (int32_t)gridDim.x < n_units) {
           wait(&sm.q_done, it & 1);
-          issue_loads(u + gridDim.x);
+          issue_loads(u + gridDim.x, 0);
         }
       }
     }
