@@ -69,6 +69,7 @@ struct __align__(1024) BwdSmem {
   float dlt[kMaxBlk * kB];        // -Delta of the view's query rows
   uint64_t load_full[kMaxBlk], kv_done, q_done;  // load_full[blk]: Q, K, V, dO of 128-row block blk
   uint64_t s_full[2], p_full[2];                 // per query half: S^T / dP^T ready, P^T / dS^T written
+  uint64_t blk0_free;  // two-block views: every MMA reading block 0 (steps up to (1, 0)) completed
   uint32_t tmem_base;
 };
 
@@ -109,10 +110,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // barrier per 128-row block.  Views of one block (m <= 128, nb = 1) leave
   // the second block's tiles free: units alternate between the two (slot
   // `sl`), so the next unit's loads go out while this unit computes.
-  auto issue_loads = [&](int32_t u, int sl) {
+  auto issue_loads = [&](int32_t u, int sl, int b0 = 0, int b1 = -1) {
     const View x = view(u);
     const uint64_t pol = ptx::policy_evict_first();
-    for (int blk = 0; blk < nb; ++blk) {  // block 0 first: the unit's first step needs only it
+    if (b1 < 0) b1 = nb;
+    for (int blk = b0; blk < b1; ++blk) {  // block 0 first: the unit's first step needs only it
       const int32_t tb = x.t0 + blk * kB;
       const int t = blk + sl;
       uint64_t* bar = &sm.load_full[t];
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0 && lane == 0) {
     for (int blk = 0; blk < kMaxBlk; ++blk) ptx::mbar_init(&sm.load_full[blk], 1);
+    ptx::mbar_init(&sm.blk0_free, 1);
     for (int hf = 0; hf < 2; ++hf) {
       ptx::mbar_init(&sm.s_full[hf], 1);
       ptx::mbar_init(&sm.p_full[hf], kB);
@@ -158,6 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // at r = 2; at r >= 4 the units are dominated by the zero-box stores and
       // the extra loads in flight cost 2-8%, so they keep the single buffer.
       const bool dbl = nb == 1 && p.r <= 2;
+      // Two-block views (r <= 2, same measurement): block 0 of the next unit
+      // is loaded as soon as its last reader (step (1, 0)) has completed.
+      const bool early0 = nb == 2 && p.r <= 2;
       for (int32_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
         const int sl = dbl ? (it & 1) : 0;
         wait(&sm.load_full[sl], dbl ? ((it >> 1) & 1) : (it & 1));
@@ -189,6 +195,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               ptx::tc_commit(&sm.s_full[hf]);
             }
+            if (early0 && kb == 1 && qb == 1 && u + (int32_t)gridDim.x < n_units) {
+              // block 0 of the next unit loads under this unit's last step
+              wait(&sm.blk0_free, it & 1);
+              issue_loads(u + gridDim.x, 0, 0, 1);
+            }
             // dV / dK per half as soon as that warpgroup has written P^T / dS^T
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
@@ -204,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < kB / 16; ++kk)  // K-step of 16 keys: 16 rows of dS / K
               ptx::mma_ss(tbase + cDQ + 64 * qb, dsd + kk * 128, kd + kk * 128, id_dq, (kb > 0 || kk > 0) ? 1u : 0u);
+            if (early0 && kb == 1 && qb == 0) ptx::tc_commit(&sm.blk0_free);  // last reader of Q0 / dO0 / K0 / V0
           }
           ptx::tc_commit(&sm.kv_done);
         }
@@ -212,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // unit's loads overlap this unit's dQ epilogue and output stores
         if (!dbl && u + (int32_t)gridDim.x < n_units) {
           wait(&sm.q_done, it & 1);
-          issue_loads(u + gridDim.x, 0);
+          issue_loads(u + gridDim.x, 0, early0 ? 1 : 0);  // early0: block 0 went out already
         }
       }
     }
