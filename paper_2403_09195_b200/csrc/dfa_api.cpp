@@ -640,6 +640,40 @@ static dfa_status_t class_split_layer(const dfa_config_t* cfg, dfa_dtype_t dtype
   char* wopack = qkv + up256((size_t)(3 * Mr * D) * es);
   *launches += dfa_impl::launch_pack_class(dtype, wq, wk, wv, wo, wpack, wopack, g.h, D, g.d, g.offsets, s);
   const char* why = "";
+  bool equal = g.h % r == 0;  // every class holds h / r heads (e.g. spread offsets j mod r)
+  for (int64_t gc = 0; equal && gc < r; ++gc) {
+    int64_t cnt = 0;
+    for (int64_t j = 0; j < g.h; ++j) cnt += g.offsets[j] == gc ? 1 : 0;
+    equal = cnt == g.h / r;
+  }
+  if (equal) {
+    // Equal classes: the r classes' buffers lie back to back, so each stage is
+    // ONE call -- a strided-batched GEMM over the classes (A rows offset by the
+    // class, weight columns / rows by the class's block) and one core launch
+    // with batch r B (class-major images): fuller waves than r separate calls.
+    const int64_t hd = (g.h / r) * g.d;
+    if (!dfa_impl::gemm_rowmajor(dtype, Mr, 3 * hd, D, x, r * D, D, wpack, 3 * D, 3 * hd, qkv, 3 * hd, Mr * 3 * hd,
+                                 nullptr, 0, 0.0f, nullptr, (int)r, lt, kLtWorkspace, s, &why))
+      return fail(DFA_ERR_CUDA, "%s: QKV projection: %s", who, why);
+    ++*launches;
+    std::vector<int64_t> zero_offs((size_t)(g.h / r), 0);
+    dfa_config_t cc = *cfg;
+    cc.seq_len = g.N / r;
+    cc.segment_len = g.w / r;
+    cc.interval = 1;
+    cc.num_heads = g.h / r;
+    cc.head_offsets = zero_offs.data();
+    const int64_t ld[4] = {3 * hd, 3 * hd, 3 * hd, hd};
+    dfa_status_t st = forward_impl(&cc, dtype, g.B * r, qkv, qkv + hd * es, qkv + 2 * hd * es, att, nullptr,
+                                   reinterpret_cast<void*>(s), nullptr, nullptr, false, ld);
+    if (st != DFA_OK) return st;
+    *launches += g_launches;
+    if (!dfa_impl::gemm_rowmajor(dtype, Mr, D, hd, att, hd, Mr * hd, wopack, D, hd * D, out, r * D, D, resid, r * D,
+                                 resid ? 1.0f : 0.0f, bias, (int)r, lt, kLtWorkspace, s, &why))
+      return fail(DFA_ERR_CUDA, "%s: output projection: %s", who, why);
+    ++*launches;
+    return DFA_OK;
+  }
   int64_t start = 0;  // first class-major head position of the class
   for (int64_t gc = 0; gc < r; ++gc) {
     int64_t cnt = 0;
