@@ -85,7 +85,7 @@ def _block_weights(D, h, hidden, seed):
 
 
 @pytest.mark.parametrize("n,h,d,w,r,B", [(256, 2, 64, 64, 2, 2), (1024, 6, 64, 256, 2, 1), (64, 4, 16, 16, 2, 1),
-                                        (256, 12, 64, 64, 2, 1)])
+                                        (256, 12, 64, 64, 2, 1), (256, 4, 64, 64, 4, 2)])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_encoder_block_vs_reference(dfa, ref, cuda, n, h, d, w, r, B, dtype):
     import torch
