@@ -244,38 +244,56 @@ def last_launch_count() -> int:
     return int(lib.dfa_last_launch_count())
 
 
+def _check_qkv(q, k, v, cfg: AttentionConfig, who: str):
+    """Shape / dtype / device checks shared by every device entry point (the
+    C-ABI trusts cfg for sizes, so a mismatch here would read or write out of
+    bounds instead of raising).  Returns (B, N, h, d, d_v)."""
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not t.is_cuda:
+            raise DimensionError(f"{who}: {name} is not a CUDA tensor (no CPU path)")
+        if t.dim() != 4:
+            raise DimensionError(f"{who}: {name} must be [B, N, h, d], got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise DimensionError(f"{who}: {name} must be contiguous")
+        if t.device != q.device:
+            raise DimensionError(f"{who}: q, k, v are on different devices")
+    B, N, h, d = q.shape
+    dv = v.shape[3]
+    if tuple(k.shape) != (B, N, h, d):
+        raise DimensionError(f"{who}: query/key shape mismatch {tuple(q.shape)} vs {tuple(k.shape)}")
+    if tuple(v.shape[:3]) != (B, N, h):
+        raise DimensionError(f"{who}: key/value shape mismatch {tuple(k.shape)} vs {tuple(v.shape)}")
+    if q.dtype != k.dtype or q.dtype != v.dtype:
+        raise DimensionError(f"{who}: q, k, v dtypes differ")
+    if N != cfg.seq_len:
+        raise DimensionError(f"{who}: expected {cfg.seq_len} rows, got {N}")
+    if h != cfg.num_heads or len(cfg.head_offsets) != h:
+        raise ConfigError(f"attention: {len(cfg.head_offsets)} offsets for {h} heads")
+    if d != cfg.head_dim:
+        raise DimensionError(f"{who}: head_dim {cfg.head_dim} but q has width {d}")
+    return B, N, h, d, dv
+
+
+def _check_buffer(t, shape, dtype, device, who: str, name: str):
+    """A caller-supplied output / gradient buffer: exact shape, dtype, device, contiguous."""
+    if (tuple(t.shape) != tuple(shape) or t.dtype != dtype or not t.is_cuda or t.device != device
+            or not t.is_contiguous()):
+        raise DimensionError(f"{who}: {name} must be a contiguous {dtype} CUDA tensor of shape {tuple(shape)} "
+                             f"on {device}, got {tuple(t.shape)} {t.dtype} on {t.device}")
+
+
 def dfa_forward(q, k, v, cfg: AttentionConfig, out=None, lse=None, stream=None):
     """Batched multi-head forward: q, k [B, N, h, d], v [B, N, h, d_v] (CUDA,
     contiguous, float32 or bfloat16) -> o [B, N, h, d_v].  Head j uses offset
     cfg.head_offsets[j].  `lse`: optional float32 [B, h, N] output tensor."""
     torch = _torch()
-    for name, t in (("q", q), ("k", k), ("v", v)):
-        if not t.is_cuda:
-            raise DimensionError(f"dfa_forward: {name} is not a CUDA tensor (no CPU path)")
-        if t.dim() != 4:
-            raise DimensionError(f"dfa_forward: {name} must be [B, N, h, d], got {tuple(t.shape)}")
-        if not t.is_contiguous():
-            raise DimensionError(f"dfa_forward: {name} must be contiguous")
-    B, N, h, d = q.shape
-    dv = v.shape[3]
-    if tuple(k.shape) != (B, N, h, d):
-        raise DimensionError(f"dfa_forward: query/key shape mismatch {tuple(q.shape)} vs {tuple(k.shape)}")
-    if tuple(v.shape[:3]) != (B, N, h):
-        raise DimensionError(f"dfa_forward: key/value shape mismatch {tuple(k.shape)} vs {tuple(v.shape)}")
-    if q.dtype != k.dtype or q.dtype != v.dtype:
-        raise DimensionError("dfa_forward: q, k, v dtypes differ")
-    if N != cfg.seq_len:
-        raise DimensionError(f"dfa_forward: expected {cfg.seq_len} rows, got {N}")
-    if h != cfg.num_heads or len(cfg.head_offsets) != h:
-        raise ConfigError(f"attention: {len(cfg.head_offsets)} offsets for {h} heads")
-    if d != cfg.head_dim:
-        raise DimensionError(f"dfa_forward: head_dim {cfg.head_dim} but q has width {d}")
+    B, N, h, d, dv = _check_qkv(q, k, v, cfg, "dfa_forward")
     if out is None:
         out = torch.empty((B, N, h, dv), dtype=q.dtype, device=q.device)
-    elif tuple(out.shape) != (B, N, h, dv) or out.dtype != q.dtype or not out.is_contiguous():
-        raise DimensionError("dfa_forward: bad output tensor")
-    if lse is not None and (tuple(lse.shape) != (B, h, N) or lse.dtype != torch.float32 or not lse.is_contiguous()):
-        raise DimensionError("dfa_forward: lse must be float32 [B, h, N]")
+    else:
+        _check_buffer(out, (B, N, h, dv), q.dtype, q.device, "dfa_forward", "out")
+    if lse is not None:
+        _check_buffer(lse, (B, h, N), torch.float32, q.device, "dfa_forward", "lse")
     c = cfg._c()
     c.value_dim = dv
     _check(lib.dfa_forward(ctypes.byref(c), _dtype_code(q), B, q.data_ptr(), k.data_ptr(), v.data_ptr(),
@@ -290,7 +308,18 @@ def dfa_forward_strided(qkv, cfg: AttentionConfig, out=None, lse=None, stream=No
     if not qkv.is_cuda or not qkv.is_contiguous() or qkv.dim() != 5 or qkv.shape[2] != 3:
         raise DimensionError("dfa_forward_strided: qkv must be a contiguous CUDA [B, N, 3, h, d] tensor")
     B, N, _, h, d = qkv.shape
-    out = torch.empty((B, N, h, d), dtype=qkv.dtype, device=qkv.device) if out is None else out
+    if N != cfg.seq_len:
+        raise DimensionError(f"dfa_forward_strided: expected {cfg.seq_len} rows, got {N}")
+    if h != cfg.num_heads or len(cfg.head_offsets) != h:
+        raise ConfigError(f"attention: {len(cfg.head_offsets)} offsets for {h} heads")
+    if d != cfg.head_dim:
+        raise DimensionError(f"dfa_forward_strided: head_dim {cfg.head_dim} but qkv has width {d}")
+    if out is None:
+        out = torch.empty((B, N, h, d), dtype=qkv.dtype, device=qkv.device)
+    else:
+        _check_buffer(out, (B, N, h, d), qkv.dtype, qkv.device, "dfa_forward_strided", "out")
+    if lse is not None:
+        _check_buffer(lse, (B, h, N), torch.float32, qkv.device, "dfa_forward_strided", "lse")
     c = cfg._c()
     es = qkv.element_size()
     base = qkv.data_ptr()
@@ -398,12 +427,13 @@ def dfa_forward_multibranch(q, k, v, cfg: AttentionConfig, branches, out=None, l
     `branches`: list of (w, r) or (w, r, head_offsets); offsets default to
     j mod r.  cfg supplies N, h, d, scale_scores.  Returns o [B, N, h, d_v]."""
     torch = _torch()
-    B, N, h, d = q.shape
-    dv = v.shape[3]
+    B, N, h, d, dv = _check_qkv(q, k, v, cfg, "dfa_forward_multibranch")
     bs, keep = [], []
     for br in branches:
         w, r = br[0], br[1]
         offs = list(br[2]) if len(br) > 2 else AttentionConfig.spread_offsets(h, r)
+        if len(offs) != h:
+            raise ConfigError(f"attention: {len(offs)} offsets for {h} heads (branch w={w}, r={r})")
         arr = (ctypes.c_int64 * h)(*offs)
         keep.append(arr)
         bs.append(_lib.DfaBranch(w, r, ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64))))
@@ -417,6 +447,10 @@ def dfa_forward_multibranch(q, k, v, cfg: AttentionConfig, branches, out=None, l
         workspace = torch.empty(need.value, dtype=torch.uint8, device=q.device)
     if out is None:
         out = torch.empty((B, N, h, dv), dtype=q.dtype, device=q.device)
+    else:
+        _check_buffer(out, (B, N, h, dv), q.dtype, q.device, "dfa_forward_multibranch", "out")
+    if lse is not None:
+        _check_buffer(lse, (B, h, N), torch.float32, q.device, "dfa_forward_multibranch", "lse")
     _check(lib.dfa_forward_multibranch(ctypes.byref(c), len(bs), barr, code, B, q.data_ptr(), k.data_ptr(),
                                        v.data_ptr(), out.data_ptr(), lse.data_ptr() if lse is not None else None,
                                        workspace.data_ptr(), workspace.numel(), _stream_ptr(stream)))
@@ -451,18 +485,16 @@ def dfa_backward(q, k, v, o, lse, do, cfg: AttentionConfig, dq=None, dk=None, dv
     the reference's tape for the dilated branch of attention_mix,
     encoder.hpp:204-219)."""
     torch = _torch()
-    B, N, h, d = q.shape
-    dvd = v.shape[3]
-    for name, t in (("q", q), ("k", k), ("v", v), ("o", o), ("do", do), ("lse", lse)):
-        if not t.is_cuda or not t.is_contiguous():
-            raise DimensionError(f"dfa_backward: {name} must be a contiguous CUDA tensor")
-    if tuple(o.shape) != (B, N, h, dvd) or tuple(do.shape) != (B, N, h, dvd):
-        raise DimensionError("dfa_backward: o / do must be [B, N, h, d_v]")
-    if tuple(lse.shape) != (B, h, N) or lse.dtype != torch.float32:
-        raise DimensionError("dfa_backward: lse must be float32 [B, h, N]")
+    B, N, h, d, dvd = _check_qkv(q, k, v, cfg, "dfa_backward")
+    _check_buffer(o, (B, N, h, dvd), q.dtype, q.device, "dfa_backward", "o")
+    _check_buffer(do, (B, N, h, dvd), q.dtype, q.device, "dfa_backward", "do")
+    _check_buffer(lse, (B, h, N), torch.float32, q.device, "dfa_backward", "lse")
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
+    _check_buffer(dq, tuple(q.shape), q.dtype, q.device, "dfa_backward", "dq")
+    _check_buffer(dk, tuple(k.shape), q.dtype, q.device, "dfa_backward", "dk")
+    _check_buffer(dv, tuple(v.shape), q.dtype, q.device, "dfa_backward", "dv")
     c = cfg._c()
     c.value_dim = dvd
     need = ctypes.c_size_t(0)

@@ -93,21 +93,6 @@ dfa_status_t resolve(const dfa_config_t* c, int64_t batch, dfa_impl::Geometry* g
   return DFA_OK;
 }
 
-// Forward kernel of the tcgen05 path: DFA_FWD_KERNEL=v1 / v2 forces one
-// (measurement and tests); default "auto".
-int fwd_kernel_choice() {
-  const char* e = getenv("DFA_FWD_KERNEL");  // read per call: scripts flip it between runs
-  if (e && strcmp(e, "v1") == 0) return 1;
-  if (e && strcmp(e, "v2") == 0) return 2;
-  return 0;
-}
-bool use_v2(const dfa_impl::Geometry& g) {
-  const int c = fwd_kernel_choice();
-  if (c) return c == 2;
-  (void)g;
-  return false;
-}
-
 int pick_path(const dfa_impl::Geometry& g, dfa_dtype_t dtype, const void* q, const void* k, const void* v,
               const void* o) {
   const int ov = g_path_override.load();
@@ -303,9 +288,7 @@ static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int
   int launches = 0;
   if (path == DFA_PATH_SM100_TCGEN05) {
     const char* why = "";
-    launches = (!trace && !watchdog && use_v2(g))
-                   ? dfa_impl::launch_sm100_v2(g, q, k, v, o, lse, s, &err, &why)
-                   : dfa_impl::launch_sm100(g, q, k, v, o, lse, s, &err, &why, trace, watchdog);
+    launches = dfa_impl::launch_sm100(g, q, k, v, o, lse, s, &err, &why, trace, watchdog);
     if (launches == 0 && err != cudaSuccess)
       return fail(DFA_ERR_CUDA, "dfa_forward: sm100 path: %s (%s)", why, cudaGetErrorString(err));
   } else if (trace) {

@@ -899,13 +899,7 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
   p.scale = g.scale;
   p.c = g.scale * kLog2e;
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = device_sms();
   if (p.nblk > kMaxBlk || p.nblk >= DFA_BWD_LONG_FROM) {
     LongParams lp;
     lp.N = p.N;
@@ -919,13 +913,8 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
     lp.scale = p.scale;
     for (int i = 0; i < kMaxHeads; ++i) lp.offsets[i] = p.offsets[i];
     const size_t s1 = sizeof(DkdvSmem) + 1024, s2 = sizeof(DqSmem) + 1024;
-    static std::once_flag once_l;
-    static cudaError_t attr_l = cudaSuccess;
-    std::call_once(once_l, [&] {
-      attr_l = cudaFuncSetAttribute(dfa_bwd_dkdv_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-      if (attr_l == cudaSuccess)
-        attr_l = cudaFuncSetAttribute(dfa_bwd_dq_long_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-    });
+    cudaError_t attr_l = ensure_smem_attr(reinterpret_cast<const void*>(dfa_bwd_dkdv_long_kernel), s1);
+    if (attr_l == cudaSuccess) attr_l = ensure_smem_attr(reinterpret_cast<const void*>(dfa_bwd_dq_long_kernel), s2);
     if (attr_l != cudaSuccess) {
       *err = attr_l;
       *why = "cudaFuncSetAttribute failed";
@@ -938,11 +927,7 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
     return 2;
   }
   const size_t smem = sizeof(BwdSmem) + 1024;
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [&] {
-    attr = cudaFuncSetAttribute(dfa_bwd_sm100_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
+  const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void*>(dfa_bwd_sm100_kernel), smem);
   if (attr != cudaSuccess) {
     *err = attr;
     *why = "cudaFuncSetAttribute failed";

@@ -6,6 +6,10 @@
 #include <stdlib.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+#include <vector>
+
 namespace dfa_impl {
 
 constexpr int kMaxHeads = 256;  // head offsets travel in the kernel parameter block
@@ -30,6 +34,46 @@ inline void ensure_context() {
     cudaFree(nullptr);
     bound = true;
   }
+}
+
+// Per-device facts.  A process may drive several GPUs (one host thread per
+// device, or one thread switching devices), so every cache is keyed by the
+// current device, never process-wide.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+inline int device_sms() {
+  static std::atomic<int> cache[kMaxDevices];  // 0 = not queried yet
+  const int dev = current_device();
+  int n = (dev >= 0 && dev < kMaxDevices) ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (n > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 148;
+  }
+  if (dev >= 0 && dev < kMaxDevices) cache[dev].store(n, std::memory_order_relaxed);
+  return n;
+}
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute of
+// the kernel: set it once per (kernel, device, size).
+inline cudaError_t ensure_smem_attr(const void* fn, size_t smem) {
+  struct Done {
+    const void* fn;
+    int dev;
+    size_t smem;
+  };
+  static std::mutex mu;
+  static std::vector<Done> done;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(mu);
+  for (const Done& d : done)
+    if (d.fn == fn && d.dev == dev && d.smem >= smem) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) done.push_back({fn, dev, smem});
+  return e;
 }
 
 // Launch with the programmatic-stream-serialization attribute (PDL): the
@@ -72,12 +116,6 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr,
                  unsigned long long* watchdog = nullptr, bool merge = false);
-
-// Four-slot variant of the tcgen05 kernel (dfa_sm100_v2.cu): same coverage
-// as launch_sm100 without merge mode; 512-row work units.
-int launch_sm100_v2(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
-                    cudaStream_t stream, cudaError_t* err, const char** why);
-int64_t sm100_v2_units(const Geometry& g);
 
 // LSE-weighted combine of nb <= 8 branch outputs (dfa_combine.cu).
 int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int nb, const void* const* o,

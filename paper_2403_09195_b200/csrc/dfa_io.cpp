@@ -4,6 +4,7 @@
 //   rank x uint32 little-endian dims | raw little-endian scalars, row-major.
 // Errors map to DFA_ERR_IO (attnkit::io_error) with the reference's message
 // text, so golden vectors written by either side load on the other.
+#include <algorithm>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -92,24 +93,39 @@ dfa_status_t dfa_tensor_load(const char* path, int32_t want, void* out, int64_t 
   int64_t dims[kMaxRank];
   dfa_status_t st = read_header(fh.f, path, &dtype, &rank, dims);
   if (st != DFA_OK) return st;
+  // Element count with an overflow check: a crafted header (up to 8 dims of
+  // 2^32 - 1) must fail as io_error before anything is allocated or read.
+  const size_t width = dtype == 0 ? 4 : 8;
   int64_t n = 1;
-  for (int i = 0; i < rank; ++i) n *= dims[i];
+  for (int i = 0; i < rank; ++i) {
+    if (dims[i] != 0 && n > (int64_t)(SIZE_MAX / width) / dims[i])
+      return dfa_io_fail("tensor file %s: element count overflows", path);
+    n *= dims[i];
+  }
   if (n > capacity) return dfa_io_fail("dfa_tensor_load: %s holds %lld scalars, buffer has %lld", path, (long long)n,
                                        (long long)capacity);
-  const size_t width = dtype == 0 ? 4 : 8;
-  std::vector<uint8_t> raw((size_t)n * width);
-  if (n && fread(raw.data(), width, (size_t)n, fh.f) != (size_t)n) return dfa_io_fail("truncated tensor file: %s", path);
-  if (!little_endian()) swap_bytes(raw.data(), width, (size_t)n);
-  if (dtype == want) {
-    memcpy(out, raw.data(), raw.size());
-  } else if (dtype == 0) {
-    const float* src = reinterpret_cast<const float*>(raw.data());
-    double* dst = static_cast<double*>(out);
-    for (int64_t i = 0; i < n; ++i) dst[i] = (double)src[i];
-  } else {
-    const double* src = reinterpret_cast<const double*>(raw.data());
-    float* dst = static_cast<float*>(out);
-    for (int64_t i = 0; i < n; ++i) dst[i] = (float)src[i];
+  if (dtype == want) {  // straight into the caller's buffer (sized above)
+    if (n && fread(out, width, (size_t)n, fh.f) != (size_t)n) return dfa_io_fail("truncated tensor file: %s", path);
+    if (!little_endian()) swap_bytes(out, width, (size_t)n);
+    return DFA_OK;
+  }
+  // converting load: stream the payload through a bounded chunk buffer
+  constexpr size_t kChunk = 1 << 14;
+  std::vector<uint8_t> buf(kChunk * width);
+  uint8_t* raw = buf.data();
+  for (int64_t i0 = 0; i0 < n; i0 += (int64_t)kChunk) {
+    const size_t c = (size_t)std::min<int64_t>((int64_t)kChunk, n - i0);
+    if (fread(raw, width, c, fh.f) != c) return dfa_io_fail("truncated tensor file: %s", path);
+    if (!little_endian()) swap_bytes(raw, width, c);
+    if (dtype == 0) {
+      const float* src = reinterpret_cast<const float*>(raw);
+      double* dst = static_cast<double*>(out) + i0;
+      for (size_t i = 0; i < c; ++i) dst[i] = (double)src[i];
+    } else {
+      const double* src = reinterpret_cast<const double*>(raw);
+      float* dst = static_cast<float*>(out) + i0;
+      for (size_t i = 0; i < c; ++i) dst[i] = (float)src[i];
+    }
   }
   return DFA_OK;
 }
@@ -123,6 +139,7 @@ dfa_status_t dfa_tensor_save(const char* path, int32_t dtype, int32_t rank, cons
   for (int i = 0; i < rank; ++i) {
     if (dims[i] < 0 || dims[i] > (int64_t)UINT32_MAX) return dfa_io_fail("tensor dim %lld not representable",
                                                                          (long long)dims[i]);
+    if (dims[i] != 0 && n > (int64_t)(SIZE_MAX / 8) / dims[i]) return dfa_io_fail("tensor element count overflows");
     n *= dims[i];
   }
   if (n && !data) return dfa_io_fail("dfa_tensor_save: null data");

@@ -846,18 +846,6 @@ bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t 
   return res == CUDA_SUCCESS;
 }
 
-int num_sms() {
-  static int n = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  });
-  return n;
-}
-
 }  // namespace
 
 bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o) {
@@ -902,7 +890,7 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.unit_rows = kUnitRows;
   p.n_pairs = (p.T + kUnitRows - 1) / kUnitRows;
   // small grids: 128-row half units when twice the units still fit one wave
-  if ((int64_t)g.B * g.h * ((p.T + kBM - 1) / kBM) <= num_sms()) {
+  if ((int64_t)g.B * g.h * ((p.T + kBM - 1) / kBM) <= device_sms()) {
     p.unit_rows = kBM;
     p.n_pairs = (p.T + kBM - 1) / kBM;
   }
@@ -915,19 +903,15 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.div_m = make_fastdiv((uint32_t)p.m);
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
   const size_t smem = sizeof(SmemLayout) + 1024;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(dfa_sm100_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(dfa_sm100_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  });
+  cudaError_t attr_err = ensure_smem_attr(reinterpret_cast<const void*>(trace ? dfa_sm100_kernel<true>
+                                                                              : dfa_sm100_kernel<false>),
+                                          smem);
   if (attr_err != cudaSuccess) {
     *err = attr_err;
     *why = "cudaFuncSetAttribute failed";
     return 0;
   }
-  const int grid = (int)std::min<int64_t>(p.n_units, num_sms());
+  const int grid = (int)std::min<int64_t>(p.n_units, device_sms());
   cudaError_t le = cudaSuccess;
   if (trace)
     dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, mz, lse, p, trace, watchdog);

@@ -64,30 +64,54 @@ def segment_shard(n: int, w: int, rank: int, world: int) -> Tuple[int, int]:
     return min(a * w, n), min(b * w, n)
 
 
-def segment_parallel_forward(q, k, v, cfg, group=None, stream=None):
-    """Batch-1 latency path (SURVEY §8(e)): every rank computes the dilated
-    attention of its contiguous block of segments and one all-gather
-    assembles the [B, N, h, d_v] output on every rank.  The partition keeps
-    the segment grid (the local problem has N' = stop - start rows, the same
-    w, r and offsets), so the result is bit-identical to the one-GPU call."""
+def segment_local_forward(q, k, v, cfg, rank: int, world: int, stream=None):
+    """This rank's rows [a, b) of the dilated attention of q, k, v (whole
+    segments, segment_shard): the unchanged kernel on the local N' = b - a
+    problem, whose segment grid is the global one restricted to [a, b)."""
     import dataclasses
 
     import torch
-    import torch.distributed as dist
 
     from . import dfa_forward
+
+    a, b = segment_shard(cfg.seq_len, cfg.segment_len, rank, world)
+    n_loc = b - a
+    out = torch.zeros((q.shape[0], n_loc) + tuple(v.shape[2:]), dtype=v.dtype, device=v.device)
+    if n_loc == 0:
+        return out
+    if n_loc < cfg.interval:
+        # the tail segment is shorter than r: head j's view is the single row
+        # gamma_j (empty when gamma_j >= n_loc, attention.hpp:84-98); softmax
+        # over one key is exactly 1, so that row's output is the value row and
+        # every other row stays 0 (validate rejects r > w' for this problem)
+        for j, gj in enumerate(cfg.head_offsets):
+            if gj < n_loc:
+                out[:, gj, j] = v[:, a + gj, j]
+        return out
+    # a shard shorter than w is exactly the tail segment: one local segment of
+    # n_loc rows (w' = n_loc keeps validate's w <= N rule)
+    local = dataclasses.replace(cfg, seq_len=n_loc, segment_len=min(cfg.segment_len, n_loc))
+    return dfa_forward(q[:, a:b].contiguous(), k[:, a:b].contiguous(), v[:, a:b].contiguous(), local,
+                       out=out, stream=stream)
+
+
+def segment_parallel_forward(q, k, v, cfg, group=None, stream=None):
+    """Batch-1 latency path (SURVEY §8(e)): every rank computes the dilated
+    attention of its contiguous block of segments (segment_local_forward) and
+    one all-gather assembles the [B, N, h, d_v] output on every rank.  The
+    partition keeps the segment grid, so the result is bit-identical to the
+    one-GPU call."""
+    import torch
+    import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     n = cfg.seq_len
-    a, b = segment_shard(n, cfg.segment_len, rank, world)
-    local = dataclasses.replace(cfg, seq_len=b - a)
     parts_rows = [segment_shard(n, cfg.segment_len, r, world) for r in range(world)]
     width = max(hi - lo for lo, hi in parts_rows)
     mine = torch.zeros((q.shape[0], width) + tuple(v.shape[2:]), dtype=v.dtype, device=v.device)
-    if b > a:  # padded to the widest shard so the all-gather sees equal sizes
-        mine[:, : b - a] = dfa_forward(q[:, a:b].contiguous(), k[:, a:b].contiguous(), v[:, a:b].contiguous(),
-                                       local, stream=stream)
+    local = segment_local_forward(q, k, v, cfg, rank, world, stream=stream)
+    mine[:, : local.shape[1]] = local  # padded to the widest shard so the all-gather sees equal sizes
     gathered = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(gathered, mine, group=group)
     return torch.cat([g[:, : hi - lo] for g, (lo, hi) in zip(gathered, parts_rows)], dim=1)

@@ -1,5 +1,4 @@
-"""One forward shape, a few launches (for ncu captures): fwd_once.py W R [B] [KERNEL]."""
-import os
+"""One forward shape, a few launches (for ncu captures): fwd_once.py W R [B]."""
 import sys
 
 import torch
@@ -9,8 +8,6 @@ import paper_2403_09195_b200 as dfa  # noqa: E402
 
 w, r = int(sys.argv[1]), int(sys.argv[2])
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 16
-if len(sys.argv) > 4:
-    os.environ["DFA_FWD_KERNEL"] = sys.argv[4]
 N, h = 4096, 6
 q, k, v = (torch.randn((B, N, h, 64), device="cuda", dtype=torch.bfloat16) for _ in range(3))
 cfg = dfa.AttentionConfig(N, w, r, h, 64, dfa.AttentionConfig.spread_offsets(h, r))

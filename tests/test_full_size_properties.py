@@ -17,8 +17,8 @@ pytestmark = pytest.mark.gpu
 GRID = [(w, r) for w in (256, 512, 1024, 2048, 4096) for r in (1, 2, 4, 8)]
 
 
-def _cfg(dfa, w, r, h=6):
-    return dfa.AttentionConfig(4096, w, r, h, 64, dfa.AttentionConfig.spread_offsets(h, r))
+def _cfg(dfa, w, r, n=4096, h=6):
+    return dfa.AttentionConfig(n, w, r, h, 64, dfa.AttentionConfig.spread_offsets(h, r))
 
 
 @pytest.fixture(scope="module")
@@ -75,26 +75,24 @@ def test_config5_batch_decomposition(dfa, cuda):
     assert torch.equal(whole, parts)
 
 
-@pytest.mark.parametrize("world", [2, 3, 4, 8])
-def test_segment_sharded_forward_is_bit_identical(dfa, cuda, world):
-    """dist.segment_parallel_forward's partition (whole segments per rank, the
-    unchanged kernel on each N' = stop - start problem) reproduces the
-    one-GPU output bit for bit -- computed here shard by shard on one GPU."""
-    import dataclasses
-
+@pytest.mark.parametrize("n,w,r,world", [
+    (4096, 512, 2, 2), (4096, 512, 2, 3), (4096, 512, 2, 8),
+    (1000, 300, 2, 4),   # N % w != 0, world = n_seg: the last rank holds only the 100-row tail
+    (4196, 512, 2, 8),   # 9 segments over 8 ranks, 100-row tail
+    (601, 300, 4, 4),    # 1-row tail shorter than r
+])
+def test_segment_sharded_forward_is_bit_identical(dfa, cuda, n, w, r, world):
+    """dist.segment_local_forward's partition (whole segments per rank, the
+    unchanged kernel on each N' = stop - start problem, tail-only shards
+    included) reproduces the one-GPU output bit for bit -- every rank's part
+    computed here on one GPU."""
     import torch
-    from paper_2403_09195_b200.dist import segment_shard
+    from paper_2403_09195_b200.dist import segment_local_forward
 
-    g = torch.Generator(device="cuda").manual_seed(world)
-    q, k, v = (torch.randn((2, 4096, 6, 64), device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
-    cfg = _cfg(dfa, 512, 2)
+    g = torch.Generator(device="cuda").manual_seed(world + n)
+    q, k, v = (torch.randn((2, n, 6, 64), device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(3))
+    cfg = _cfg(dfa, w, r, n)
     full = dfa.dfa_forward(q, k, v, cfg)
-    parts = []
-    for rank in range(world):
-        a, b = segment_shard(4096, 512, rank, world)
-        if b > a:
-            local = dataclasses.replace(cfg, seq_len=b - a)
-            parts.append(dfa.dfa_forward(q[:, a:b].contiguous(), k[:, a:b].contiguous(), v[:, a:b].contiguous(),
-                                         local))
+    parts = [segment_local_forward(q, k, v, cfg, rank, world) for rank in range(world)]
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, dim=1), full)

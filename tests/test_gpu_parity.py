@@ -452,21 +452,6 @@ def test_host_entry_zero_copy_equals_copy_path(dfa, cuda):
         assert torch.equal(o, ref)
 
 
-@pytest.mark.parametrize("n,w,r,h", [
-    (4096, 512, 2, 6),   # headline geometry: slot groups {0,1}, {2,3} in different segments
-    (1000, 300, 2, 2),   # m = 150: groups with equal first tile, unequal lengths; tails
-    (512, 64, 2, 2),     # m = 32: four segments per slot, disjoint groups
-    (4104, 513, 3, 3),   # m = 171, tail unit with empty slots
-    (640, 640, 1, 1),    # one segment spanning every slot
-])
-def test_v2_four_slot_kernel_vs_oracle(dfa, port, cuda, n, w, r, h, monkeypatch):
-    """The opt-in four-slot forward (DFA_FWD_KERNEL=v2, csrc/dfa_sm100_v2.cu)
-    meets the same bf16 bar as the default kernel."""
-    monkeypatch.setenv("DFA_FWD_KERNEL", "v2")
-    mx, rel = _bf16_case(dfa, port, 2, n, w, r, h, 3 * n + w)
-    assert mx <= BF16_MAX_ABS and rel <= BF16_MEAN_REL, (mx, rel)
-
-
 def test_forward_and_backward_from_a_fresh_thread(dfa, cuda):
     """The tcgen05 launchers encode TMA descriptors with the driver API; a
     thread whose first CUDA call that is (e.g. PyTorch's autograd worker)

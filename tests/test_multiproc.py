@@ -91,6 +91,7 @@ def _seg_worker(rank, world, port, q):
 
     def fake_forward(qq, kk, vv, cfg, out=None, stream=None):
         assert qq.shape[1] == cfg.seq_len  # the local problem keeps the segment grid
+        cfg.validate()  # a tail-only shard must still be a valid configuration
         return vv * 2
 
     dfa_pkg.dfa_forward = fake_forward
@@ -114,3 +115,51 @@ def test_segment_parallel_world2_gloo():
         assert p.exitcode == 0
     for _, rows in res:
         assert rows == [2.0 * i for i in range(1000)]
+
+
+def _tail_worker(rank, world, port, q):
+    """A shard holding only a tail segment shorter than w (N = 1000, w = 300,
+    world 4: the last rank owns rows 900-999) and one shorter than r (N = 601,
+    w = 300, r = 4: the last rank owns row 600 only)."""
+    import dataclasses
+
+    import paper_2403_09195_b200 as dfa_pkg
+    from paper_2403_09195_b200 import dist as ddist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def fake_forward(qq, kk, vv, cfg, out=None, stream=None):
+        cfg.validate()
+        assert cfg.segment_len <= cfg.seq_len
+        return vv * 2
+
+    dfa_pkg.dfa_forward = fake_forward
+    res = []
+    for n, w, r in ((1000, 300, 2), (601, 300, 4)):
+        cfg = dfa_pkg.AttentionConfig(n, w, r, 2, 4, [0, 1])
+        v = torch.arange(n, dtype=torch.float32).view(1, n, 1, 1).expand(1, n, 2, 4).contiguous()
+        out = ddist.segment_parallel_forward(v, v, v, dataclasses.replace(cfg))
+        res.append(out[0, :, :, 0].tolist())
+    q.put((rank, res))
+    dist.destroy_process_group()
+
+
+def test_segment_parallel_tail_shards_world4_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tail_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, (a, b) in res:
+        assert a == [[2.0 * i, 2.0 * i] for i in range(1000)]
+        # rows 0-599: the stand-in kernel; row 600 (tail shorter than r = 4):
+        # head 0 (gamma 0) keeps v's row, head 1 (gamma 1 >= 1 row) is 0
+        assert b[:600] == [[2.0 * i, 2.0 * i] for i in range(600)]
+        assert b[600] == [600.0, 0.0]

@@ -46,15 +46,3 @@ def test_model_flags_the_stat_full_hazard(monkeypatch):
     with pytest.raises(pm.ParityHazard):
         for seed in range(3):
             pm.run(p, 10, seed)
-
-
-import protocol_model_v2 as pm2  # noqa: E402
-
-
-@pytest.mark.parametrize("n,w,r", GEOMS[::3] + [(2000, 192, 2), (1000, 96, 4), (300, 60, 3)])
-def test_v2_protocol_is_deadlock_and_parity_safe(n, w, r):
-    """The opt-in four-slot kernel (csrc/dfa_sm100_v2.cu): round-robin step
-    order over slot groups, one S buffer per slot -- no deadlock, no parity
-    hazard, and every step reads the key tile its group lead loaded."""
-    for B, h, grid in ((2, 6, 148), (1, 2, 5)):
-        assert pm2.check(n, w, r, h, B, grid, seeds=2) == [], (n, w, r, B, h, grid)
