@@ -130,22 +130,31 @@ class ClockSampler:
             time.sleep(0.0002)
 
     def start(self):
-        self.samples, self.stop_flag = [], False
-        if self.nvml:
+        """Poll from now until close(); window() reads any timed region."""
+        if self.nvml and self.thread is None:
             self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
+            time.sleep(0.02)  # first samples land before the first region
 
-    def stop(self, t0, t1):
+    def close(self):
+        self.stop_flag = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def window(self, t0, t1):
         if not self.nvml:
             return self._smi_once()
-        self.stop_flag = True
-        self.thread.join(timeout=2)
-        window = [x for x in self.samples if t0 <= x[0] <= t1] or self.samples[-3:]
-        if not window:
+        samples = list(self.samples)
+        win = [x for x in samples if t0 <= x[0] <= t1]
+        if not win:  # region shorter than one NVML poll: the samples bracketing it
+            before = [x for x in samples if x[0] < t0][-1:]
+            after = [x for x in samples if x[0] > t1][:1]
+            win = before + after
+        if not win:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"]}
-        reasons = sorted({n for x in window for n, bit in self.bits.items() if x[3] & bit})
-        return {"sm_mhz": statistics.median(x[1] for x in window), "sm_max_mhz": self.max_mhz,
-                "power_w_max": max(x[2] for x in window), "samples": len(window), "reasons": reasons,
+        reasons = sorted({n for x in win for n, bit in self.bits.items() if x[3] & bit})
+        return {"sm_mhz": statistics.median(x[1] for x in win), "sm_max_mhz": self.max_mhz,
+                "power_w_max": max(x[2] for x in win), "samples": len(win), "reasons": reasons,
                 "sampler": "nvml ~0.5 ms during the timed region"}
 
     def _smi_once(self):
@@ -358,6 +367,7 @@ class Ctx:
             dist.init_process_group("nccl", device_id=self.dev)
         self.stream = torch.cuda.current_stream(self.dev)
         self.sampler = ClockSampler(self.dev)
+        self.sampler.start()
 
     def cfg(self, w, r, h=H, d=D, n=N_TOK):
         return self.dfa.AttentionConfig(n, w, r, h, d, self.dfa.AttentionConfig.spread_offsets(h, r))
@@ -388,7 +398,6 @@ class Ctx:
             step()
         self.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        self.sampler.start()
         launches = 0
         t0 = time.time()
         e0.record(self.stream)
@@ -397,7 +406,7 @@ class Ctx:
         e1.record(self.stream)
         self.barrier()
         t1 = time.time()
-        clocks = self.sampler.stop(t0, t1)
+        clocks = self.sampler.window(t0, t1)
         total_ms, = self.max_over_ranks(e0.elapsed_time(e1))
         return total_ms, launches, clocks
 
@@ -737,6 +746,7 @@ def run_b200(args):
         ctx.torch.cuda.empty_cache()
         extras["config4"] = wl_config4(ctx, 20, 3)
         extras["lse"] = wl_lse(ctx, 20, 3)
+    ctx.sampler.close()
     if ctx.rank == 0:
         emit(args, ctx.world, res, extras)
     if ctx.world > 1:
@@ -829,7 +839,7 @@ def main(argv=None):
     argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")

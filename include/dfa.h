@@ -45,7 +45,9 @@ typedef enum {
   DFA_ERR_IO = 7            /* attnkit::io_error (DTNSR1 tensor files)  */
 } dfa_status_t;
 
-typedef enum { DFA_F32 = 0, DFA_BF16 = 1 } dfa_dtype_t;
+/* F64: the reference's double instantiation (attention.hpp with Scalar =
+ * double) -- forward only, on the SIMT kernel with double arithmetic. */
+typedef enum { DFA_F32 = 0, DFA_BF16 = 1, DFA_F64 = 2 } dfa_dtype_t;
 
 /* attention.hpp:15 Kernel{naive, tiled}.  Validated exactly as the reference
  * does (tile_size >= 1 when tiled); on the GPU every kernel streams keys in

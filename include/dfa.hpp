@@ -220,7 +220,7 @@ void require_rank2(const T& t, const char* op) {
 }
 }  // namespace detail
 
-// attention.hpp:280-301 on host tensors (GPU fp32 validation kernel).
+// attention.hpp:280-301 on host tensors (GPU fp32 / f64 validation kernels).
 // Same preconditions and error types as the reference: validate(); q/k widths
 // and k/v rows agree (require_qkv :102-110); q and k have cfg.seq_len rows
 // (:285-286); head_offset in [0, r) else std::out_of_range (:287-288).
@@ -254,27 +254,14 @@ Tensor dilated_attention(const Tensor& q, const Tensor& k, const Tensor& v, cons
   one.head_dim = q.cols();
   std::vector<int64_t> offs;
   dfa_config_t c = one.to_c(offs, v.cols());
+  // float tensors run the fp32 validation kernel, double tensors the f64
+  // kernel (double arithmetic end to end, the reference's f64 mode)
+  constexpr dfa_dtype_t dt = std::is_same_v<Scalar, double> ? DFA_F64 : DFA_F32;
   std::size_t bytes = 0;
-  check(dfa_workspace_bytes(&c, DFA_F32, 1, 0, &bytes));
+  check(dfa_workspace_bytes(&c, dt, 1, 0, &bytes));
   Tensor out({q.rows(), v.cols()});
-  if constexpr (std::is_same_v<Scalar, float>) {
-    check(dfa_forward_host(&c, DFA_F32, 1, q.data(), k.data(), v.data(), out.data(), nullptr,
-                           thread_workspace().get(bytes), nullptr));
-  } else {
-    // double tensors (the reference's f64 mode) run the fp32 device path:
-    // inputs rounded to float, the result widened back (~1e-7 relative)
-    auto narrow = [](const Tensor& t) {
-      const std::size_t n = static_cast<std::size_t>(t.rows() * t.cols());
-      std::vector<float> f(n);
-      for (std::size_t i = 0; i < n; ++i) f[i] = static_cast<float>(t.data()[i]);
-      return f;
-    };
-    const auto fq = narrow(q), fk = narrow(k), fv = narrow(v);
-    std::vector<float> fo(static_cast<std::size_t>(q.rows() * v.cols()));
-    check(dfa_forward_host(&c, DFA_F32, 1, fq.data(), fk.data(), fv.data(), fo.data(), nullptr,
-                           thread_workspace().get(bytes), nullptr));
-    for (std::size_t i = 0; i < fo.size(); ++i) out.data()[i] = static_cast<double>(fo[i]);
-  }
+  check(dfa_forward_host(&c, dt, 1, q.data(), k.data(), v.data(), out.data(), nullptr, thread_workspace().get(bytes),
+                         nullptr));
   return out;
 }
 

@@ -441,3 +441,100 @@ int oracle_dilated_backward_f64(const double* q, const double* k, const double* 
   free(dP);
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * Batched, threaded drivers (test infrastructure): the multi-head layout
+ * [B, N, h, d] of the device API, one (image, head) unit per task over a
+ * pool of pthreads.  Each unit calls the single-head restatement above on
+ * the head's column block, so the arithmetic is exactly the pinned port's
+ * (attention.hpp:280-301 per head, the multi-head concat of :350-357). */
+#include <pthread.h>
+#include <stdatomic.h>
+
+typedef struct {
+  const double *q, *k, *v;
+  int64_t B, n, h, d, dv, w, r, nb;
+  const int64_t *offsets; /* [h] (single branch) or [nb * h] */
+  const int64_t *ws, *rs; /* [nb] (multibranch) */
+  double *out, *lse;
+  atomic_long next;
+  atomic_int status;
+  int multibranch;
+} orc_batch_t;
+
+static void* orc_batch_worker(void* arg) {
+  orc_batch_t* t = (orc_batch_t*)arg;
+  const int64_t n = t->n, d = t->d, dv = t->dv, h = t->h;
+  double* qs = (double*)malloc(sizeof(double) * (size_t)(n * d));
+  double* ks = (double*)malloc(sizeof(double) * (size_t)(n * d));
+  double* vs = (double*)malloc(sizeof(double) * (size_t)(n * dv));
+  double* os = (double*)malloc(sizeof(double) * (size_t)(n * dv));
+  double* ls = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t gs[64];
+  for (;;) {
+    const long u = atomic_fetch_add(&t->next, 1);
+    if (u >= t->B * h) break;
+    const int64_t b = u / h, j = u % h;
+    for (int64_t a = 0; a < n; ++a) {
+      memcpy(qs + a * d, t->q + ((b * n + a) * h + j) * d, sizeof(double) * (size_t)d);
+      memcpy(ks + a * d, t->k + ((b * n + a) * h + j) * d, sizeof(double) * (size_t)d);
+      memcpy(vs + a * dv, t->v + ((b * n + a) * h + j) * dv, sizeof(double) * (size_t)dv);
+    }
+    int st;
+    if (t->multibranch) {
+      for (int64_t e = 0; e < t->nb; ++e) gs[e] = t->offsets[e * h + j];
+      st = oracle_multibranch_f64(qs, ks, vs, n, d, dv, t->nb, t->ws, t->rs, gs, 1, os, ls);
+    } else {
+      st = oracle_dilated_attention_f64(qs, ks, vs, n, d, dv, t->w, t->r, t->offsets[j], 1, 0, 1, os);
+    }
+    if (st != ORC_OK) {
+      atomic_store(&t->status, st);
+      break;
+    }
+    for (int64_t a = 0; a < n; ++a) {
+      memcpy(t->out + ((b * n + a) * h + j) * dv, os + a * dv, sizeof(double) * (size_t)dv);
+      if (t->multibranch && t->lse) t->lse[(b * h + j) * n + a] = ls[a];
+    }
+  }
+  free(qs);
+  free(ks);
+  free(vs);
+  free(os);
+  free(ls);
+  return NULL;
+}
+
+static int orc_batch_run(orc_batch_t* t, int32_t threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t pool[256];
+  atomic_init(&t->next, 0);
+  atomic_init(&t->status, ORC_OK);
+  for (int32_t i = 0; i < threads; ++i) pthread_create(&pool[i], NULL, orc_batch_worker, t);
+  for (int32_t i = 0; i < threads; ++i) pthread_join(pool[i], NULL);
+  return atomic_load(&t->status);
+}
+
+/* dilated_attention (f64, naive kernel) for every (image, head) of [B, N, h, d]. */
+int oracle_dilated_batched_f64(const double* q, const double* k, const double* v, int64_t B, int64_t n, int64_t h,
+                               int64_t d, int64_t dv, int64_t w, int64_t r, const int64_t* offsets, int32_t threads,
+                               double* out) {
+  orc_batch_t t;
+  memset(&t, 0, sizeof(t));
+  t.q = q, t.k = k, t.v = v, t.B = B, t.n = n, t.h = h, t.d = d, t.dv = dv, t.w = w, t.r = r;
+  t.offsets = offsets, t.out = out;
+  return orc_batch_run(&t, threads);
+}
+
+/* oracle_multibranch_f64 for every (image, head); offsets [nb * h]
+ * (branch-major), lse (optional) [B, h, N]. */
+int oracle_multibranch_batched_f64(const double* q, const double* k, const double* v, int64_t B, int64_t n,
+                                   int64_t h, int64_t d, int64_t dv, int64_t nb, const int64_t* ws, const int64_t* rs,
+                                   const int64_t* offsets, int32_t threads, double* out, double* lse) {
+  if (nb < 1 || nb > 64) return ORC_ERR_CONFIG;
+  orc_batch_t t;
+  memset(&t, 0, sizeof(t));
+  t.q = q, t.k = k, t.v = v, t.B = B, t.n = n, t.h = h, t.d = d, t.dv = dv, t.nb = nb;
+  t.ws = ws, t.rs = rs, t.offsets = offsets, t.out = out, t.lse = lse, t.multibranch = 1;
+  return orc_batch_run(&t, threads);
+}

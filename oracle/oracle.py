@@ -41,6 +41,13 @@ def _ptr(a: np.ndarray, t):
     return a.ctypes.data_as(t)
 
 
+def _threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 class OracleError(RuntimeError):
     def __init__(self, code: int, msg: str = ""):
         super().__init__(f"status {code}: {msg}")
@@ -76,6 +83,11 @@ class Port:
         L.oracle_time_dilated_f32.argtypes = [_f, _f, _f, _i64, _i64, _i64, _i64, _i64, _i64, _f]
         L.oracle_dilated_backward_f64.restype = _i32
         L.oracle_dilated_backward_f64.argtypes = [_d, _d, _d, _d, _i64, _i64, _i64, _i64, _i64, _i64, _i32, _d, _d, _d]
+        L.oracle_dilated_batched_f64.restype = _i32
+        L.oracle_dilated_batched_f64.argtypes = [_d, _d, _d, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64p, _i32, _d]
+        L.oracle_multibranch_batched_f64.restype = _i32
+        L.oracle_multibranch_batched_f64.argtypes = [_d, _d, _d, _i64, _i64, _i64, _i64, _i64, _i64, _i64p, _i64p,
+                                                     _i64p, _i32, _d, _d]
 
     def validate(self, n, w, r, h, d, offsets, tiled=False, tile=1, full=False) -> int:
         offs = np.asarray(offsets, dtype=np.int64)
@@ -144,6 +156,37 @@ class Port:
         st = self.lib.oracle_multibranch_f64(_ptr(q, _d), _ptr(k, _d), _ptr(v, _d), n, d, v.shape[1], len(branches),
                                              _ptr(ws, _i64p), _ptr(rs, _i64p), _ptr(gs, _i64p), int(scale),
                                              _ptr(out, _d), _ptr(lse, _d))
+        if st:
+            raise OracleError(st)
+        return out, lse
+
+    def dilated_batched(self, q, k, v, w, r, offsets, threads=None):
+        """[B, N, h, d] (f64) -> [B, N, h, dv]: dilated_attention per (image, head)
+        on `threads` host threads (default: all)."""
+        q, k, v = (np.ascontiguousarray(x, dtype=np.float64) for x in (q, k, v))
+        B, n, h, d = q.shape
+        dv = v.shape[3]
+        offs = np.asarray(offsets, dtype=np.int64)
+        out = np.zeros((B, n, h, dv))
+        st = self.lib.oracle_dilated_batched_f64(_ptr(q, _d), _ptr(k, _d), _ptr(v, _d), B, n, h, d, dv, w, r,
+                                                 _ptr(offs, _i64p), threads or _threads(), _ptr(out, _d))
+        if st:
+            raise OracleError(st)
+        return out
+
+    def multibranch_batched(self, q, k, v, branches, threads=None):
+        """branches: list of (w, r, offsets[h]).  Returns (out [B, N, h, dv], lse [B, h, N])."""
+        q, k, v = (np.ascontiguousarray(x, dtype=np.float64) for x in (q, k, v))
+        B, n, h, d = q.shape
+        dv = v.shape[3]
+        ws = np.array([b[0] for b in branches], dtype=np.int64)
+        rs = np.array([b[1] for b in branches], dtype=np.int64)
+        gs = np.ascontiguousarray(np.array([list(b[2]) for b in branches], dtype=np.int64))
+        out = np.zeros((B, n, h, dv))
+        lse = np.zeros((B, h, n))
+        st = self.lib.oracle_multibranch_batched_f64(_ptr(q, _d), _ptr(k, _d), _ptr(v, _d), B, n, h, d, dv,
+                                                     len(branches), _ptr(ws, _i64p), _ptr(rs, _i64p), _ptr(gs, _i64p),
+                                                     threads or _threads(), _ptr(out, _d), _ptr(lse, _d))
         if st:
             raise OracleError(st)
         return out, lse

@@ -221,7 +221,17 @@ def _dtype_code(t) -> int:
         return _lib.DFA_F32
     if t.dtype == torch.bfloat16:
         return _lib.DFA_BF16
-    raise DimensionError(f"dfa: unsupported dtype {t.dtype} (float32 or bfloat16)")
+    if t.dtype == torch.float64:
+        return _lib.DFA_F64
+    raise DimensionError(f"dfa: unsupported dtype {t.dtype} (float32, bfloat16 or float64)")
+
+
+def _code(dtype: str) -> int:
+    """"f32" | "bf16" | "f64" -> DFA_* code."""
+    try:
+        return {"f32": _lib.DFA_F32, "bf16": _lib.DFA_BF16, "f64": _lib.DFA_F64}[dtype]
+    except KeyError:
+        raise ConfigError(f"dfa: unknown dtype {dtype!r} (f32, bf16 or f64)") from None
 
 
 def _stream_ptr(stream) -> int:
@@ -235,7 +245,7 @@ def query_path(cfg: AttentionConfig, dtype: str = "bf16", batch: int = 1) -> int
     """Which device kernel dfa_forward takes (DFA_PATH_* in include/dfa.h)."""
     c = cfg._c()
     out = ctypes.c_int32(0)
-    _check(lib.dfa_query_path(ctypes.byref(c), _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16, batch,
+    _check(lib.dfa_query_path(ctypes.byref(c), _code(dtype), batch,
                               ctypes.byref(out)))
     return out.value
 
@@ -370,7 +380,7 @@ class Workspace:
     def bytes_for(cfg: AttentionConfig, dtype: str, batch: int, with_lse: bool = False) -> int:
         c = cfg._c()
         out = ctypes.c_size_t(0)
-        _check(lib.dfa_workspace_bytes(ctypes.byref(c), _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16, batch,
+        _check(lib.dfa_workspace_bytes(ctypes.byref(c), _code(dtype), batch,
                                        1 if with_lse else 0, ctypes.byref(out)))
         return out.value
 
@@ -393,7 +403,7 @@ def dfa_forward_host(q, k, v, out, cfg: AttentionConfig, ws: Workspace, dtype: s
     B = q.shape[0]
     c = cfg._c()
     c.value_dim = v.shape[-1]
-    code = _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16
+    code = _code(dtype)
     sp = _stream_ptr(stream) if stream is not None else None
     _check(lib.dfa_forward_host(ctypes.byref(c), code, B, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                 lse.data_ptr() if lse is not None else None, ws.handle, sp))
@@ -415,7 +425,7 @@ def host_transfer_bytes(q, k, v, cfg: AttentionConfig, dtype: str = "bf16", with
     c = cfg._c()
     c.value_dim = v.shape[-1]
     h2d, d2h = ctypes.c_size_t(0), ctypes.c_size_t(0)
-    _check(lib.dfa_host_transfer_bytes(ctypes.byref(c), _lib.DFA_F32 if dtype == "f32" else _lib.DFA_BF16,
+    _check(lib.dfa_host_transfer_bytes(ctypes.byref(c), _code(dtype),
                                        q.shape[0], q.data_ptr(), k.data_ptr(), v.data_ptr(), 1 if with_lse else 0,
                                        ctypes.byref(h2d), ctypes.byref(d2h)))
     return h2d.value, d2h.value

@@ -24,6 +24,7 @@ DFA_ERR_IO = 7
 
 DFA_F32 = 0
 DFA_BF16 = 1
+DFA_F64 = 2
 
 DFA_PATH_NONE = 0
 DFA_PATH_SM100_TCGEN05 = 1

@@ -102,7 +102,7 @@ int pick_path(const dfa_impl::Geometry& g, dfa_dtype_t dtype, const void* q, con
   return DFA_PATH_SIMT;
 }
 
-size_t elem_size(dfa_dtype_t t) { return t == DFA_F32 ? 4 : 2; }
+size_t elem_size(dfa_dtype_t t) { return t == DFA_F64 ? 8 : t == DFA_F32 ? 4 : 2; }
 
 // Device address of pinned, mapped host memory (nullptr for pageable or device memory).
 const void* mapped_host(const void* p) {
@@ -279,7 +279,8 @@ static dfa_status_t forward_impl(const dfa_config_t* cfg, dfa_dtype_t dtype, int
     g.ldv = ld[2];
     g.ldo = ld[3];
   }
-  if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_CONFIG, "dfa_forward: unknown dtype %d", (int)dtype);
+  if (dtype != DFA_F32 && dtype != DFA_BF16 && dtype != DFA_F64)
+    return fail(DFA_ERR_CONFIG, "dfa_forward: unknown dtype %d", (int)dtype);
   if (batch == 0) return DFA_OK;
   if (!q || !k || !v || !o) return fail(DFA_ERR_DIMENSION, "dfa_forward: null tensor pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -451,6 +452,7 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t nb, const
   dfa_status_t st = dfa_multibranch_workspace_bytes(base, nb, dtype, batch, &need);
   if (st != DFA_OK) return st;
   if (!branches) return fail(DFA_ERR_CONFIG, "multibranch: null branch list");
+  if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_UNSUPPORTED, "multibranch: dtype %d (f32 / bf16)", (int)dtype);
   if (ws_bytes < need || !workspace)
     return fail(DFA_ERR_DIMENSION, "multibranch: workspace has %zu bytes, needs %zu", ws_bytes, need);
   g_launches = 0;
@@ -531,7 +533,7 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
   dfa_impl::Geometry g;
   dfa_status_t st = resolve(cfg, batch, &g);
   if (st != DFA_OK) return st;
-  if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_CONFIG, "dfa_backward: unknown dtype %d", (int)dtype);
+  if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_UNSUPPORTED, "dfa_backward: dtype %d (f32 / bf16)", (int)dtype);
   if (batch == 0) return DFA_OK;
   if (!q || !k || !v || !o || !lse || !dout || !dq || !dk || !dv)
     return fail(DFA_ERR_DIMENSION, "dfa_backward: null tensor pointer");
@@ -568,6 +570,8 @@ dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t
   dfa_impl::Geometry g;
   dfa_status_t st = layer_geometry(cfg, batch, &g, "multi_head_dilated");
   if (st != DFA_OK) return st;
+  if (dtype != DFA_F32 && dtype != DFA_BF16)
+    return fail(DFA_ERR_UNSUPPORTED, "multi_head_dilated: dtype %d (f32 / bf16)", (int)dtype);
   const size_t es = elem_size(dtype), D = (size_t)(g.h * g.d);
   *bytes = 4 * up256((size_t)(g.B * g.N) * D * es) + up256(3 * D * D * es) + kLtWorkspace;
   return DFA_OK;
@@ -701,7 +705,8 @@ dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, 
   dfa_status_t st = layer_geometry(cfg, batch, &g, "multi_head_dilated");
   if (st != DFA_OK) return st;
   size_t need = 0;
-  dfa_multi_head_workspace_bytes(cfg, dtype, batch, &need);
+  st = dfa_multi_head_workspace_bytes(cfg, dtype, batch, &need);
+  if (st != DFA_OK) return st;
   if (!workspace || ws_bytes < need)
     return fail(DFA_ERR_DIMENSION, "multi_head_dilated: workspace has %zu bytes, needs %zu", ws_bytes, need);
   if (batch == 0) return DFA_OK;
@@ -751,7 +756,8 @@ dfa_status_t dfa_multi_head_dilated_host(const dfa_config_t* cfg, dfa_dtype_t dt
   size_t need = 0, dev_need = 0;
   dfa_status_t st = dfa_multi_head_host_workspace_bytes(cfg, dtype, batch, &need);
   if (st != DFA_OK) return st;
-  dfa_multi_head_workspace_bytes(cfg, dtype, batch, &dev_need);
+  st = dfa_multi_head_workspace_bytes(cfg, dtype, batch, &dev_need);
+  if (st != DFA_OK) return st;
   if (!ws || ws->bytes < need)
     return fail(DFA_ERR_DIMENSION, "multi_head_dilated: workspace has %zu bytes, needs %zu", ws ? ws->bytes : 0,
                 need);
@@ -780,6 +786,8 @@ dfa_status_t dfa_encoder_block_workspace_bytes(const dfa_config_t* cfg, dfa_dtyp
   dfa_impl::Geometry g;
   dfa_status_t st = layer_geometry(cfg, batch, &g, "encoder_block");
   if (st != DFA_OK) return st;
+  if (dtype != DFA_F32 && dtype != DFA_BF16)
+    return fail(DFA_ERR_UNSUPPORTED, "encoder_block: dtype %d (f32 / bf16)", (int)dtype);
   if (hidden < 1) return fail(DFA_ERR_CONFIG, "encoder: mlp_ratio must yield a positive width");
   const size_t es = elem_size(dtype), D = (size_t)(g.h * g.d);
   const size_t act = up256((size_t)(g.B * g.N) * D * es);

@@ -12,6 +12,8 @@
 // memset.  Index math is the closed form of make_segment_view
 // (attention.hpp:84-98): view rows are seg_begin + gamma + t*r.
 #include <cuda_bf16.h>
+
+#include <algorithm>
 #include <math.h>
 
 #include "dfa_internal.h"
@@ -23,6 +25,7 @@ struct SimtParams {
   int64_t N, w, r, h, d, dv, n_chunks;
   int64_t ldq, ldk, ldv, ldo;  // token strides (elements)
   float scale;
+  double scale64;  // Scalar(1) / sqrt(Scalar(d)) in double (f64 mode)
   int32_t offsets[kMaxHeads];
 };
 
@@ -259,6 +262,123 @@ __global__ void __launch_bounds__(128) simt_split_kernel(const T* __restrict__ q
   }
 }
 
+// f64 mode (the reference's double instantiation, attention.hpp:280-301 with
+// Scalar = double): the same thread-per-query-row online softmax as
+// simt_kernel with every operation in double -- DFMA dot products, the scale
+// applied after the dot (attention.hpp:124-125), exp() of the max-subtracted
+// scores and a final reciprocal multiply (the tiled recurrence,
+// attention.hpp:170-205).  Only the summation order differs from the
+// reference's naive kernel, so results agree to ~1e-15 relative (the
+// reference's own f64 gates use 1e-10).
+template <int DMAX, int KT>
+__global__ void __launch_bounds__(128) simt_f64_kernel(const double* __restrict__ q, const double* __restrict__ k,
+                                                       const double* __restrict__ v, double* __restrict__ o,
+                                                       float* __restrict__ lse, const __grid_constant__ SimtParams p) {
+  __shared__ double ks[KT][DMAX];
+  __shared__ double vs[KT][DMAX];
+  const int tid = threadIdx.x;
+  const int64_t seg = blockIdx.x / p.n_chunks;
+  const int64_t chunk = blockIdx.x % p.n_chunks;
+  const int64_t j = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const int64_t g = p.offsets[j];
+  const int64_t seg_begin = seg * p.w;
+  const int64_t seg_rows = min(seg_begin + p.w, p.N) - seg_begin;
+  const int64_t m = g >= seg_rows ? 0 : (seg_rows - g + p.r - 1) / p.r;  // attention.hpp:96
+  const double* qb = q + b * p.N * p.ldq + j * p.d;
+  const double* kb = k + b * p.N * p.ldk + j * p.d;
+  const double* vb = v + b * p.N * p.ldv + j * p.dv;
+  double* ob = o + b * p.N * p.ldo + j * p.dv;
+  float* lb = lse ? lse + (b * p.h + j) * p.N : nullptr;
+  if (chunk == 0) {  // rows the view does not select: exact zeros (attention.hpp:243-245, 270)
+    for (int64_t l = tid; l < seg_rows; l += blockDim.x) {
+      if (l % p.r == g && l >= g) continue;
+      double* orow = ob + (seg_begin + l) * p.ldo;
+      for (int64_t c = 0; c < p.dv; ++c) orow[c] = 0.0;
+      if (lb) lb[seg_begin + l] = -INFINITY;
+    }
+  }
+  if (chunk * 128 >= m) return;
+  const int64_t t = chunk * 128 + tid;
+  const bool active = t < m;
+  const int64_t row = seg_begin + g + t * p.r;
+  double qr[DMAX], acc[DMAX];
+#pragma unroll
+  for (int c = 0; c < DMAX; ++c) {
+    qr[c] = (active && c < p.d) ? qb[row * p.ldq + c] : 0.0;
+    acc[c] = 0.0;
+  }
+  double mx = -INFINITY, l = 0.0;
+  for (int64_t k0 = 0; k0 < m; k0 += KT) {
+    __syncthreads();
+    for (int e = tid; e < KT * DMAX; e += blockDim.x) {
+      const int jj = e / DMAX, c = e % DMAX;
+      const int64_t tk = k0 + jj;
+      const int64_t krow = seg_begin + g + tk * p.r;
+      ks[jj][c] = (tk < m && c < p.d) ? kb[krow * p.ldk + c] : 0.0;
+      vs[jj][c] = (tk < m && c < p.dv) ? vb[krow * p.ldv + c] : 0.0;
+    }
+    __syncthreads();
+    if (!active) continue;
+    double s[KT];
+    double tmax = -INFINITY;
+#pragma unroll
+    for (int jj = 0; jj < KT; ++jj) {
+      double dot = 0.0;
+#pragma unroll
+      for (int c = 0; c < DMAX; ++c) dot = fma(qr[c], ks[jj][c], dot);
+      s[jj] = (k0 + jj < m) ? dot * p.scale64 : -INFINITY;
+      tmax = fmax(tmax, s[jj]);
+    }
+    const double nmax = fmax(mx, tmax);
+    const double corr = exp(mx - nmax);
+    l *= corr;
+#pragma unroll
+    for (int c = 0; c < DMAX; ++c) acc[c] *= corr;
+#pragma unroll
+    for (int jj = 0; jj < KT; ++jj) {
+      const double pj = exp(s[jj] - nmax);
+      l += pj;
+#pragma unroll
+      for (int c = 0; c < DMAX; ++c) acc[c] = fma(pj, vs[jj][c], acc[c]);
+    }
+    mx = nmax;
+  }
+  if (active) {
+    const double inv = 1.0 / l;
+    double* orow = ob + row * p.ldo;
+#pragma unroll
+    for (int c = 0; c < DMAX; ++c)
+      if (c < p.dv) orow[c] = acc[c] * inv;
+    if (lb) lb[row] = (float)(mx + log(l));
+  }
+}
+
+template <int DMAX, int KT>
+int launch_f64(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
+               cudaStream_t stream, cudaError_t* err) {
+  SimtParams p;
+  p.N = g.N;
+  p.w = g.w;
+  p.r = g.r;
+  p.h = g.h;
+  p.d = g.d;
+  p.dv = g.dv;
+  p.ldq = g.ldq;
+  p.ldk = g.ldk;
+  p.ldv = g.ldv;
+  p.ldo = g.ldo;
+  p.n_chunks = std::max<int64_t>(1, (g.m_max + 127) / 128);
+  p.scale = g.scale;
+  p.scale64 = g.scale == 1.0f ? 1.0 : 1.0 / sqrt((double)g.d);
+  for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
+  dim3 grid((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
+  simt_f64_kernel<DMAX, KT><<<grid, 128, 0, stream>>>((const double*)q, (const double*)k, (const double*)v,
+                                                      (double*)o, lse, p);
+  *err = cudaGetLastError();
+  return 1;
+}
+
 template <typename T, int DMAX, int KT>
 int launch_t(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
              cudaStream_t stream, cudaError_t* err) {
@@ -332,11 +452,23 @@ __global__ void perturb_kernel(T* o) {
 int launch_simt(const Geometry& g, int dtype, const void* q, const void* k, const void* v, void* o, float* lse,
                 cudaStream_t stream, cudaError_t* err) {
   if (dtype == 0) return launch_dtype<float>(g, q, k, v, o, lse, stream, err);
+  if (dtype == 2) {
+    const int64_t dm = g.d > g.dv ? g.d : g.dv;
+    if (dm <= 16) return launch_f64<16, 32>(g, q, k, v, o, lse, stream, err);
+    if (dm <= 32) return launch_f64<32, 32>(g, q, k, v, o, lse, stream, err);
+    if (dm <= 64) return launch_f64<64, 16>(g, q, k, v, o, lse, stream, err);
+    if (dm <= 128) return launch_f64<128, 8>(g, q, k, v, o, lse, stream, err);
+    return launch_f64<256, 4>(g, q, k, v, o, lse, stream, err);
+  }
   return launch_dtype<__nv_bfloat16>(g, q, k, v, o, lse, stream, err);
 }
 
+__global__ void perturb_f64_kernel(double* o) { o[0] += 1e-3; }
+
 int launch_perturb(int dtype, void* o, cudaStream_t stream) {
-  if (dtype == 0)
+  if (dtype == 2)
+    perturb_f64_kernel<<<1, 1, 0, stream>>>((double*)o);
+  else if (dtype == 0)
     perturb_kernel<float><<<1, 1, 0, stream>>>((float*)o);
   else
     perturb_kernel<__nv_bfloat16><<<1, 1, 0, stream>>>((__nv_bfloat16*)o);

@@ -46,3 +46,15 @@ def test_cpp_multi_head_dilated_vs_reference(binary, ref, tmp_path):
     wq, wk, wv = (np.stack([ld(f"mh_{n}{j}", (128, 64)) for j in range(2)]) for n in ("wq", "wk", "wv"))
     want = ref.multi_head_dilated(x, wq, wk, wv, wo, 64, 2)
     assert np.abs(y - want).max() <= 1e-4 * max(1.0, np.abs(want).max())
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_gates_through_dfa_hpp(binary):
+    """The reference's acceptance gates 1 (masked oracle, f64, 1e-10), 3
+    (collapse, f32, 1e-6) and 8 (worker determinism, f64, bitwise) with the
+    reference's seeds and draws, every dilated_attention call going through
+    dfa::dilated_attention (float -> fp32 kernel, double -> f64 kernel)."""
+    r = subprocess.run([binary, "gates"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    for gate in (1, 3, 8):
+        assert f"GATE {gate} " in r.stdout and "FAIL" not in r.stdout, r.stdout

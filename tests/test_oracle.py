@@ -260,3 +260,21 @@ def test_lse_oracle_definition(port):
     for i in range(n // w):
         sel[i * w + g: i * w + w: r] = True
     assert np.isneginf(lse[~sel]).all()
+
+
+def test_batched_oracle_drivers_match_per_head_calls(port):
+    """The threaded [B, N, h, d] drivers used by the full-batch GPU parity
+    tests run exactly the pinned single-head restatement per (image, head)."""
+    rng = np.random.default_rng(5)
+    B, n, h, d = 2, 96, 3, 8
+    q, k, v = (rng.standard_normal((B, n, h, d)) for _ in range(3))
+    offs = [0, 1, 1]
+    out = port.dilated_batched(q, k, v, 32, 2, offs, threads=3)
+    br = [(32, 1, [0, 0, 0]), (48, 2, offs)]
+    mb, mbl = port.multibranch_batched(q, k, v, br, threads=2)
+    for b in range(B):
+        for j in range(h):
+            assert np.array_equal(out[b, :, j], port.dilated_attention(q[b, :, j], k[b, :, j], v[b, :, j], 32, 2,
+                                                                       offs[j]))
+            o1, l1 = port.multibranch(q[b, :, j], k[b, :, j], v[b, :, j], [(w, r, g[j]) for w, r, g in br])
+            assert np.array_equal(mb[b, :, j], o1) and np.array_equal(mbl[b, j], l1)
