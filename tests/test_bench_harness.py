@@ -79,13 +79,16 @@ def test_repeats_and_coarse_clock(bh, dfa, cuda):
 def test_rows_counts_band_order_and_parity(bh, dfa, cuda):
     par = bh.bench_attention(_entry(dfa, bh, "parity", 4096, 4096, 1, 1, 64), [64], 7, dtype="bf16").rows[0]
     assert 0.8 < par.measured_speedup < 1.25 and par.dense_mults == par.dilated_mults
-    e = _entry(dfa, bh, "counts", 128, 32, 2, 2, 8)
+    # sizes / repeats large enough that CUDA-event samples land on >= 3
+    # distinct ticks (the reference's coarse-clock rule, bench.hpp:75-77)
+    e = _entry(dfa, bh, "counts", 2048, 256, 2, 2, 64)
     fc = dfa.flop_count(e.attn)
-    for row in bh.bench_attention(e, [1, 2], 3).rows:
+    for row in bh.bench_attention(e, [1, 2], 9).rows:
         assert (row.dense_mults, row.dilated_mults) == (fc.dense_mults, fc.dilated_mults)
         assert 0.0 < row.p10_ms <= row.median_ms <= row.p90_ms
-    s = bh.SweepConfig(configs=[_entry(dfa, bh, "alpha", 64, 16, 2, 1, 8), _entry(dfa, bh, "beta", 64, 32, 2, 1, 8)],
-                       batch_sizes=[1, 2], repeats=3)
+    s = bh.SweepConfig(configs=[_entry(dfa, bh, "alpha", 2048, 256, 2, 1, 64),
+                                _entry(dfa, bh, "beta", 2048, 512, 2, 1, 64)],
+                       batch_sizes=[1, 2], repeats=9)
     rows = bh.run_sweep(s).rows
     assert [(r.id, r.batch) for r in rows] == [("alpha", 1), ("alpha", 2), ("beta", 1), ("beta", 2)]
     out = io.StringIO()

@@ -84,8 +84,8 @@ def test_config5_batch_decomposition(dfa, cuda):
 def test_segment_sharded_forward_is_bit_identical(dfa, cuda, n, w, r, world):
     """dist.segment_local_forward's partition (whole segments per rank, the
     unchanged kernel on each N' = stop - start problem, tail-only shards
-    included) reproduces the one-GPU output bit for bit -- every rank's part
-    computed here on one GPU."""
+    included) reproduces the one-GPU output -- bit for bit when segments align
+    with the 128-row key tiles -- every rank's part computed here on one GPU."""
     import torch
     from paper_2403_09195_b200.dist import segment_local_forward
 
@@ -95,4 +95,13 @@ def test_segment_sharded_forward_is_bit_identical(dfa, cuda, n, w, r, world):
     full = dfa.dfa_forward(q, k, v, cfg)
     parts = [segment_local_forward(q, k, v, cfg, rank, world) for rank in range(world)]
     torch.cuda.synchronize()
-    assert torch.equal(torch.cat(parts, dim=1), full)
+    got = torch.cat(parts, dim=1)
+    if n % w == 0 and (w // r) % 128 == 0:
+        # segments align with the kernel's 128-row key tiles in both problems:
+        # the same MMAs in the same order, bit for bit
+        assert torch.equal(got, full)
+    else:
+        # a tail segment (or a different kernel for the local N') tiles its
+        # keys differently: the same math to bf16 accuracy, zero rows exact
+        assert (got.float() - full.float()).abs().max().item() <= 2e-2
+        assert torch.equal(got == 0, full == 0)
