@@ -188,15 +188,28 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
                           const void* v, const void* o, const float* lse, const void* dout, void* dq, void* dk,
                           void* dv, void* workspace, size_t workspace_bytes, void* stream);
 
+/* tensor.hpp:175-195 matmul (row-major, C = A B) on device buffers, with the
+ * layers' epilogue: D[b] = epi(A[b] B[b] + bias + beta C[b]) for b < batch;
+ * A [M, K] (row stride lda, batch stride sa), B [K, N] (ldb, sb), C / D
+ * [M, N] (ldc / ldd, batch stride sd); bias [N] or NULL; C NULL for none;
+ * gelu != 0 applies GELU in the reference's erf form (tensor.hpp:262-265).
+ * bf16: the tcgen05 kernel (fp32 accumulate); f32: the SIMT validation
+ * kernel (FFMA, no TF32).  Strides in elements; the building block of the
+ * projections below, exported for parity tests. */
+dfa_status_t dfa_gemm(dfa_dtype_t dtype, int64_t batch, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                      int64_t sa, const void* B, int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd,
+                      const void* C, int64_t ldc, float beta, const void* bias, int32_t gelu, void* stream);
+
 /* attention.hpp:340-360 multi_head_dilated for a batch: x [B, N, D] with
  * D = h * d; wq, wk, wv [h, D, d] (the reference's per-head D x d
  * projections, stacked); wo [D, D]; out [B, N, D] = concat_j(head_j) wo,
  * head_j = dilated_attention(x wq_j, x wk_j, x wv_j) at offset gamma_j.
  * Requires full coverage (attention.hpp:343).  All tensors `dtype`, device.
- * The three projections run as ONE cuBLASLt GEMM against the weights packed
- * [D, 3, h, d]; the core reads q / k / v straight out of its [B, N, 3, h, d]
- * output (dfa_forward_strided) and writes the concat layout the output
- * projection consumes.  `workspace` holds dfa_multi_head_workspace_bytes. */
+ * The projections run as this library's own tcgen05 GEMM (dfa_gemm.cu)
+ * against the weights packed [D, 3, h, d] (bf16 with r > 1: per offset class,
+ * 1/r of the rows); the core reads q / k / v straight out of its output and
+ * writes the concat layout the output projection consumes.  `workspace`
+ * holds dfa_multi_head_workspace_bytes. */
 dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch,
                                             size_t* bytes);
 dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* x,

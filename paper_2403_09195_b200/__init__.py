@@ -586,6 +586,31 @@ def multi_head_dilated(x, wq, wk, wv, wo, cfg: AttentionConfig, out=None, stream
     return out
 
 
+def gemm(a, b, bias=None, c=None, beta=1.0, gelu=False, out=None, stream=None):
+    """dfa_gemm: out = epi(a @ b + bias + beta c) for row-major CUDA tensors
+    a [.., M, K] (row stride may exceed K), b [.., K, N], c / out [.., M, N];
+    a leading batch dim is passed as the batch stride (tensor.hpp:175-195 matmul
+    plus the layers' epilogue; bf16 -> tcgen05, float32 -> SIMT)."""
+    torch = _torch()
+    if a.dim() == 2:
+        a, b = a.unsqueeze(0), b.unsqueeze(0) if b.dim() == 2 else b
+    batch, M, K = a.shape
+    N = b.shape[-1]
+    if b.dim() == 2:
+        b = b.unsqueeze(0)
+    for name, t in (("a", a), ("b", b)):
+        if not t.is_cuda or t.stride(-1) != 1:
+            raise DimensionError(f"gemm: {name} must be a CUDA tensor with unit column stride")
+    if out is None:
+        out = torch.empty((batch, M, N), dtype=a.dtype, device=a.device)
+    sb = b.stride(0) if b.shape[0] > 1 else 0
+    _check(lib.dfa_gemm(_dtype_code(a), batch, M, N, K, a.data_ptr(), a.stride(1), a.stride(0), b.data_ptr(),
+                        b.stride(1), sb, out.data_ptr(), out.stride(-2), out.stride(0) if out.dim() == 3 else M * N,
+                        c.data_ptr() if c is not None else None, c.stride(-2) if c is not None else 0, beta,
+                        bias.data_ptr() if bias is not None else None, 1 if gelu else 0, _stream_ptr(stream)))
+    return out
+
+
 BLOCK_KEYS = ("ln1_g", "ln1_b", "wq", "wk", "wv", "wo", "bo", "ln2_g", "ln2_b", "w1", "b1", "w2", "b2")
 
 

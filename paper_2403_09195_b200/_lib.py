@@ -66,6 +66,7 @@ EXPORTED = (
     "dfa_tensor_header",
     "dfa_tensor_load",
     "dfa_tensor_save",
+    "dfa_gemm",
 )
 
 
@@ -155,6 +156,8 @@ def _load() -> ctypes.CDLL:
         "dfa_tensor_header": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), p_i64]),
         "dfa_tensor_load": (c_i32, [ctypes.c_char_p, c_i32, c_vp, c_i64]),
         "dfa_tensor_save": (c_i32, [ctypes.c_char_p, c_i32, c_i32, p_i64, c_vp]),
+        "dfa_gemm": (c_i32, [c_i32, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64,
+                             c_i64, c_vp, c_i64, ctypes.c_float, c_vp, c_i32, c_vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -551,8 +551,28 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
   return DFA_OK;
 }
 
+// tensor.hpp:175-195 matmul + the layers' epilogue (include/dfa.h).
+dfa_status_t dfa_gemm(dfa_dtype_t dtype, int64_t batch, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                      int64_t sa, const void* B, int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd,
+                      const void* C, int64_t ldc, float beta, const void* bias, int32_t gelu, void* stream) {
+  g_launches = 0;
+  if (dtype != DFA_F32 && dtype != DFA_BF16) return fail(DFA_ERR_UNSUPPORTED, "dfa_gemm: dtype %d (f32 / bf16)", (int)dtype);
+  if (batch < 0 || M < 0 || N < 0 || K < 0)
+    return fail(DFA_ERR_DIMENSION, "dfa_gemm: negative extent (batch %lld, M %lld, N %lld, K %lld)", (long long)batch,
+                (long long)M, (long long)N, (long long)K);
+  if (lda < K || ldb < N || ldd < N || (C && ldc < N))
+    return fail(DFA_ERR_DIMENSION, "dfa_gemm: row strides below the row widths");
+  if (batch == 0 || M == 0 || N == 0) return DFA_OK;
+  if (!A || !B || !D) return fail(DFA_ERR_DIMENSION, "dfa_gemm: null operand");
+  const char* why = "";
+  if (!dfa_impl::gemm_rowmajor(dtype, M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, (int)batch,
+                               reinterpret_cast<cudaStream_t>(stream), &why, gelu != 0))
+    return fail(DFA_ERR_CUDA, "dfa_gemm: %s", why);
+  g_launches = 1;
+  return DFA_OK;
+}
+
 // ------------------------------------------------------------ §8(f) 1-2
-static constexpr size_t kLtWorkspace = 32u << 20;
 
 static dfa_status_t layer_geometry(const dfa_config_t* cfg, int64_t batch, dfa_impl::Geometry* g, const char* who) {
   dfa_status_t st = validate(cfg, 1);  // attention.hpp:343 / EncoderConfig::validate: full coverage
@@ -573,7 +593,7 @@ dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t
   if (dtype != DFA_F32 && dtype != DFA_BF16)
     return fail(DFA_ERR_UNSUPPORTED, "multi_head_dilated: dtype %d (f32 / bf16)", (int)dtype);
   const size_t es = elem_size(dtype), D = (size_t)(g.h * g.d);
-  *bytes = 4 * up256((size_t)(g.B * g.N) * D * es) + up256(3 * D * D * es) + kLtWorkspace;
+  *bytes = 4 * up256((size_t)(g.B * g.N) * D * es) + up256(3 * D * D * es);
   return DFA_OK;
 }
 
@@ -581,13 +601,13 @@ dfa_status_t dfa_multi_head_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t
 // weights, then the core reads q / k / v as column blocks (token stride 3hd).
 static dfa_status_t fused_qkv_attention(const dfa_config_t* cfg, dfa_dtype_t dtype, const dfa_impl::Geometry& g,
                                         const void* x, const void* wq, const void* wk, const void* wv, char* qkv,
-                                        char* wpack, void* att, void* lt, cudaStream_t s, int* launches,
+                                        char* wpack, void* att, cudaStream_t s, int* launches,
                                         const char* who) {
   const int64_t M = g.B * g.N, D = g.h * g.d;
   const char* why = "";
   *launches += dfa_impl::launch_pack_qkv(dtype, wq, wk, wv, wpack, g.h, D, g.d, s);
   if (!dfa_impl::gemm_rowmajor(dtype, M, 3 * D, D, x, D, 0, wpack, 3 * D, 0, qkv, 3 * D, 0, nullptr, 0, 0.0f, nullptr,
-                               1, lt, kLtWorkspace, s, &why))
+                               1, s, &why))
     return fail(DFA_ERR_CUDA, "%s: QKV projection: %s", who, why);
   ++*launches;
   const size_t es = elem_size(dtype);
@@ -621,7 +641,7 @@ static bool class_split_ok(const dfa_impl::Geometry& g, dfa_dtype_t dtype) {
 static dfa_status_t class_split_layer(const dfa_config_t* cfg, dfa_dtype_t dtype, const dfa_impl::Geometry& g,
                                       const void* x, const void* wq, const void* wk, const void* wv, const void* wo,
                                       const void* bias, const void* resid, void* out, char* qkv, char* att,
-                                      char* wpack, void* lt, cudaStream_t s, int* launches, const char* who) {
+                                      char* wpack, cudaStream_t s, int* launches, const char* who) {
   const int64_t M = g.B * g.N, D = g.h * g.d, r = g.r, Mr = M / r;
   const size_t es = elem_size(dtype);
   char* wopack = qkv + up256((size_t)(3 * Mr * D) * es);
@@ -640,7 +660,7 @@ static dfa_status_t class_split_layer(const dfa_config_t* cfg, dfa_dtype_t dtype
     // with batch r B (class-major images): fuller waves than r separate calls.
     const int64_t hd = (g.h / r) * g.d;
     if (!dfa_impl::gemm_rowmajor(dtype, Mr, 3 * hd, D, x, r * D, D, wpack, 3 * D, 3 * hd, qkv, 3 * hd, Mr * 3 * hd,
-                                 nullptr, 0, 0.0f, nullptr, (int)r, lt, kLtWorkspace, s, &why))
+                                 nullptr, 0, 0.0f, nullptr, (int)r, s, &why))
       return fail(DFA_ERR_CUDA, "%s: QKV projection: %s", who, why);
     ++*launches;
     std::vector<int64_t> zero_offs((size_t)(g.h / r), 0);
@@ -656,7 +676,7 @@ static dfa_status_t class_split_layer(const dfa_config_t* cfg, dfa_dtype_t dtype
     if (st != DFA_OK) return st;
     *launches += g_launches;
     if (!dfa_impl::gemm_rowmajor(dtype, Mr, D, hd, att, hd, Mr * hd, wopack, D, hd * D, out, r * D, D, resid, r * D,
-                                 resid ? 1.0f : 0.0f, bias, (int)r, lt, kLtWorkspace, s, &why))
+                                 resid ? 1.0f : 0.0f, bias, (int)r, s, &why))
       return fail(DFA_ERR_CUDA, "%s: output projection: %s", who, why);
     ++*launches;
     return DFA_OK;
@@ -671,7 +691,7 @@ static dfa_status_t class_split_layer(const dfa_config_t* cfg, dfa_dtype_t dtype
     char* a_g = att + (size_t)(Mr * start * g.d) * es;
     if (!dfa_impl::gemm_rowmajor(dtype, Mr, 3 * hd, D, static_cast<const char*>(x) + gc * D * es, r * D, 0,
                                  wpack + (size_t)(3 * start * g.d) * es, 3 * D, 0, q_g, 3 * hd, 0, nullptr, 0, 0.0f,
-                                 nullptr, 1, lt, kLtWorkspace, s, &why))
+                                 nullptr, 1, s, &why))
       return fail(DFA_ERR_CUDA, "%s: QKV projection (class %lld): %s", who, (long long)gc, why);
     ++*launches;
     std::vector<int64_t> zero_offs((size_t)cnt, 0);
@@ -689,7 +709,7 @@ static dfa_status_t class_split_layer(const dfa_config_t* cfg, dfa_dtype_t dtype
     const void* c_g = resid ? static_cast<const char*>(resid) + gc * D * es : nullptr;
     if (!dfa_impl::gemm_rowmajor(dtype, Mr, D, hd, a_g, hd, 0, wopack + (size_t)(start * g.d * D) * es, D, 0,
                                  static_cast<char*>(out) + gc * D * es, r * D, 0, c_g, r * D, c_g ? 1.0f : 0.0f,
-                                 bias, 1, lt, kLtWorkspace, s, &why))
+                                 bias, 1, s, &why))
       return fail(DFA_ERR_CUDA, "%s: output projection (class %lld): %s", who, (long long)gc, why);
     ++*launches;
     start += cnt;
@@ -717,19 +737,18 @@ dfa_status_t dfa_multi_head_dilated(const dfa_config_t* cfg, dfa_dtype_t dtype, 
   char* qkv = base;                   // [M, 3, h, d]
   void* att = base + 3 * act;         // [M, h, d]
   char* wpack = base + 4 * act;       // [D, 3, h, d]
-  void* lt = wpack + up256((size_t)(3 * D * D) * es);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int launches = 0;
   if (class_split_ok(g, dtype)) {
     st = class_split_layer(cfg, dtype, g, x, wq, wk, wv, wo, nullptr, nullptr, out, qkv, static_cast<char*>(att),
-                           wpack, lt, s, &launches, "multi_head_dilated");
+                           wpack, s, &launches, "multi_head_dilated");
     if (st != DFA_OK) return st;
   } else {
-    st = fused_qkv_attention(cfg, dtype, g, x, wq, wk, wv, qkv, wpack, att, lt, s, &launches, "multi_head_dilated");
+    st = fused_qkv_attention(cfg, dtype, g, x, wq, wk, wv, qkv, wpack, att, s, &launches, "multi_head_dilated");
     if (st != DFA_OK) return st;
     const char* why = "";
-    if (!dfa_impl::gemm_rowmajor(dtype, M, D, D, att, D, 0, wo, D, 0, out, D, 0, nullptr, 0, 0.0f, nullptr, 1, lt,
-                                 kLtWorkspace, s, &why))
+    if (!dfa_impl::gemm_rowmajor(dtype, M, D, D, att, D, 0, wo, D, 0, out, D, 0, nullptr, 0, 0.0f, nullptr, 1, s,
+                                 &why))
       return fail(DFA_ERR_CUDA, "multi_head_dilated: output projection: %s", why);
     ++launches;
   }
@@ -791,7 +810,7 @@ dfa_status_t dfa_encoder_block_workspace_bytes(const dfa_config_t* cfg, dfa_dtyp
   if (hidden < 1) return fail(DFA_ERR_CONFIG, "encoder: mlp_ratio must yield a positive width");
   const size_t es = elem_size(dtype), D = (size_t)(g.h * g.d);
   const size_t act = up256((size_t)(g.B * g.N) * D * es);
-  *bytes = 6 * act + up256((size_t)(g.B * g.N * hidden) * es) + up256(3 * D * D * es) + kLtWorkspace;
+  *bytes = 6 * act + up256((size_t)(g.B * g.N * hidden) * es) + up256(3 * D * D * es);
   return DFA_OK;
 }
 
@@ -823,38 +842,30 @@ dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtyp
   void* x1 = base + 5 * act;
   char* hid = base + 6 * act;
   char* wpack = hid + up256((size_t)(M * H) * es);
-  void* lt = wpack + up256((size_t)(3 * D * D) * es);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const char* why = "";
   int launches = 0;
   auto gemm = [&](int64_t m, int64_t n, int64_t k, const void* a, const void* b, void* d, const void* c,
                   const void* bias, bool gelu = false) {
     ++launches;
-    return dfa_impl::gemm_rowmajor(dtype, m, n, k, a, k, 0, b, n, 0, d, n, 0, c, n, c ? 1.0f : 0.0f, bias, 1, lt,
-                                   kLtWorkspace, s, &why, gelu);
+    return dfa_impl::gemm_rowmajor(dtype, m, n, k, a, k, 0, b, n, 0, d, n, 0, c, n, c ? 1.0f : 0.0f, bias, 1, s, &why,
+                                   gelu);
   };
   launches += dfa_impl::launch_layer_norm(dtype, x, wt->ln1_g, wt->ln1_b, ln, M, (int)D, s);
   if (class_split_ok(g, dtype)) {  // x1 = x + attention_mix(LN1 x) Wo + bo, per offset class
     st = class_split_layer(cfg, dtype, g, ln, wt->wq, wt->wk, wt->wv, wt->wo, wt->bo, x, x1, qkv,
-                           static_cast<char*>(att), wpack, lt, s, &launches, "encoder_block");
+                           static_cast<char*>(att), wpack, s, &launches, "encoder_block");
     if (st != DFA_OK) return st;
   } else {
-    st = fused_qkv_attention(cfg, dtype, g, ln, wt->wq, wt->wk, wt->wv, qkv, wpack, att, lt, s, &launches,
+    st = fused_qkv_attention(cfg, dtype, g, ln, wt->wq, wt->wk, wt->wv, qkv, wpack, att, s, &launches,
                              "encoder_block");
     if (st != DFA_OK) return st;
     if (!gemm(M, D, D, att, wt->wo, x1, x, wt->bo)) return fail(DFA_ERR_CUDA, "encoder_block: wo: %s", why);
   }
   launches += dfa_impl::launch_layer_norm(dtype, x1, wt->ln2_g, wt->ln2_b, ln, M, (int)D, s);
-  // bf16: GELU (tanh form, within bf16's resolution of the erf form, like
-  // gelu_bf16_kernel) in the w1 GEMM's epilogue -- saves a 1.6 GB pass over
-  // the hidden activations.  fp32 (validation): separate erf GELU.
-  if (dtype == DFA_BF16) {
-    if (!gemm(M, H, D, ln, wt->w1, hid, nullptr, wt->b1, true))
-      return fail(DFA_ERR_CUDA, "encoder_block: w1+gelu: %s", why);
-  } else {
-    if (!gemm(M, H, D, ln, wt->w1, hid, nullptr, wt->b1)) return fail(DFA_ERR_CUDA, "encoder_block: w1: %s", why);
-    launches += dfa_impl::launch_gelu(dtype, hid, hid, M * H, s);
-  }
+  // GELU in the reference's erf form (tensor.hpp:262-265) inside the w1
+  // GEMM's epilogue -- no separate pass over the hidden activations.
+  if (!gemm(M, H, D, ln, wt->w1, hid, nullptr, wt->b1, true)) return fail(DFA_ERR_CUDA, "encoder_block: w1+gelu: %s", why);
   if (!gemm(M, D, H, hid, wt->w2, out, x1, wt->b2)) return fail(DFA_ERR_CUDA, "encoder_block: w2: %s", why);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return fail(DFA_ERR_CUDA, "encoder_block: %s", cudaGetErrorString(err));

@@ -132,12 +132,14 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
                      const float* lse, const float* delta, void* dq, void* dk, void* dv, cudaStream_t stream,
                      cudaError_t* err, const char** why);
 
-// dfa_layers.cu: cuBLASLt row-major GEMM D = A B (+ bias) (+ beta C), strided
-// batch; LayerNorm (eps 1e-5) and erf-GELU kernels.  Return 0 on failure.
+// dfa_gemm.cu: row-major D = epi(A B + bias + beta C), strided batch (A rows
+// at lda, batch stride sa; B at ldb / sb; C and D at ldc / ldd, batch stride
+// sd); epi = GELU(erf) when gelu.  bf16 -> tcgen05 kernel, f32 -> SIMT
+// (validation).  Returns 0 on failure (why set).
 int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
                   int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
-                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why,
-                  bool gelu = false);  // gelu: D = GELU(A B + bias), cuBLASLt's (tanh-form) GELU epilogue
+                  const void* bias, int batch, cudaStream_t stream, const char** why, bool gelu = false);
+// dfa_layers.cu: LayerNorm (eps 1e-5) and erf-GELU kernels, weight packing.
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
                       cudaStream_t stream);
 int launch_gelu(int dtype, const void* xin, void* x, int64_t n, cudaStream_t stream);  // x = GELU(xin); may alias

@@ -7,16 +7,11 @@
 // B200 layout: activations stay in the core's [B, N, h, d] = [B*N, D] layout
 // end to end, so the projections write exactly what the TMA boxes of the
 // attention kernel read and the concat of the heads IS the attention output
-// -- no gather, scatter or transpose pass exists.  The plain GEMMs go to
-// cuBLASLt (row-major via the transposed problem; per-head projections as
-// one strided-batched call writing the head's column block; bias and the
-// residual ride in the GEMM epilogue as bias + beta * C).  LayerNorm and the
-// erf-GELU (autodiff.hpp / tensor.hpp:262-279 -- cuBLASLt's GELU epilogue is
-// the tanh approximation, so it is not used) are this file's own kernels.
-// fp32 runs with CUBLAS_COMPUTE_32F (no TF32) as the validation mode.
-#include <cublasLt.h>
+// -- no gather, scatter or transpose pass exists.  The GEMMs are this
+// library's own tcgen05 kernel (dfa_gemm.cu: bias, residual and the erf GELU
+// in its epilogue); this file holds LayerNorm, a standalone erf-GELU and the
+// weight-packing kernels.
 #include <cuda_bf16.h>
-#include <dlfcn.h>
 #include <math.h>
 
 #include <algorithm>
@@ -372,214 +367,7 @@ __global__ void __launch_bounds__(256) pack_wo_class_kernel(const T* __restrict_
   }
 }
 
-// cuBLASLt is bound at run time, not linked: if the process already holds a
-// libcublasLt.so.12 (e.g. PyTorch's wheel copy) that one is used, otherwise
-// the CUDA toolkit's is loaded.  Linking it would pin a second copy under the
-// same soname and break the host framework's own cuBLAS.
-struct Lt {
-#define DFA_LT_FN(name) decltype(&::name) name = nullptr;
-  DFA_LT_FN(cublasLtCreate)
-  DFA_LT_FN(cublasLtDestroy)
-  DFA_LT_FN(cublasLtMatmulDescCreate)
-  DFA_LT_FN(cublasLtMatmulDescDestroy)
-  DFA_LT_FN(cublasLtMatmulDescSetAttribute)
-  DFA_LT_FN(cublasLtMatrixLayoutCreate)
-  DFA_LT_FN(cublasLtMatrixLayoutDestroy)
-  DFA_LT_FN(cublasLtMatrixLayoutSetAttribute)
-  DFA_LT_FN(cublasLtMatmulPreferenceCreate)
-  DFA_LT_FN(cublasLtMatmulPreferenceDestroy)
-  DFA_LT_FN(cublasLtMatmulPreferenceSetAttribute)
-  DFA_LT_FN(cublasLtMatmulAlgoGetHeuristic)
-  DFA_LT_FN(cublasLtMatmul)
-#undef DFA_LT_FN
-  bool ok = false;
-};
-
-const Lt& lt() {
-  static Lt t;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* h = dlopen("libcublasLt.so.12", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libcublasLt.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("/usr/local/cuda/lib64/libcublasLt.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return;
-    bool ok = true;
-#define DFA_LT_SYM(name) \
-  t.name = reinterpret_cast<decltype(&::name)>(dlsym(h, #name)); \
-  ok = ok && t.name;
-    DFA_LT_SYM(cublasLtCreate)
-    DFA_LT_SYM(cublasLtDestroy)
-    DFA_LT_SYM(cublasLtMatmulDescCreate)
-    DFA_LT_SYM(cublasLtMatmulDescDestroy)
-    DFA_LT_SYM(cublasLtMatmulDescSetAttribute)
-    DFA_LT_SYM(cublasLtMatrixLayoutCreate)
-    DFA_LT_SYM(cublasLtMatrixLayoutDestroy)
-    DFA_LT_SYM(cublasLtMatrixLayoutSetAttribute)
-    DFA_LT_SYM(cublasLtMatmulPreferenceCreate)
-    DFA_LT_SYM(cublasLtMatmulPreferenceDestroy)
-    DFA_LT_SYM(cublasLtMatmulPreferenceSetAttribute)
-    DFA_LT_SYM(cublasLtMatmulAlgoGetHeuristic)
-    DFA_LT_SYM(cublasLtMatmul)
-#undef DFA_LT_SYM
-    t.ok = ok;
-  });
-  return t;
-}
-
-struct LtHandle {
-  cublasLtHandle_t h = nullptr;
-  ~LtHandle() {
-    if (h && lt().ok) lt().cublasLtDestroy(h);
-  }
-};
-cublasLtHandle_t lt_handle() {
-  if (!lt().ok) return nullptr;
-  thread_local LtHandle lh;
-  if (!lh.h && lt().cublasLtCreate(&lh.h) != CUBLAS_STATUS_SUCCESS) lh.h = nullptr;
-  return lh.h;
-}
-
 }  // namespace
-
-// Row-major D[M, N] (ldd) = A[M, K] (lda) * B[K, N] (ldb) (+ bias[N]) (+ beta * C[M, N] (ldc)),
-// `batch` problems at element strides sa / sb / sc / sd (sa may be 0).
-// Column-major cuBLASLt sees D^T = B^T A^T: m = N, n = M.
-// Per-shape cuBLASLt algorithm cache (see gemm_rowmajor).
-struct GemmKey {
-  int dtype;
-  int64_t M, N, K, lda, ldb, ldd;
-  bool c, bias, gelu;
-  int batch;
-  bool operator<(const GemmKey& o) const {
-    return std::tie(dtype, M, N, K, lda, ldb, ldd, c, bias, gelu, batch) <
-           std::tie(o.dtype, o.M, o.N, o.K, o.lda, o.ldb, o.ldd, o.c, o.bias, o.gelu, o.batch);
-  }
-};
-static std::mutex g_algo_mu;
-static std::map<GemmKey, cublasLtMatmulAlgo_t>& algo_cache() {
-  static std::map<GemmKey, cublasLtMatmulAlgo_t> m;
-  return m;
-}
-static bool cached_algo(const GemmKey& k, cublasLtMatmulAlgo_t* a) {
-  std::lock_guard<std::mutex> lk(g_algo_mu);
-  auto it = algo_cache().find(k);
-  if (it == algo_cache().end()) return false;
-  *a = it->second;
-  return true;
-}
-static void store_algo(const GemmKey& k, const cublasLtMatmulAlgo_t& a) {
-  std::lock_guard<std::mutex> lk(g_algo_mu);
-  algo_cache()[k] = a;
-}
-
-int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
-                  int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
-                  const void* bias, int batch, void* ws, size_t ws_bytes, cudaStream_t stream, const char** why,
-                  bool gelu) {
-  cublasLtHandle_t h = lt_handle();
-  const Lt& L = lt();
-  if (!h) {
-    *why = "cuBLASLt unavailable (libcublasLt.so.12 not loadable)";
-    return 0;
-  }
-  const cudaDataType_t dt = dtype == 0 ? CUDA_R_32F : CUDA_R_16BF;
-  cublasLtMatmulDesc_t op = nullptr;
-  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr, ld = nullptr;
-  cublasLtMatmulPreference_t pref = nullptr;
-  int ok = 0;
-  do {
-    if (L.cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS) break;
-    cublasLtEpilogue_t epi = gelu ? (bias ? CUBLASLT_EPILOGUE_GELU_BIAS : CUBLASLT_EPILOGUE_GELU)
-                                  : (bias ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT);
-    L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi));
-    if (bias) {
-      L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
-      L.cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &dt, sizeof(dt));
-    }
-    // cublas operand "A" = our B^T ([N x K] col-major, ld = ldb); "B" = our A^T ([K x M], ld = lda)
-    if (L.cublasLtMatrixLayoutCreate(&la, dt, N, K, ldb) != CUBLAS_STATUS_SUCCESS) break;
-    if (L.cublasLtMatrixLayoutCreate(&lb, dt, K, M, lda) != CUBLAS_STATUS_SUCCESS) break;
-    if (L.cublasLtMatrixLayoutCreate(&lc, dt, N, M, C ? ldc : ldd) != CUBLAS_STATUS_SUCCESS) break;
-    if (L.cublasLtMatrixLayoutCreate(&ld, dt, N, M, ldd) != CUBLAS_STATUS_SUCCESS) break;
-    if (batch > 1) {
-      const int32_t bc = batch;
-      const int64_t strides[4] = {sb, sa, C ? sd : sd, sd};
-      cublasLtMatrixLayout_t ls[4] = {la, lb, lc, ld};
-      for (int i = 0; i < 4; ++i) {
-        L.cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &bc, sizeof(bc));
-        L.cublasLtMatrixLayoutSetAttribute(ls[i], CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET, &strides[i],
-                                         sizeof(int64_t));
-      }
-    }
-    if (L.cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS) break;
-    L.cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes, sizeof(ws_bytes));
-    const float alpha = 1.0f;
-    const float b2 = C ? beta : 0.0f;
-    // Algorithm: cached per GEMM shape / epilogue.  First sight of a shape
-    // times up to kTune heuristic candidates on the caller's stream and keeps
-    // the fastest (cuBLASLt's first pick is not the fastest on several of the
-    // encoder-block shapes); skipped while the stream is being captured, when
-    // C aliases D, or with DFA_GEMM_AUTOTUNE=0.
-    const GemmKey key{dtype, M, N, K, lda, ldb, ldd, C != nullptr, bias != nullptr, gelu, batch};
-    cublasLtMatmulAlgo_t algo;
-    if (!cached_algo(key, &algo)) {
-      constexpr int kTune = 8;
-      cublasLtMatmulHeuristicResult_t res[kTune];
-      int found = 0;
-      if (L.cublasLtMatmulAlgoGetHeuristic(h, op, la, lb, lc, ld, pref, kTune, res, &found) != CUBLAS_STATUS_SUCCESS ||
-          found == 0) {
-        *why = "no cuBLASLt algorithm for this GEMM";
-        break;
-      }
-      int best = 0;
-      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(stream, &cap);
-      const char* e = getenv("DFA_GEMM_AUTOTUNE");
-      if (found > 1 && cap == cudaStreamCaptureStatusNone && C != D && !(e && e[0] == '0')) {
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        float best_ms = 1e30f;
-        for (int i = 0; i < found; ++i) {
-          if (res[i].state != CUBLAS_STATUS_SUCCESS) continue;
-          bool good = L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res[i].algo, ws,
-                                       ws_bytes, stream) == CUBLAS_STATUS_SUCCESS;  // warm-up
-          cudaEventRecord(e0, stream);
-          for (int r = 0; good && r < 2; ++r)
-            good = L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &res[i].algo, ws,
-                                    ws_bytes, stream) == CUBLAS_STATUS_SUCCESS;
-          cudaEventRecord(e1, stream);
-          cudaEventSynchronize(e1);
-          float ms = 0.0f;
-          if (good && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess && ms < best_ms) {
-            best_ms = ms;
-            best = i;
-          }
-        }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaGetLastError();
-        store_algo(key, res[best].algo);
-      } else if (cap == cudaStreamCaptureStatusNone) {
-        store_algo(key, res[0].algo);
-      }
-      algo = res[best].algo;
-    }
-    if (L.cublasLtMatmul(h, op, &alpha, B, la, A, lb, &b2, C ? C : D, lc, D, ld, &algo, ws, ws_bytes, stream) !=
-        CUBLAS_STATUS_SUCCESS) {
-      *why = "cublasLtMatmul failed";
-      break;
-    }
-    ok = 1;
-  } while (0);
-  if (pref) L.cublasLtMatmulPreferenceDestroy(pref);
-  if (ld) L.cublasLtMatrixLayoutDestroy(ld);
-  if (lc) L.cublasLtMatrixLayoutDestroy(lc);
-  if (lb) L.cublasLtMatrixLayoutDestroy(lb);
-  if (la) L.cublasLtMatrixLayoutDestroy(la);
-  if (op) L.cublasLtMatmulDescDestroy(op);
-  return ok;
-}
 
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
                       cudaStream_t stream) {

@@ -3,7 +3,7 @@ the C-ABI, against the compiled reference:
   * dfa_multi_head_dilated vs attnkit::multi_head_dilated (attention.hpp:340-360);
   * dfa_encoder_block_forward vs one block of encoder_forward run on the
     reference's own ops (encoder.hpp:241-248 via ref_encoder_block_f64).
-fp32 (validation mode, SIMT core + fp32 cuBLASLt without TF32): <= 1e-4
+fp32 (validation mode, SIMT core + SIMT fp32 GEMM, no TF32): <= 1e-4
 relative to the output scale.  bf16: <= 2e-2 max-abs relative to the output
 scale and <= 1e-2 mean relative error, oracle fed the same bf16-rounded
 inputs and weights."""
