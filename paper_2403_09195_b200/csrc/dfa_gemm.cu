@@ -48,16 +48,28 @@ constexpr int kGM = 128;        // tile rows (MMA M, TMEM lanes)
 constexpr int kGK = 64;         // K per stage: one 128-byte swizzle atom of bf16
 constexpr int kGThreads = 384;  // warps 0-3 control, 4-11 epilogue
 constexpr int kGTile = kGM * 128;  // bytes of a [128 x 64] bf16 tile
+constexpr int kPanelBytes = 144 * 1024;  // resident B panel (K x BN bf16) capacity
 
-template <int BN>
+// Two main-loop forms:
+//  * resident (kRes): the whole B panel [K x BN] of the tile's column block
+//    stays in shared memory and only A streams through the ring -- the
+//    weights are read from L2 once per panel change instead of once per
+//    tile (K <= 384 at BN = 192: the projections, w1).  Each CTA owns a
+//    contiguous range of tiles ordered (batch, n, m), so it changes panels
+//    at most a couple of times.
+//  * streaming: A and B tiles both stream (long K: w2); tiles strided over
+//    the grid with n fastest so A's rows are reused from L2.
+template <int BN, bool kRes>
 struct GemmSmem {
-  static constexpr int kStages = BN >= 256 ? 3 : 4;
+  static constexpr int kStages = kRes ? 3 : (BN >= 256 ? 3 : 4);
+  static constexpr int kBStages = kRes ? kPanelBytes / (BN / 64 * kGK * 128) : kStages;
   uint8_t a[kStages][kGTile];
-  uint8_t b[kStages][BN / 64][kGK * 128];
-  uint8_t stage[2][kGTile];  // one staging tile per epilogue group
+  uint8_t b[kBStages][BN / 64][kGK * 128];  // panel (k-tiles) or ring stages
+  uint8_t stage[2][kGTile];                 // one staging tile per epilogue group
   uint64_t full[kStages], empty[kStages];
   uint64_t acc_full[2], acc_empty[2];
   uint64_t cload[2];
+  uint64_t b_full, b_empty;                 // resident panel loaded / released
   uint32_t tmem_base;
 };
 
@@ -75,25 +87,62 @@ __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
 }
 
-__device__ __forceinline__ void decode_tile(const GemmParams& p, int32_t t, int32_t* b, int32_t* m0, int32_t* n0) {
-  const int32_t nt = t % p.nt;  // N fastest: consecutive tiles reuse A's rows from L2
-  const int32_t rest = t / p.nt;
-  *m0 = (rest % p.mt) * kGM;
-  *b = rest / p.mt;
-  *n0 = nt;  // scaled by BN by the caller
+// GELU of the bf16 epilogue: x Phi(x) with Phi(x) = (1 + tanh(y)) / 2,
+// y = x (a + b x^2 + c x^4) minimax-fitted to the erf form over |x| <= 8
+// (|x| clamped there, where Phi is 0 / 1 to fp32): max |GELU error| 2.6e-5
+// from the fit plus tanh.approx's 2^-11 relative -- below the bf16 result's
+// rounding step (2^-9 relative) -- on one MUFU op instead of erff's ~20.
+__device__ __forceinline__ float gelu_fast(float x) {
+  const float xc = fminf(fmaxf(x, -8.0f), 8.0f);
+  const float x2 = xc * xc;
+  const float y = xc * fmaf(fmaf(-3.51516789e-4f, x2, 3.70056460e-2f), x2, 7.97507884e-1f);
+  const float hx = 0.5f * x;
+  return fmaf(hx, ptx::tanh_approx(y), hx);
 }
 
-template <int BN>
+// Tile t -> (batch b, first row m0, column block nt).
+template <bool kRes>
+__device__ __forceinline__ void decode_tile(const GemmParams& p, int32_t t, int32_t* b, int32_t* m0, int32_t* nt) {
+  if (kRes) {  // (b, n, m): consecutive tiles share the B panel
+    *m0 = (t % p.mt) * kGM;
+    const int32_t rest = t / p.mt;
+    *nt = rest % p.nt;
+    *b = rest / p.nt;
+  } else {  // (b, m, n): consecutive tiles share A's rows (L2)
+    *nt = t % p.nt;
+    const int32_t rest = t / p.nt;
+    *m0 = (rest % p.mt) * kGM;
+    *b = rest / p.mt;
+  }
+}
+
+// This CTA's tiles: a contiguous range (resident) or a grid-strided set.
+template <bool kRes>
+__device__ __forceinline__ void tile_range(const GemmParams& p, int32_t* t0, int32_t* t1, int32_t* dt) {
+  if (kRes) {
+    *t0 = (int32_t)(((int64_t)blockIdx.x * p.n_tiles) / gridDim.x);
+    *t1 = (int32_t)(((int64_t)(blockIdx.x + 1) * p.n_tiles) / gridDim.x);
+    *dt = 1;
+  } else {
+    *t0 = blockIdx.x;
+    *t1 = p.n_tiles;
+    *dt = gridDim.x;
+  }
+}
+
+template <int BN, bool kRes>
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_d,
                       const __grid_constant__ GemmParams p) {
-  using Smem = GemmSmem<BN>;
+  using Smem = GemmSmem<BN, kRes>;
   constexpr int S = Smem::kStages;
   constexpr int NC = BN / 64;
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
+  int32_t t0, t1, dt;
+  tile_range<kRes>(p, &t0, &t1, &dt);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -105,6 +154,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
       ptx::mbar_init(&sm.acc_empty[b], 2 * kGM);
       ptx::mbar_init(&sm.cload[b], 1);
     }
+    ptx::mbar_init(&sm.b_full, 1);
+    ptx::mbar_init(&sm.b_empty, 1);
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tm_a);
     ptx::tma_prefetch_desc(&tm_b);
@@ -123,21 +174,37 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 0) {
     // ================================================================ producer
     if (ptx::elect_one()) {
-      const uint64_t pol_a = ptx::policy_evict_first();  // activations: streamed
-      const uint64_t pol_b = ptx::policy_evict_last();   // weights: reused by every tile
-      uint32_t it = 0;
-      for (int32_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
+      const uint64_t pol_a = ptx::policy_evict_first();  // activations: streamed once
+      const uint64_t pol_b = ptx::policy_evict_last();   // weights: reused by every CTA
+      uint32_t it = 0, pan = 0;
+      int32_t key = -1;
+      for (int32_t t = t0; t < t1; t += dt) {
         int32_t b, m0, nt;
-        decode_tile(p, t, &b, &m0, &nt);
+        decode_tile<kRes>(p, t, &b, &m0, &nt);
         const int32_t n0 = nt * BN;
+        if (kRes) {
+          const int32_t k = nt + b * p.b_batched * p.nt;
+          if (k != key) {  // new column block: reload the panel once its last MMA completed
+            if (pan > 0) ptx::mbar_wait(&sm.b_empty, (pan - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&sm.b_full, (uint32_t)(p.ktiles * NC * kGK * 128));
+            for (int32_t kt = 0; kt < p.ktiles; ++kt)
+#pragma unroll
+              for (int c = 0; c < NC; ++c)
+                ptx::tma_load_3d(sm.b[kt][c], &tm_b, &sm.b_full, n0 + 64 * c, kt * kGK, b * p.b_batched, pol_b);
+            key = k;
+            ++pan;
+          }
+        }
         for (int32_t kt = 0; kt < p.ktiles; ++kt, ++it) {
           const uint32_t s = it % S;
           ptx::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&sm.full[s], kGTile + NC * kGK * 128);
+          ptx::mbar_arrive_expect_tx(&sm.full[s], kRes ? kGTile : kGTile + NC * kGK * 128);
           ptx::tma_load_3d(sm.a[s], &tm_a, &sm.full[s], kt * kGK, m0, b * p.a_batched, pol_a);
+          if (!kRes) {
 #pragma unroll
-          for (int c = 0; c < NC; ++c)
-            ptx::tma_load_3d(sm.b[s][c], &tm_b, &sm.full[s], n0 + 64 * c, kt * kGK, b * p.b_batched, pol_b);
+            for (int c = 0; c < NC; ++c)
+              ptx::tma_load_3d(sm.b[s][c], &tm_b, &sm.full[s], n0 + 64 * c, kt * kGK, b * p.b_batched, pol_b);
+          }
         }
       }
     }
@@ -145,8 +212,20 @@ __global__ void __launch_bounds__(kGThreads, 1)
     // ============================================================ MMA issuer
     if (ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16(kGM, BN, 0, 1);  // A K-major, B MN-major
-      uint32_t it = 0, tc = 0;
-      for (int32_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++tc) {
+      uint32_t it = 0, tc = 0, pan = 0;
+      int32_t key = -1;
+      for (int32_t t = t0; t < t1; t += dt, ++tc) {
+        int32_t b, m0, nt;
+        decode_tile<kRes>(p, t, &b, &m0, &nt);
+        if (kRes) {
+          const int32_t k = nt + b * p.b_batched * p.nt;
+          if (k != key) {
+            if (pan > 0) ptx::tc_commit(&sm.b_empty);  // the old panel is free once these MMAs retire
+            ptx::mbar_wait(&sm.b_full, pan & 1);
+            key = k;
+            ++pan;
+          }
+        }
         const uint32_t buf = tc & 1;
         ptx::mbar_wait(&sm.acc_empty[buf], ((tc >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -157,7 +236,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
           ptx::tc_fence_after();
           const uint64_t ad = ptx::sdesc_sw128(ptx::smem_u32(sm.a[s]));
           // MN-major B: 64-column atoms 8 KB apart (LBO), 8-row groups 1 KB apart (SBO)
-          const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(sm.b[s][0]), 1024, kGK * 128);
+          const uint64_t bd = ptx::sdesc_sw128(ptx::smem_u32(sm.b[kRes ? kt : s][0]), 1024, kGK * 128);
 #pragma unroll
           for (int kk = 0; kk < kGK / 16; ++kk)
             ptx::mma_ss(dcol, ad + (uint64_t)(2 * kk), bd + (uint64_t)(kk * (2048 >> 4)), idesc,
@@ -177,19 +256,25 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const uint32_t stage_addr = ptx::smem_u32(sm.stage[grp]);
     const uint64_t pol_c = ptx::policy_evict_first();
     uint32_t tc = 0, cl_par = 0;
-    for (int32_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++tc) {
+    for (int32_t t = t0; t < t1; t += dt, ++tc) {
       int32_t b, m0, nt;
-      decode_tile(p, t, &b, &m0, &nt);
+      decode_tile<kRes>(p, t, &b, &m0, &nt);
       const int32_t n0 = nt * BN;
       const uint32_t buf = tc & 1;
+      // the residual chunk of this group's first column block lands in the
+      // staging tile while the main loop still runs
+      if (p.has_c && leader && n0 + 64 * (int)grp < p.N) {
+        ptx::tma_store_wait_read<0>();
+        ptx::mbar_arrive_expect_tx(&sm.cload[grp], kGTile);
+        ptx::tma_load_3d(sm.stage[grp], &tm_c, &sm.cload[grp], n0 + 64 * grp, m0, b, pol_c);
+      }
       ptx::mbar_wait(&sm.acc_full[buf], (tc >> 1) & 1);
       ptx::tc_fence_after();
       for (int c = grp; c < NC; c += 2) {
         const int32_t col0 = n0 + 64 * c;
         if (col0 >= p.N) break;
         if (p.has_c) {
-          // the residual chunk lands in the staging tile the result is built in
-          if (leader) {
+          if (c != (int)grp && leader) {  // later chunks: load after the previous store drained
             ptx::tma_store_wait_read<0>();
             ptx::mbar_arrive_expect_tx(&sm.cload[grp], kGTile);
             ptx::tma_load_3d(sm.stage[grp], &tm_c, &sm.cload[grp], col0, m0, b, pol_c);
@@ -237,7 +322,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
           }
           if (p.gelu) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = gelu_erf(f[e]);
+            for (int e = 0; e < 8; ++e) f[e] = gelu_fast(f[e]);
           }
           ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0], f[1]), ptx::pack_bf16x2(f[2], f[3]),
                             ptx::pack_bf16x2(f[4], f[5]), ptx::pack_bf16x2(f[6], f[7]));
@@ -382,7 +467,7 @@ bool tma_ok(const void* p, int64_t ld, int64_t sb, int batch) {
   return true;
 }
 
-template <int BN>
+template <int BN, bool kRes>
 int launch_bn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B, int64_t ldb,
               int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta, const void* bias,
               int batch, cudaStream_t stream, const char** why, bool gelu) {
@@ -408,20 +493,32 @@ int launch_bn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64
   p.gelu = gelu ? 1 : 0;
   p.beta = beta;
   p.bias = static_cast<const __nv_bfloat16*>(bias);
-  const size_t smem = sizeof(GemmSmem<BN>) + 1024;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_sm100_kernel<BN>), smem);
+  const size_t smem = sizeof(GemmSmem<BN, kRes>) + 1024;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_sm100_kernel<BN, kRes>), smem);
   if (e != cudaSuccess) {
     *why = "cudaFuncSetAttribute failed (GEMM)";
     return 0;
   }
   const int grid = (int)std::min<int64_t>(p.n_tiles, device_sms());
-  e = launch_pdl(gemm_sm100_kernel<BN>, grid, kGThreads, smem, stream, ma, mb, mc, md, p);
+  e = launch_pdl(gemm_sm100_kernel<BN, kRes>, grid, kGThreads, smem, stream, ma, mb, mc, md, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *why = cudaGetErrorString(e);
     return 0;
   }
   return 1;
+}
+
+template <int BN>
+int launch_pick(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B, int64_t ldb,
+                int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
+                const void* bias, int batch, cudaStream_t stream, const char** why, bool gelu) {
+  const int64_t ktiles = (K + kGK - 1) / kGK;
+  if (ktiles <= GemmSmem<BN, true>::kBStages)  // the whole B panel fits: weights read once per panel
+    return launch_bn<BN, true>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream, why,
+                               gelu);
+  return launch_bn<BN, false>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream, why,
+                              gelu);
 }
 
 // Tile width: the largest of 256 / 192 / 128 / 64 that divides N, else the
@@ -455,13 +552,13 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
                   (!bias || (reinterpret_cast<uintptr_t>(bias) & 15u) == 0);
   if (tc) {
     switch (pick_bn(N)) {
-      case 64: return launch_bn<64>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
+      case 64: return launch_pick<64>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
                                     why, gelu);
-      case 128: return launch_bn<128>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
+      case 128: return launch_pick<128>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
                                       why, gelu);
-      case 192: return launch_bn<192>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
+      case 192: return launch_pick<192>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
                                       why, gelu);
-      default: return launch_bn<256>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
+      default: return launch_pick<256>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
                                      why, gelu);
     }
   }
