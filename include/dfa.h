@@ -196,6 +196,9 @@ dfa_status_t dfa_backward(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t ba
  * bf16: the tcgen05 kernel (fp32 accumulate); f32: the SIMT validation
  * kernel (FFMA, no TF32).  Strides in elements; the building block of the
  * projections below, exported for parity tests. */
+/* Measurement knob: force dfa_gemm's tile width (64 / 128 / 192 / 256; 0 = the
+ * dispatcher's choice).  Process-wide; not for production use. */
+void dfa_set_gemm_tile(int32_t bn);
 dfa_status_t dfa_gemm(dfa_dtype_t dtype, int64_t batch, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                       int64_t sa, const void* B, int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd,
                       const void* C, int64_t ldc, float beta, const void* bias, int32_t gelu, void* stream);

@@ -67,6 +67,7 @@ EXPORTED = (
     "dfa_tensor_load",
     "dfa_tensor_save",
     "dfa_gemm",
+    "dfa_set_gemm_tile",
 )
 
 
@@ -156,6 +157,7 @@ def _load() -> ctypes.CDLL:
         "dfa_tensor_header": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), p_i64]),
         "dfa_tensor_load": (c_i32, [ctypes.c_char_p, c_i32, c_vp, c_i64]),
         "dfa_tensor_save": (c_i32, [ctypes.c_char_p, c_i32, c_i32, p_i64, c_vp]),
+        "dfa_set_gemm_tile": (None, [c_i32]),
         "dfa_gemm": (c_i32, [c_i32, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64,
                              c_i64, c_vp, c_i64, ctypes.c_float, c_vp, c_i32, c_vp]),
     }

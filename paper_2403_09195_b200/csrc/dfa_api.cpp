@@ -151,6 +151,7 @@ void dfa_set_fault_perturb(int32_t armed) { g_fault.store(armed ? 1 : 0); }
 int32_t dfa_get_fault_perturb(void) { return g_fault.load(); }
 void dfa_set_path_override(int32_t path) { g_path_override.store(path); }
 void dfa_set_host_zero_copy(int32_t enabled) { g_host_zero_copy.store(enabled ? 1 : 0); }
+void dfa_set_gemm_tile(int32_t bn) { dfa_impl::set_gemm_tile(bn); }
 
 dfa_status_t dfa_host_transfer_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
                                      const void* k, const void* v, int32_t with_lse, size_t* h2d, size_t* d2h) {

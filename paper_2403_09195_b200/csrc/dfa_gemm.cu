@@ -36,6 +36,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "dfa_internal.h"
@@ -44,6 +45,11 @@
 namespace dfa_impl {
 namespace {
 
+// Profiling probes (variant builds only, results wrong): 1 = the epilogue
+// only hands the accumulator back; 2 = no A loads (the MMAs run on stale tiles).
+#ifndef DFA_GEMM_PROBE
+#define DFA_GEMM_PROBE 0
+#endif
 constexpr int kGM = 128;        // tile rows (MMA M, TMEM lanes)
 constexpr int kGK = 64;         // K per stage: one 128-byte swizzle atom of bf16
 constexpr int kGThreads = 384;  // warps 0-3 control, 4-11 epilogue
@@ -51,25 +57,35 @@ constexpr int kGTile = kGM * 128;  // bytes of a [128 x 64] bf16 tile
 constexpr int kPanelBytes = 144 * 1024;  // resident B panel (K x BN bf16) capacity
 
 // Two main-loop forms:
-//  * resident (kRes): the whole B panel [K x BN] of the tile's column block
-//    stays in shared memory and only A streams through the ring -- the
-//    weights are read from L2 once per panel change instead of once per
-//    tile (K <= 384 at BN = 192: the projections, w1).  Each CTA owns a
-//    contiguous range of tiles ordered (batch, n, m), so it changes panels
-//    at most a couple of times.
+//  * resident (kRes): each CTA owns ONE column block (batch entry b, tile
+//    column nt) whose whole B panel [K x BN] sits in shared memory, and a
+//    contiguous run of its m-tiles; only A streams through the ring.  CTAs
+//    i .. i + NT - 1 hold the NT column blocks of the same batch entry and
+//    the same run of rows, so they read each A tile from DRAM once and from
+//    L2 NT - 1 times, while the weights are read once per CTA (K <= 384 at
+//    BN = 192: the projections, w1).
 //  * streaming: A and B tiles both stream (long K: w2); tiles strided over
 //    the grid with n fastest so A's rows are reused from L2.
-template <int BN, bool kRes>
+template <int BN, bool kRes, int kStgT>
 struct GemmSmem {
-  static constexpr int kStages = kRes ? 3 : (BN >= 256 ? 3 : 4);
-  static constexpr int kBStages = kRes ? kPanelBytes / (BN / 64 * kGK * 128) : kStages;
+  // budget: A ring + B (panel or ring) + staging tiles within 224 KB
+  static constexpr int kNC = BN / 64;
+  // k-tiles a resident panel holds: K <= 384 up to BN = 192, K <= 256 at 256
+  static constexpr int kPanelStages = kPanelBytes / (kNC * kGK * 128) < 6 ? kPanelBytes / (kNC * kGK * 128) : 6;
+  // staging tiles per epilogue group: 2 lets consecutive chunks' stores
+  // overlap (heavy epilogues: GELU, residual); 1 leaves room for a deeper A
+  // ring (the light ones are load-latency bound)
+  static constexpr int kStg = kStgT;
+  static constexpr int kStages = kRes ? (224 * 1024 - kPanelStages * kNC * kGK * 128 - 2 * kStg * kGTile) / kGTile
+                                      : (224 * 1024 - 2 * kStg * kGTile) / (kGTile + kNC * kGK * 128);
+  static constexpr int kBStages = kRes ? kPanelStages : kStages;
   uint8_t a[kStages][kGTile];
-  uint8_t b[kBStages][BN / 64][kGK * 128];  // panel (k-tiles) or ring stages
-  uint8_t stage[2][kGTile];                 // one staging tile per epilogue group
+  uint8_t b[kBStages][kNC][kGK * 128];     // panel (k-tiles) or ring stages
+  uint8_t stage[2][kStg][kGTile];          // staging tiles per epilogue group
   uint64_t full[kStages], empty[kStages];
   uint64_t acc_full[2], acc_empty[2];
   uint64_t cload[2];
-  uint64_t b_full, b_empty;                 // resident panel loaded / released
+  uint64_t b_full;                          // resident panel loaded
   uint32_t tmem_base;
 };
 
@@ -77,6 +93,7 @@ struct GemmParams {
   int32_t M, N, K, batch;
   int32_t a_batched, b_batched;  // 0: the operand is shared by every batch entry (batch stride 0)
   int32_t mt, nt, n_tiles, ktiles;
+  int32_t n_keys, rows_per_key, ctas_per_key;  // resident: column blocks, m-tiles per block, CTAs per block
   int32_t has_c, gelu;
   float beta;
   const __nv_bfloat16* bias;
@@ -100,14 +117,21 @@ __device__ __forceinline__ float gelu_fast(float x) {
   return fmaf(hx, ptx::tanh_approx(y), hx);
 }
 
-// Tile t -> (batch b, first row m0, column block nt).
+// Tile t -> (batch b, first row m0, column block nt).  Resident: t counts
+// this CTA's own m-tiles of its column block (key = blockIdx.x % n_keys).
 template <bool kRes>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int32_t t, int32_t* b, int32_t* m0, int32_t* nt) {
-  if (kRes) {  // (b, n, m): consecutive tiles share the B panel
-    *m0 = (t % p.mt) * kGM;
-    const int32_t rest = t / p.mt;
-    *nt = rest % p.nt;
-    *b = rest / p.nt;
+  if (kRes) {
+    const int32_t key = blockIdx.x % p.n_keys;
+    if (p.b_batched) {  // a B panel per batch entry: key = (b, nt)
+      *b = key / p.nt;
+      *nt = key % p.nt;
+      *m0 = t * kGM;
+    } else {  // shared weights: key = nt, the rows run over (b, m)
+      *nt = key;
+      *b = t / p.mt;
+      *m0 = (t % p.mt) * kGM;
+    }
   } else {  // (b, m, n): consecutive tiles share A's rows (L2)
     *nt = t % p.nt;
     const int32_t rest = t / p.nt;
@@ -116,12 +140,14 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int32_t t, int3
   }
 }
 
-// This CTA's tiles: a contiguous range (resident) or a grid-strided set.
+// This CTA's tiles: a contiguous run of its column block's m-tiles
+// (resident) or a grid-strided set.
 template <bool kRes>
 __device__ __forceinline__ void tile_range(const GemmParams& p, int32_t* t0, int32_t* t1, int32_t* dt) {
   if (kRes) {
-    *t0 = (int32_t)(((int64_t)blockIdx.x * p.n_tiles) / gridDim.x);
-    *t1 = (int32_t)(((int64_t)(blockIdx.x + 1) * p.n_tiles) / gridDim.x);
+    const int32_t j = blockIdx.x / p.n_keys;
+    *t0 = (int32_t)(((int64_t)j * p.rows_per_key) / p.ctas_per_key);
+    *t1 = (int32_t)(((int64_t)(j + 1) * p.rows_per_key) / p.ctas_per_key);
     *dt = 1;
   } else {
     *t0 = blockIdx.x;
@@ -130,12 +156,12 @@ __device__ __forceinline__ void tile_range(const GemmParams& p, int32_t* t0, int
   }
 }
 
-template <int BN, bool kRes>
+template <int BN, bool kRes, int kStgT>
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_d,
                       const __grid_constant__ GemmParams p) {
-  using Smem = GemmSmem<BN, kRes>;
+  using Smem = GemmSmem<BN, kRes, kStgT>;
   constexpr int S = Smem::kStages;
   constexpr int NC = BN / 64;
   extern __shared__ uint8_t smem_raw[];
@@ -155,7 +181,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
       ptx::mbar_init(&sm.cload[b], 1);
     }
     ptx::mbar_init(&sm.b_full, 1);
-    ptx::mbar_init(&sm.b_empty, 1);
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&tm_a);
     ptx::tma_prefetch_desc(&tm_b);
@@ -174,30 +199,28 @@ __global__ void __launch_bounds__(kGThreads, 1)
   if (warp == 0) {
     // ================================================================ producer
     if (ptx::elect_one()) {
-      const uint64_t pol_a = ptx::policy_evict_first();  // activations: streamed once
+      const uint64_t pol_a = ptx::policy_evict_normal();  // activations: re-read by the other column blocks
       const uint64_t pol_b = ptx::policy_evict_last();   // weights: reused by every CTA
       uint32_t it = 0, pan = 0;
-      int32_t key = -1;
       for (int32_t t = t0; t < t1; t += dt) {
         int32_t b, m0, nt;
         decode_tile<kRes>(p, t, &b, &m0, &nt);
         const int32_t n0 = nt * BN;
-        if (kRes) {
-          const int32_t k = nt + b * p.b_batched * p.nt;
-          if (k != key) {  // new column block: reload the panel once its last MMA completed
-            if (pan > 0) ptx::mbar_wait(&sm.b_empty, (pan - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&sm.b_full, (uint32_t)(p.ktiles * NC * kGK * 128));
-            for (int32_t kt = 0; kt < p.ktiles; ++kt)
+        if (kRes && pan == 0) {  // the CTA's column block: its whole B panel, once
+          ptx::mbar_arrive_expect_tx(&sm.b_full, (uint32_t)(p.ktiles * NC * kGK * 128));
+          for (int32_t kt = 0; kt < p.ktiles; ++kt)
 #pragma unroll
-              for (int c = 0; c < NC; ++c)
-                ptx::tma_load_3d(sm.b[kt][c], &tm_b, &sm.b_full, n0 + 64 * c, kt * kGK, b * p.b_batched, pol_b);
-            key = k;
-            ++pan;
-          }
+            for (int c = 0; c < NC; ++c)
+              ptx::tma_load_3d(sm.b[kt][c], &tm_b, &sm.b_full, n0 + 64 * c, kt * kGK, b * p.b_batched, pol_b);
+          pan = 1;
         }
         for (int32_t kt = 0; kt < p.ktiles; ++kt, ++it) {
           const uint32_t s = it % S;
           ptx::mbar_wait(&sm.empty[s], ((it / S) & 1) ^ 1);
+          if (DFA_GEMM_PROBE == 2 && kRes) {
+            ptx::mbar_arrive(&sm.full[s]);
+            continue;
+          }
           ptx::mbar_arrive_expect_tx(&sm.full[s], kRes ? kGTile : kGTile + NC * kGK * 128);
           ptx::tma_load_3d(sm.a[s], &tm_a, &sm.full[s], kt * kGK, m0, b * p.a_batched, pol_a);
           if (!kRes) {
@@ -212,20 +235,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
     // ============================================================ MMA issuer
     if (ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16(kGM, BN, 0, 1);  // A K-major, B MN-major
-      uint32_t it = 0, tc = 0, pan = 0;
-      int32_t key = -1;
+      uint32_t it = 0, tc = 0;
+      if (kRes && t0 < t1) ptx::mbar_wait(&sm.b_full, 0);  // the CTA's B panel
       for (int32_t t = t0; t < t1; t += dt, ++tc) {
-        int32_t b, m0, nt;
-        decode_tile<kRes>(p, t, &b, &m0, &nt);
-        if (kRes) {
-          const int32_t k = nt + b * p.b_batched * p.nt;
-          if (k != key) {
-            if (pan > 0) ptx::tc_commit(&sm.b_empty);  // the old panel is free once these MMAs retire
-            ptx::mbar_wait(&sm.b_full, pan & 1);
-            key = k;
-            ++pan;
-          }
-        }
         const uint32_t buf = tc & 1;
         ptx::mbar_wait(&sm.acc_empty[buf], ((tc >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -253,9 +265,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const bool leader = (warp % 4) == 0 && lane == 0;
     const uint32_t bar_id = 1 + grp;
-    const uint32_t stage_addr = ptx::smem_u32(sm.stage[grp]);
+    constexpr int kStg = Smem::kStg;
     const uint64_t pol_c = ptx::policy_evict_first();
-    uint32_t tc = 0, cl_par = 0;
+    uint32_t tc = 0, cl_par = 0, sc = 0;  // sc: chunks this group stored (staging rotation)
     for (int32_t t = t0; t < t1; t += dt, ++tc) {
       int32_t b, m0, nt;
       decode_tile<kRes>(p, t, &b, &m0, &nt);
@@ -263,26 +275,28 @@ __global__ void __launch_bounds__(kGThreads, 1)
       const uint32_t buf = tc & 1;
       // the residual chunk of this group's first column block lands in the
       // staging tile while the main loop still runs
-      if (p.has_c && leader && n0 + 64 * (int)grp < p.N) {
-        ptx::tma_store_wait_read<0>();
+      if (p.has_c && leader && (int)grp < NC && n0 + 64 * (int)grp < p.N && DFA_GEMM_PROBE != 1) {
+        ptx::tma_store_wait_read<kStg - 1>();
         ptx::mbar_arrive_expect_tx(&sm.cload[grp], kGTile);
-        ptx::tma_load_3d(sm.stage[grp], &tm_c, &sm.cload[grp], n0 + 64 * grp, m0, b, pol_c);
+        ptx::tma_load_3d(sm.stage[grp][sc % kStg], &tm_c, &sm.cload[grp], n0 + 64 * grp, m0, b, pol_c);
       }
       ptx::mbar_wait(&sm.acc_full[buf], (tc >> 1) & 1);
       ptx::tc_fence_after();
-      for (int c = grp; c < NC; c += 2) {
+      for (int c = grp; c < NC && DFA_GEMM_PROBE != 1; c += 2) {
         const int32_t col0 = n0 + 64 * c;
         if (col0 >= p.N) break;
+        uint8_t* stg = sm.stage[grp][sc % kStg];
+        const uint32_t stage_addr = ptx::smem_u32(stg);
         if (p.has_c) {
-          if (c != (int)grp && leader) {  // later chunks: load after the previous store drained
-            ptx::tma_store_wait_read<0>();
+          if (c != (int)grp && leader) {  // later chunks: load once this buffer's last store drained
+            ptx::tma_store_wait_read<kStg - 1>();
             ptx::mbar_arrive_expect_tx(&sm.cload[grp], kGTile);
-            ptx::tma_load_3d(sm.stage[grp], &tm_c, &sm.cload[grp], col0, m0, b, pol_c);
+            ptx::tma_load_3d(stg, &tm_c, &sm.cload[grp], col0, m0, b, pol_c);
           }
           ptx::mbar_wait(&sm.cload[grp], cl_par);
           cl_par ^= 1;
         } else {
-          if (leader) ptx::tma_store_wait_read<0>();
+          if (leader) ptx::tma_store_wait_read<kStg - 1>();  // this buffer's previous store has been read
           ptx::named_bar_sync(bar_id, kGM);
         }
         uint32_t acc[2][32];
@@ -330,9 +344,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(bar_id, kGM);
         if (leader) {
-          ptx::tma_store_3d(&tm_d, sm.stage[grp], col0, m0, b);
+          ptx::tma_store_3d(&tm_d, stg, col0, m0, b);
           ptx::tma_store_commit();
         }
+        ++sc;
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&sm.acc_empty[buf]);
@@ -447,8 +462,11 @@ EncodeTiledFn encode_fn() {
 
 // Row-major bf16 matrix [batch][rows][cols] with row stride ld and batch
 // stride sb (elements); box (64 cols, box_rows rows, 1), 128-byte swizzle.
+#ifndef DFA_GEMM_PROMO_A
+#define DFA_GEMM_PROMO_A CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
 bool map3(CUtensorMap* map, const void* base, int64_t cols, int64_t rows, int64_t batch, int64_t ld, int64_t sb,
-          uint32_t box_rows) {
+          uint32_t box_rows, CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_128B) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)batch};
@@ -456,7 +474,7 @@ bool map3(CUtensorMap* map, const void* base, int64_t cols, int64_t rows, int64_
   cuuint32_t box[3] = {64, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -467,13 +485,13 @@ bool tma_ok(const void* p, int64_t ld, int64_t sb, int batch) {
   return true;
 }
 
-template <int BN, bool kRes>
+template <int BN, bool kRes, int kStg>
 int launch_bn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B, int64_t ldb,
               int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta, const void* bias,
               int batch, cudaStream_t stream, const char** why, bool gelu) {
   CUtensorMap ma, mb, mc, md;
   const int a_bat = (batch > 1 && sa != 0) ? batch : 1, b_bat = (batch > 1 && sb != 0) ? batch : 1;
-  if (!map3(&ma, A, K, M, a_bat, lda, sa, kGM) || !map3(&mb, B, N, K, b_bat, ldb, sb, kGK) ||
+  if (!map3(&ma, A, K, M, a_bat, lda, sa, kGM, (CUtensorMapL2promotion)DFA_GEMM_PROMO_A) || !map3(&mb, B, N, K, b_bat, ldb, sb, kGK) ||
       !map3(&md, D, N, M, batch, ldd, sd, kGM) || !map3(&mc, C ? C : D, N, M, batch, C ? ldc : ldd, sd, kGM)) {
     *why = "cuTensorMapEncodeTiled failed (GEMM operands)";
     return 0;
@@ -489,18 +507,24 @@ int launch_bn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64
   p.nt = (int32_t)((N + BN - 1) / BN);
   p.n_tiles = p.mt * p.nt * batch;
   p.ktiles = (int32_t)((K + kGK - 1) / kGK);
+  p.n_keys = (int32_t)((p.b_batched ? batch : 1) * p.nt);
+  p.rows_per_key = (int32_t)(p.b_batched ? p.mt : (int64_t)p.mt * batch);
+  p.ctas_per_key = std::max(1, device_sms() / p.n_keys);
   p.has_c = C ? 1 : 0;
   p.gelu = gelu ? 1 : 0;
   p.beta = beta;
   p.bias = static_cast<const __nv_bfloat16*>(bias);
-  const size_t smem = sizeof(GemmSmem<BN, kRes>) + 1024;
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_sm100_kernel<BN, kRes>), smem);
+  using Smem = GemmSmem<BN, kRes, kStg>;
+  const size_t smem = sizeof(Smem) + 1024;
+  static_assert(sizeof(Smem) + 1024 <= 232448, "GEMM shared memory exceeds 227 KB");
+  static_assert(Smem::kStages >= 2, "GEMM A ring needs >= 2 stages");
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_sm100_kernel<BN, kRes, kStg>), smem);
   if (e != cudaSuccess) {
     *why = "cudaFuncSetAttribute failed (GEMM)";
     return 0;
   }
-  const int grid = (int)std::min<int64_t>(p.n_tiles, device_sms());
-  e = launch_pdl(gemm_sm100_kernel<BN, kRes>, grid, kGThreads, smem, stream, ma, mb, mc, md, p);
+  const int grid = kRes ? p.n_keys * p.ctas_per_key : (int)std::min<int64_t>(p.n_tiles, device_sms());
+  e = launch_pdl(gemm_sm100_kernel<BN, kRes, kStg>, grid, kGThreads, smem, stream, ma, mb, mc, md, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *why = cudaGetErrorString(e);
@@ -509,35 +533,36 @@ int launch_bn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64
   return 1;
 }
 
-template <int BN>
-int launch_pick(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B, int64_t ldb,
-                int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
-                const void* bias, int batch, cudaStream_t stream, const char** why, bool gelu) {
-  const int64_t ktiles = (K + kGK - 1) / kGK;
-  if (ktiles <= GemmSmem<BN, true>::kBStages)  // the whole B panel fits: weights read once per panel
-    return launch_bn<BN, true>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream, why,
-                               gelu);
-  return launch_bn<BN, false>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream, why,
-                              gelu);
-}
+std::atomic<int> g_force_bn{0};  // measurement knob (dfa_set_gemm_tile); 0 = auto
 
-// Tile width: the largest of 256 / 192 / 128 / 64 that divides N, else the
-// one that wastes the fewest columns.
-int pick_bn(int64_t N) {
-  if (N <= 64) return 64;
-  const int cands[4] = {256, 192, 128, 64};
-  for (int bn : cands)
-    if (N % bn == 0) return bn;
-  int best = 256;
-  int64_t waste = (N + 255) / 256 * 256 - N;
-  for (int bn : cands) {
-    const int64_t w = (N + bn - 1) / bn * bn - N;
-    if (w < waste) {
-      waste = w;
-      best = bn;
-    }
+#ifndef DFA_GEMM_STG
+#define DFA_GEMM_STG 0
+#endif
+// Resident panel at BN = 128 whenever it fits (K <= 384): measured best on
+// every projection / w1 shape (BN = 192 leaves only 3 A stages; the main
+// loop is load-latency bound); light epilogues take a 6-deep A ring with one
+// staging tile per group, GELU / residual epilogues 4 stages and two.
+// Longer K streams A and B tiles (BN = 192, 4 stages).
+int launch_dispatch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
+                    int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
+                    const void* bias, int batch, cudaStream_t stream, const char** why, bool gelu, int force_bn) {
+  const int64_t ktiles = (K + kGK - 1) / kGK;
+  const bool heavy = gelu || C != nullptr;
+  const int stg = DFA_GEMM_STG ? DFA_GEMM_STG : (heavy ? 2 : 1);
+#define DFA_GEMM_ARGS M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream, why, gelu
+  const int bn_res = force_bn ? force_bn : 128;
+  const int64_t keys = (batch > 1 && sb != 0 ? batch : 1) * ((N + bn_res - 1) / bn_res);
+  if (ktiles <= 6 && keys <= device_sms() && (bn_res == 128 || bn_res == 64)) {
+    if (bn_res == 64) return stg == 1 ? launch_bn<64, true, 1>(DFA_GEMM_ARGS) : launch_bn<64, true, 2>(DFA_GEMM_ARGS);
+    return stg == 1 ? launch_bn<128, true, 1>(DFA_GEMM_ARGS) : launch_bn<128, true, 2>(DFA_GEMM_ARGS);
   }
-  return best;
+  switch (force_bn ? force_bn : 192) {
+    case 64: return launch_bn<64, false, 2>(DFA_GEMM_ARGS);
+    case 128: return launch_bn<128, false, 2>(DFA_GEMM_ARGS);
+    case 256: return launch_bn<256, false, 1>(DFA_GEMM_ARGS);
+    default: return launch_bn<192, false, 2>(DFA_GEMM_ARGS);
+  }
+#undef DFA_GEMM_ARGS
 }
 
 }  // namespace
@@ -550,18 +575,8 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
   const bool tc = dtype == 1 && K > 0 && M < INT32_MAX / 2 && N < INT32_MAX / 2 && tma_ok(A, lda, sa, batch) &&
                   tma_ok(B, ldb, sb, batch) && tma_ok(D, ldd, sd, batch) && (!C || tma_ok(C, ldc, sd, batch)) &&
                   (!bias || (reinterpret_cast<uintptr_t>(bias) & 15u) == 0);
-  if (tc) {
-    switch (pick_bn(N)) {
-      case 64: return launch_pick<64>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
-                                    why, gelu);
-      case 128: return launch_pick<128>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
-                                      why, gelu);
-      case 192: return launch_pick<192>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
-                                      why, gelu);
-      default: return launch_pick<256>(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream,
-                                     why, gelu);
-    }
-  }
+  if (tc) return launch_dispatch(M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream, why,
+                                 gelu, g_force_bn.load());
   SimtGemmParams p{M, N, K, lda, sa, ldb, sb, ldd, sd, ldc, beta, gelu ? 1 : 0};
   dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)batch);
   if (dtype == 0)
@@ -578,5 +593,7 @@ int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int
   }
   return 1;
 }
+
+void set_gemm_tile(int bn) { g_force_bn.store(bn); }
 
 }  // namespace dfa_impl

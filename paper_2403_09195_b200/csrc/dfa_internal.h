@@ -139,6 +139,7 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
 int gemm_rowmajor(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
                   int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
                   const void* bias, int batch, cudaStream_t stream, const char** why, bool gelu = false);
+void set_gemm_tile(int bn);  // measurement: force the GEMM tile width (0 = auto)
 // dfa_layers.cu: LayerNorm (eps 1e-5) and erf-GELU kernels, weight packing.
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
                       cudaStream_t stream);
