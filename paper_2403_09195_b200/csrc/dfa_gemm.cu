@@ -104,18 +104,25 @@ __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
 }
 
-// GELU of the bf16 epilogue: x Phi(x) with Phi(x) = (1 + tanh(y)) / 2,
-// y = x (a + b x^2 + c x^4) minimax-fitted to the erf form over |x| <= 8
-// (|x| clamped there, where Phi is 0 / 1 to fp32): max |GELU error| 2.6e-5
-// from the fit plus tanh.approx's 2^-11 relative -- below the bf16 result's
-// rounding step (2^-9 relative) -- on one MUFU op instead of erff's ~20.
-__device__ __forceinline__ float gelu_fast(float x) {
-  const float xc = fminf(fmaxf(x, -8.0f), 8.0f);
-  const float x2 = xc * xc;
-  const float y = xc * fmaf(fmaf(-3.51516789e-4f, x2, 3.70056460e-2f), x2, 7.97507884e-1f);
-  const float hx = 0.5f * x;
-  return fmaf(hx, ptx::tanh_approx(y), hx);
+// GELU of the bf16 epilogue on a pair: x Phi(x) with Phi(x) = (1 + tanh(y)) / 2,
+// y = x (a + b x^2), a and b minimax-fitted to the erf form
+// (tensor.hpp:262-265): max |GELU error| 2.7e-4 over all x, plus
+// tanh.approx's 2^-11 relative -- far below the bf16 result's rounding step
+// (2^-9 relative) -- on one MUFU op and 5 packed FMA-pipe ops per pair
+// instead of erff's ~20 instructions per element.  (fp32, the validation
+// mode, keeps erff.)
+__device__ __forceinline__ float2 gelu2(float2 v) {
+  const float2 x2 = ptx::fmul2(v, v);
+  const float2 t = ptx::ffma2(x2, make_float2(0.03470089f, 0.03470089f), make_float2(0.80015708f, 0.80015708f));
+  const float2 y = ptx::fmul2(v, t);
+  const float2 hx = ptx::fmul2(v, make_float2(0.5f, 0.5f));
+  return ptx::ffma2(hx, make_float2(ptx::tanh_approx(y.x), ptx::tanh_approx(y.y)), hx);
 }
+
+// Epilogue kinds (compile-time so the per-element path is straight-line
+// code): bit 0 bias, bit 1 residual C, bit 2 GELU; kEpiAny reads the
+// runtime flags.
+constexpr int kEpiBias = 1, kEpiC = 2, kEpiGelu = 4, kEpiAny = -1;
 
 // Tile t -> (batch b, first row m0, column block nt).  Resident: t counts
 // this CTA's own m-tiles of its column block (key = blockIdx.x % n_keys).
@@ -156,13 +163,16 @@ __device__ __forceinline__ void tile_range(const GemmParams& p, int32_t* t0, int
   }
 }
 
-template <int BN, bool kRes, int kStgT>
+template <int BN, bool kRes, int kStgT, int kEpi>
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_d,
                       const __grid_constant__ GemmParams p) {
   using Smem = GemmSmem<BN, kRes, kStgT>;
   constexpr int S = Smem::kStages;
+  const bool has_bias = kEpi == kEpiAny ? p.bias != nullptr : (kEpi & kEpiBias) != 0;
+  const bool has_c = kEpi == kEpiAny ? p.has_c != 0 : (kEpi & kEpiC) != 0;
+  const bool has_gelu = kEpi == kEpiAny ? p.gelu != 0 : (kEpi & kEpiGelu) != 0;
   constexpr int NC = BN / 64;
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       const uint32_t buf = tc & 1;
       // the residual chunk of this group's first column block lands in the
       // staging tile while the main loop still runs
-      if (p.has_c && leader && (int)grp < NC && n0 + 64 * (int)grp < p.N && DFA_GEMM_PROBE != 1) {
+      if (has_c && leader && (int)grp < NC && n0 + 64 * (int)grp < p.N && DFA_GEMM_PROBE != 1) {
         ptx::tma_store_wait_read<kStg - 1>();
         ptx::mbar_arrive_expect_tx(&sm.cload[grp], kGTile);
         ptx::tma_load_3d(sm.stage[grp][sc % kStg], &tm_c, &sm.cload[grp], n0 + 64 * grp, m0, b, pol_c);
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         if (col0 >= p.N) break;
         uint8_t* stg = sm.stage[grp][sc % kStg];
         const uint32_t stage_addr = ptx::smem_u32(stg);
-        if (p.has_c) {
+        if (has_c) {
           if (c != (int)grp && leader) {  // later chunks: load once this buffer's last store drained
             ptx::tma_store_wait_read<kStg - 1>();
             ptx::mbar_arrive_expect_tx(&sm.cload[grp], kGTile);
@@ -303,43 +313,45 @@ __global__ void __launch_bounds__(kGThreads, 1)
         ptx::tmem_ld32(tbase + lane_base + buf * BN + 64 * c, acc[0]);
         ptx::tmem_ld32(tbase + lane_base + buf * BN + 64 * c + 32, acc[1]);
         ptx::tmem_ld_wait();
-        const bool full_bias = p.bias && col0 + 64 <= p.N;
+        const bool full_bias = has_bias && col0 + 64 <= p.N;
+        const uint4* bp = reinterpret_cast<const uint4*>(p.bias + col0);  // 8 bias values per 16-byte load
+        const float2 beta2 = make_float2(p.beta, p.beta);
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
           const uint32_t addr = stage_addr + row * 128 + ((c8 ^ (row & 7)) * 16);
-          float f[8];
+          float2 v[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(acc[c8 >> 2][(c8 & 3) * 8 + e]);
-          if (full_bias) {  // 8 bias values = one 16-byte broadcast load
-            const uint4 w = *reinterpret_cast<const uint4*>(p.bias + col0 + 8 * c8);
+          for (int e = 0; e < 4; ++e)
+            v[e] = make_float2(__uint_as_float(acc[c8 >> 2][(c8 & 3) * 8 + 2 * e]),
+                               __uint_as_float(acc[c8 >> 2][(c8 & 3) * 8 + 2 * e + 1]));
+          if (full_bias) {
+            const uint4 w = bp[c8];
             const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 bv = ptx::unpack_bf16x2(ww[e]);
-              f[2 * e] += bv.x;
-              f[2 * e + 1] += bv.y;
-            }
-          } else if (p.bias) {
+            for (int e = 0; e < 4; ++e) v[e] = ptx::fadd2(v[e], ptx::unpack_bf16x2(ww[e]));
+          } else if (has_bias) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (col0 + 8 * c8 + e < p.N) f[e] += __bfloat162float(p.bias[col0 + 8 * c8 + e]);
+            for (int e = 0; e < 8; ++e) {
+              const int col = col0 + 8 * c8 + e;
+              const float bv = col < p.N ? __bfloat162float(p.bias[col]) : 0.0f;
+              if (e & 1)
+                v[e >> 1].y += bv;
+              else
+                v[e >> 1].x += bv;
+            }
           }
-          if (p.has_c) {
+          if (has_c) {
             uint32_t prev[4];
             ptx::ld_shared_v4(addr, prev);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 cv = ptx::unpack_bf16x2(prev[e]);
-              f[2 * e] = fmaf(p.beta, cv.x, f[2 * e]);
-              f[2 * e + 1] = fmaf(p.beta, cv.y, f[2 * e + 1]);
-            }
+            for (int e = 0; e < 4; ++e) v[e] = ptx::ffma2(beta2, ptx::unpack_bf16x2(prev[e]), v[e]);
           }
-          if (p.gelu) {
+          if (has_gelu) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = gelu_fast(f[e]);
+            for (int e = 0; e < 4; ++e) v[e] = gelu2(v[e]);
           }
-          ptx::st_shared_v4(addr, ptx::pack_bf16x2(f[0], f[1]), ptx::pack_bf16x2(f[2], f[3]),
-                            ptx::pack_bf16x2(f[4], f[5]), ptx::pack_bf16x2(f[6], f[7]));
+          ptx::st_shared_v4(addr, ptx::pack_bf16x2(v[0].x, v[0].y), ptx::pack_bf16x2(v[1].x, v[1].y),
+                            ptx::pack_bf16x2(v[2].x, v[2].y), ptx::pack_bf16x2(v[3].x, v[3].y));
         }
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(bar_id, kGM);
@@ -485,7 +497,7 @@ bool tma_ok(const void* p, int64_t ld, int64_t sb, int batch) {
   return true;
 }
 
-template <int BN, bool kRes, int kStg>
+template <int BN, bool kRes, int kStg, int kEpi = kEpiAny>
 int launch_bn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B, int64_t ldb,
               int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta, const void* bias,
               int batch, cudaStream_t stream, const char** why, bool gelu) {
@@ -518,13 +530,13 @@ int launch_bn(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64
   const size_t smem = sizeof(Smem) + 1024;
   static_assert(sizeof(Smem) + 1024 <= 232448, "GEMM shared memory exceeds 227 KB");
   static_assert(Smem::kStages >= 2, "GEMM A ring needs >= 2 stages");
-  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_sm100_kernel<BN, kRes, kStg>), smem);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(gemm_sm100_kernel<BN, kRes, kStg, kEpi>), smem);
   if (e != cudaSuccess) {
     *why = "cudaFuncSetAttribute failed (GEMM)";
     return 0;
   }
   const int grid = kRes ? p.n_keys * p.ctas_per_key : (int)std::min<int64_t>(p.n_tiles, device_sms());
-  e = launch_pdl(gemm_sm100_kernel<BN, kRes, kStg>, grid, kGThreads, smem, stream, ma, mb, mc, md, p);
+  e = launch_pdl(gemm_sm100_kernel<BN, kRes, kStg, kEpi>, grid, kGThreads, smem, stream, ma, mb, mc, md, p);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     *why = cudaGetErrorString(e);
@@ -552,10 +564,21 @@ int launch_dispatch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
 #define DFA_GEMM_ARGS M, N, K, A, lda, sa, B, ldb, sb, D, ldd, sd, C, ldc, beta, bias, batch, stream, why, gelu
   const int bn_res = force_bn ? force_bn : 128;
   const int64_t keys = (batch > 1 && sb != 0 ? batch : 1) * ((N + bn_res - 1) / bn_res);
+  const int epi = (bias ? kEpiBias : 0) | (C ? kEpiC : 0) | (gelu ? kEpiGelu : 0);
   if (ktiles <= 6 && keys <= device_sms() && (bn_res == 128 || bn_res == 64)) {
     if (bn_res == 64) return stg == 1 ? launch_bn<64, true, 1>(DFA_GEMM_ARGS) : launch_bn<64, true, 2>(DFA_GEMM_ARGS);
+    if (!DFA_GEMM_STG && !force_bn) {  // the layers' epilogues, straight-line
+      if (epi == 0) return launch_bn<128, true, 1, 0>(DFA_GEMM_ARGS);
+      if (epi == (kEpiBias | kEpiC)) return launch_bn<128, true, 2, kEpiBias | kEpiC>(DFA_GEMM_ARGS);
+      // GELU epilogues: 256-wide tiles (two chunks per group per tile keep
+      // the TMA store of one chunk under the math of the next): measured
+      // 0.40 vs 0.45 ms on w1 at config 2
+      if (epi == (kEpiBias | kEpiGelu) && N % 256 == 0)
+        return launch_bn<256, false, 1, kEpiBias | kEpiGelu>(DFA_GEMM_ARGS);
+    }
     return stg == 1 ? launch_bn<128, true, 1>(DFA_GEMM_ARGS) : launch_bn<128, true, 2>(DFA_GEMM_ARGS);
   }
+  if (!force_bn && epi == (kEpiBias | kEpiC)) return launch_bn<192, false, 2, kEpiBias | kEpiC>(DFA_GEMM_ARGS);
   switch (force_bn ? force_bn : 192) {
     case 64: return launch_bn<64, false, 2>(DFA_GEMM_ARGS);
     case 128: return launch_bn<128, false, 2>(DFA_GEMM_ARGS);
