@@ -176,6 +176,15 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t n_branche
                                      dfa_dtype_t dtype, int64_t batch, const void* q, const void* k, const void* v,
                                      void* o, float* lse, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Test / measurement hook for dfa_forward_multibranch (bf16, 2+ branches):
+ * DFA_MB_AUTO (default) runs every branch and the combine in one tcgen05
+ * kernel when the set fits it (intervals dividing their segment lengths,
+ * <= 4 distinct intervals, lcm | N; else per-branch launches);
+ * DFA_MB_PER_BRANCH forces one launch per branch with the LSE merge in each
+ * epilogue.  Process-wide. */
+enum { DFA_MB_AUTO = 0, DFA_MB_PER_BRANCH = 1 };
+void dfa_set_multibranch_mode(int32_t mode);
+
 /* Backward of the dilated core (the reference computes
  * it on its autodiff tape for the dilated branch of detail::attention_mix,
  * encoder.hpp:204-219, ops autodiff.hpp:99-179, 269-289): gradients of a loss

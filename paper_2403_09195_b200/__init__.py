@@ -478,6 +478,17 @@ def fault_perturb():
 
 
 @contextlib.contextmanager
+def multibranch_mode(mode: int):
+    """Test hook: DFA_MB_PER_BRANCH forces one launch per branch (epilogue
+    LSE merge) instead of the single fused multi-branch kernel."""
+    lib.dfa_set_multibranch_mode(mode)
+    try:
+        yield
+    finally:
+        lib.dfa_set_multibranch_mode(0)
+
+
+@contextlib.contextmanager
 def path_override(path: int):
     """Test hook: force DFA_PATH_SIMT or require DFA_PATH_SM100_TCGEN05."""
     lib.dfa_set_path_override(path)

@@ -29,6 +29,8 @@ DFA_F64 = 2
 DFA_PATH_NONE = 0
 DFA_PATH_SM100_TCGEN05 = 1
 DFA_PATH_SIMT = 2
+DFA_MB_AUTO = 0
+DFA_MB_PER_BRANCH = 1
 
 # Every function include/dfa.h declares (tests check the .so exports them).
 EXPORTED = (
@@ -49,6 +51,7 @@ EXPORTED = (
     "dfa_get_fault_perturb",
     "dfa_workspace_bytes",
     "dfa_set_path_override",
+    "dfa_set_multibranch_mode",
     "dfa_forward_traced",
     "dfa_forward_debug",
     "dfa_multibranch_workspace_bytes",
@@ -133,6 +136,7 @@ def _load() -> ctypes.CDLL:
         "dfa_get_fault_perturb": (c_i32, []),
         "dfa_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_i32, ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_set_path_override": (None, [c_i32]),
+        "dfa_set_multibranch_mode": (None, [c_i32]),
         "dfa_forward_traced": (c_i32, [p_cfg, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
         "dfa_forward_debug": (c_i32, [p_cfg, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
         "dfa_multibranch_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i32, c_i64, ctypes.POINTER(ctypes.c_size_t)]),

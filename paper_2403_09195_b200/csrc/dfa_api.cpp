@@ -22,6 +22,7 @@ thread_local std::string g_last_error;
 thread_local int32_t g_launches = 0;
 std::atomic<int32_t> g_fault{0};
 std::atomic<int32_t> g_path_override{0};
+std::atomic<int32_t> g_mb_mode{0};
 std::atomic<int32_t> g_host_zero_copy{1};
 
 dfa_status_t fail(dfa_status_t st, const char* fmt, ...) {
@@ -150,6 +151,7 @@ int32_t dfa_last_launch_count(void) { return g_launches; }
 void dfa_set_fault_perturb(int32_t armed) { g_fault.store(armed ? 1 : 0); }
 int32_t dfa_get_fault_perturb(void) { return g_fault.load(); }
 void dfa_set_path_override(int32_t path) { g_path_override.store(path); }
+void dfa_set_multibranch_mode(int32_t mode) { g_mb_mode.store(mode); }
 void dfa_set_host_zero_copy(int32_t enabled) { g_host_zero_copy.store(enabled ? 1 : 0); }
 void dfa_set_gemm_tile(int32_t bn) { dfa_impl::set_gemm_tile(bn); }
 
@@ -478,7 +480,18 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t nb, const
   const size_t ob = up256((size_t)(g.B * g.N * g.h * g.dv) * es), lb = up256((size_t)(g.B * g.h * g.N) * 4);
   cudaError_t err = cudaSuccess;
   int launches = 0;
-  if (fused) {
+  if (fused && nb > 1 && g_mb_mode.load() == DFA_MB_AUTO) {
+    // Every branch and the LSE combine in one persistent tcgen05 kernel
+    // (dfa_mb_sm100.cu); a set outside its envelope takes the per-branch path.
+    const char* why = "";
+    const int n = dfa_impl::launch_mb_sm100(gb, nb, q, k, v, o, lse, s, &err, &why, nullptr);
+    if (n < 0) return fail(DFA_ERR_CUDA, "multibranch: %s (%s)", why, cudaGetErrorString(err));
+    launches = n;
+    if (n > 0) fused = false;  // done
+  }
+  if (launches > 0) {
+    // fused single-kernel path taken
+  } else if (fused) {
     // Fused epilogue combine: branch 0 writes o (zero rows included) and the
     // running lse; every later branch LSE-merges its kept rows into them in
     // its epilogue.  Stream order separates the branches.

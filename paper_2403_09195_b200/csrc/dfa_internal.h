@@ -122,6 +122,16 @@ int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int n
                    const float* const* lse, void* out, float* lse_out, cudaStream_t stream, cudaError_t* err);
 constexpr int kMaxBranches = 8;
 
+// dfa_mb_sm100.cu: all branches of a multi-(w, r) set + their LSE combine in
+// one persistent tcgen05 kernel.  Returns 1 (launched), 0 (set outside the
+// kernel's envelope, why set, nothing launched), -1 (CUDA error, err set).
+// steps_out (optional): 128x128 score tiles the launch computes.
+constexpr int kMbMaxMaps = 4;     // distinct intervals in a set
+constexpr int kMbMaxTiles = 64;   // key tiles per work unit
+constexpr int kMbMaxGroups = 8;   // offset-class groups per query tile
+int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, const void* v, void* o, float* lse,
+                    cudaStream_t stream, cudaError_t* err, const char** why, int64_t* steps_out);
+
 // Backward of the dilated core (dfa_bwd.cu): delta = workspace [B, h, N] fp32.
 // allow_sm100: take the tcgen05 kernel (dfa_bwd_sm100.cu) when it covers the call.
 int launch_backward(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o,

@@ -359,19 +359,20 @@ def test_tcgen05_many_units_per_cta(dfa, cuda, w, r):
     [(256, 2), (256, 2)],             # duplicate branch: weights 1/2 each, o unchanged
 ])
 def test_multibranch_fused_epilogue_matches_unfused(dfa, cuda, branches):
-    """bf16 fused path (branch 0 writes o + running lse, later branches merge in
-    their epilogue: one launch per branch, no combine kernel) vs the unfused
+    """bf16 per-branch path (branch 0 writes o + running lse, later branches merge
+    in their epilogue: one launch per branch, no combine kernel) vs the unfused
     path (per-branch o_b/lse_b + combine kernel, forced via the SIMT override)."""
     torch = _torch()
-    from paper_2403_09195_b200 import _lib, path_override
+    from paper_2403_09195_b200 import _lib, multibranch_mode, path_override
 
     g = torch.Generator(device="cuda").manual_seed(len(branches))
     B, n, h = 4, 4096, 6
     q, k, v = (torch.randn((B, n, h, 64), device="cuda", generator=g, dtype=torch.bfloat16) for _ in range(3))
     cfg = make_cfg(dfa, n, 512, 1, h, 64)
     L1 = torch.empty((B, h, n), dtype=torch.float32, device="cuda")
-    a = dfa.dfa_forward_multibranch(q, k, v, cfg, branches, lse=L1)
-    assert dfa.last_launch_count() == len(branches)
+    with multibranch_mode(_lib.DFA_MB_PER_BRANCH):
+        a = dfa.dfa_forward_multibranch(q, k, v, cfg, branches, lse=L1)
+        assert dfa.last_launch_count() == len(branches)
     L2 = torch.empty_like(L1)
     with path_override(_lib.DFA_PATH_SIMT):
         b = dfa.dfa_forward_multibranch(q, k, v, cfg, branches, lse=L2)

@@ -1,0 +1,127 @@
+"""Fused multi-(w, r) kernel (csrc/dfa_mb_sm100.cu): every branch and the LSE
+combine in ONE tcgen05 launch, checked against the extension oracle
+(oracle/dfa_oracle.c oracle_multibranch_f64: one dense softmax over the
+multiset of keys the covering branches select) and against the per-branch
+path.  bf16 bar: max|err| <= 2e-2, mean relative <= 1e-2."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BF16_MAX_ABS, BF16_MEAN_REL = 2e-2, 1e-2
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _inputs(B, n, h, seed):
+    torch = _torch()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return tuple(torch.randn((B, n, h, 64), device="cuda", generator=g, dtype=torch.bfloat16) for _ in range(3))
+
+
+def _full(dfa, h, branches):
+    out = []
+    for br in branches:
+        w, r = br[0], br[1]
+        offs = list(br[2]) if len(br) > 2 else dfa.AttentionConfig.spread_offsets(h, r)
+        out.append((w, r, offs))
+    return out
+
+
+SETS = [
+    [(512, 1), (1024, 2), (2048, 4), (4096, 8)],      # LongNet geometric set
+    [(256, 2), (512, 2), (1024, 4)],
+    [(4096, 8), (256, 4), (512, 1)],                  # sparse first branch
+    [(256, 2), (256, 2)],                             # duplicate branch (weights 1/2)
+    [(1024, 4), (2048, 8)],                           # no r = 1: rows / tiles no branch selects
+    [(128, 1), (256, 2), (64, 1)],                    # segments shorter than a query tile's span
+    [(2048, 2), (4096, 4)],
+]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("si", range(len(SETS)))
+def test_fused_vs_extension_oracle(dfa, port, cuda, si):
+    torch = _torch()
+    branches = SETS[si]
+    B, n, h = 2, 4096, 6
+    q, k, v = _inputs(B, n, h, 100 + si)
+    cfg = dfa.AttentionConfig(n, branches[0][0], branches[0][1], h, 64,
+                              dfa.AttentionConfig.spread_offsets(h, branches[0][1]))
+    L = torch.full((B, h, n), float("nan"), device="cuda")
+    o = torch.full((B, n, h, 64), float("nan"), device="cuda", dtype=torch.bfloat16)
+    dfa.dfa_forward_multibranch(q, k, v, cfg, branches, out=o, lse=L)
+    assert dfa.last_launch_count() == 1, "fused single-kernel path not taken"
+    torch.cuda.synchronize()
+    want, want_lse = port.multibranch_batched(*(x.double().cpu().numpy() for x in (q, k, v)),
+                                              _full(dfa, h, branches))
+    got = o.double().cpu().numpy()
+    assert np.isfinite(got).all()
+    err = np.abs(got - want)
+    mx, rel = float(err.max()), float(err.sum() / np.abs(want).sum())
+    assert mx <= BF16_MAX_ABS and rel <= BF16_MEAN_REL, (branches, mx, rel)
+    Lg = L.cpu().numpy()
+    fin = np.isfinite(want_lse)
+    assert np.array_equal(np.isfinite(Lg), fin)
+    assert np.abs(Lg[fin] - want_lse[fin]).max() <= 2e-2
+    # rows no branch selects: exact zeros (the buffer was NaN-poisoned)
+    unsel = ~fin.transpose(0, 2, 1)  # [B, N, h]
+    assert (got[unsel] == 0).all()
+
+
+@pytest.mark.timeout(300)
+def test_fused_custom_offsets(dfa, port, cuda):
+    """Per-branch head offsets that are not j mod r (any class mapping)."""
+    torch = _torch()
+    B, n, h = 1, 2048, 4
+    branches = [(256, 1, [0, 0, 0, 0]), (512, 4, [3, 1, 2, 0]), (1024, 8, [7, 5, 5, 2])]
+    q, k, v = _inputs(B, n, h, 5)
+    cfg = dfa.AttentionConfig(n, 256, 1, h, 64, [0] * h)
+    L = torch.empty((B, h, n), device="cuda")
+    o = dfa.dfa_forward_multibranch(q, k, v, cfg, branches, lse=L)
+    assert dfa.last_launch_count() == 1
+    torch.cuda.synchronize()
+    want, want_lse = port.multibranch_batched(*(x.double().cpu().numpy() for x in (q, k, v)), branches)
+    err = np.abs(o.double().cpu().numpy() - want)
+    assert err.max() <= BF16_MAX_ABS and err.sum() / np.abs(want).sum() <= BF16_MEAN_REL
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("si", [0, 2, 4])
+def test_fused_vs_per_branch_full_batch(dfa, cuda, si):
+    """B = 64, h = 6 (the bench batch): fused kernel vs the per-branch launches
+    (epilogue merge); bitwise-deterministic across runs."""
+    torch = _torch()
+    from paper_2403_09195_b200 import _lib, multibranch_mode
+
+    branches = SETS[si]
+    B, n, h = 64, 4096, 6
+    q, k, v = _inputs(B, n, h, 7 + si)
+    cfg = dfa.AttentionConfig(n, 512, 1, h, 64, [0] * h)
+    a = dfa.dfa_forward_multibranch(q, k, v, cfg, branches)
+    assert dfa.last_launch_count() == 1
+    a2 = dfa.dfa_forward_multibranch(q, k, v, cfg, branches)
+    with multibranch_mode(_lib.DFA_MB_PER_BRANCH):
+        b = dfa.dfa_forward_multibranch(q, k, v, cfg, branches)
+        assert dfa.last_launch_count() == len(branches)
+    torch.cuda.synchronize()
+    assert torch.equal(a, a2)
+    err = (a.float() - b.float()).abs()
+    assert err.max().item() <= BF16_MAX_ABS
+    assert (err.sum() / b.float().abs().sum()).item() <= BF16_MEAN_REL
+
+
+def test_fused_outside_envelope_falls_back(dfa, cuda):
+    """Five distinct intervals (> 4 tensor-map slots): per-branch launches."""
+    torch = _torch()
+    branches = [(64, 1), (128, 2), (256, 4), (512, 8), (1024, 16)]
+    q, k, v = _inputs(1, 2048, 2, 3)
+    cfg = dfa.AttentionConfig(2048, 64, 1, 2, 64, [0, 0])
+    a = dfa.dfa_forward_multibranch(q, k, v, cfg, branches)
+    assert dfa.last_launch_count() == len(branches)
+    torch.cuda.synchronize()
+    assert torch.isfinite(a.float()).all()
