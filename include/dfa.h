@@ -184,6 +184,10 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t n_branche
  * epilogue.  Process-wide. */
 enum { DFA_MB_AUTO = 0, DFA_MB_PER_BRANCH = 1 };
 void dfa_set_multibranch_mode(int32_t mode);
+/* Profiling hook: while `trace` (device, 6 x 4096 uint64) is non-NULL, fused
+ * multi-branch launches record CTA 0's timeline into it (dfa_forward_traced's
+ * format; scripts/trace_timeline.py decodes it). */
+void dfa_set_multibranch_trace(uint64_t* trace);
 
 /* Backward of the dilated core (the reference computes
  * it on its autodiff tape for the dilated branch of detail::attention_mix,

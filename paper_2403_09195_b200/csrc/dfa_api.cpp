@@ -152,6 +152,7 @@ void dfa_set_fault_perturb(int32_t armed) { g_fault.store(armed ? 1 : 0); }
 int32_t dfa_get_fault_perturb(void) { return g_fault.load(); }
 void dfa_set_path_override(int32_t path) { g_path_override.store(path); }
 void dfa_set_multibranch_mode(int32_t mode) { g_mb_mode.store(mode); }
+void dfa_set_multibranch_trace(uint64_t* trace) { dfa_impl::set_mb_trace(trace); }
 void dfa_set_host_zero_copy(int32_t enabled) { g_host_zero_copy.store(enabled ? 1 : 0); }
 void dfa_set_gemm_tile(int32_t bn) { dfa_impl::set_gemm_tile(bn); }
 

@@ -23,12 +23,13 @@
 // (w < 128 R) from paying for keys outside their segment.  Key tiles are
 // 128-row boxes of the branch's own r_b-stream (as in dfa_sm100.cu).
 //
-// Schedule (host, mb_build_plan): each work unit = head j + two query tiles
+// Schedule (host, build_plan): each work unit = head j + two query tiles
 // (slots A / B, paired for equal step counts and shared key tiles) + an
 // ordered list of key tiles, each tagged (branch, t', slot mask).  A key
 // tile used by both slots is loaded once.  Units are replicated over the
-// batch and LPT-assigned to the persistent CTAs (per-CTA work lists), so
-// the mixed unit costs of a branch set stay balanced.
+// batch into one list, most expensive first, which the persistent CTAs
+// claim dynamically (global counter, handed to the roles through a
+// shared-memory ring), so the mixed unit costs of a branch set balance.
 //
 // Warp roles, TMEM (3 S buffers + O_A, O_B), barriers and the softmax are
 // those of dfa_sm100_kernel; what changes is that every role walks the
@@ -61,6 +62,12 @@ constexpr int kQStages = 2, kKStages = 3, kVStages = 3, kOStages = 2;
 constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSBufs = 3;
+// Dynamic scheduling: the producer claims work units from a global counter
+// (most expensive first) and hands the index to the other roles through a
+// shared-memory ring; consumers = Q K^T issuer, P V issuer, V producer, 8
+// softmax warps and 4 epilogue warps.
+constexpr int kSchedDepth = 3;
+constexpr uint32_t kSchedConsumers = 15;
 __host__ __device__ constexpr uint32_t col_s(int buf) { return (uint32_t)kBN * buf; }
 __host__ __device__ constexpr uint32_t col_o(int slot) { return 384u + 64u * slot; }
 constexpr float kLog2e = 1.4426950408889634f;
@@ -107,8 +114,9 @@ struct MbParams {
   int32_t br_m[kMaxBranches], br_T[kMaxBranches], br_map[kMaxBranches];
   FastDivMb br_divr[kMaxBranches], br_divm[kMaxBranches];
   const MbDesc* desc;
-  const int2* work;        // (desc index, image)
-  const int32_t* cta_off;  // [grid + 1] work-list offsets per CTA
+  const int2* work;        // (desc index, image), most expensive first
+  int32_t n_work;
+  int32_t* counters;       // [0] next unit to claim, [1] CTAs done (both 0 between launches)
 };
 
 struct MbMaps {
@@ -131,6 +139,8 @@ struct __align__(1024) MbSmem {
   uint64_t pv_done[2];
   uint64_t o_full[2], o_empty[2];
   uint64_t stat_full[2], stat_empty[2];
+  uint64_t sched_full[kSchedDepth], sched_empty[kSchedDepth];
+  int32_t sched[kSchedDepth];  // claimed work-list index per ring slot (-1: no more work)
   float stat_l[2][2][kBM];
   float stat_m[2][2][kBM];
   uint32_t tmem_base;
@@ -140,9 +150,40 @@ __device__ __forceinline__ uint32_t tile_tp(uint32_t w) { return w & 0xFFFFFFu; 
 __device__ __forceinline__ int32_t tile_br(uint32_t w) { return (int32_t)((w >> 24) & 7u); }
 __device__ __forceinline__ uint32_t tile_mask(uint32_t w) { return (w >> 28) & 3u; }
 
+// Optional timeline trace (kTrace instantiation, profiling only): CTA 0
+// records (event << 56 | clock64) per role into trace[seg * 4096]; same
+// events and layout as dfa_sm100.cu (decoded by scripts/trace_timeline.py).
+constexpr int kTraceCap = 4096;
+#define MB_TRACE(seg, ev)                                                                          \
+  do {                                                                                             \
+    if constexpr (kTrace) {                                                                        \
+      if (tr_on && tr_n < kTraceCap)                                                               \
+        trace[(seg) * kTraceCap + tr_n++] = ((uint64_t)(ev) << 56) | (clock64() & 0xFFFFFFFFFFFFFFull); \
+    }                                                                                              \
+  } while (0)
+
+// Next claimed work-list index for a consumer role (n = units taken so far);
+// -1 once the list is exhausted.  kWarp: a whole warp reads the slot and its
+// lane 0 frees it (after __syncwarp); otherwise one elected thread does both.
+template <bool kWarp>
+__device__ __forceinline__ int32_t take_unit(MbSmem& sm, uint32_t& n) {
+  const uint32_t slot = n % kSchedDepth;
+  ptx::mbar_wait(&sm.sched_full[slot], (n / kSchedDepth) & 1u);
+  const int32_t wi = sm.sched[slot];
+  if constexpr (kWarp) {
+    __syncwarp();
+    if (ptx::lane_id() == 0) ptx::mbar_arrive(&sm.sched_empty[slot]);
+  } else {
+    ptx::mbar_arrive(&sm.sched_empty[slot]);
+  }
+  ++n;
+  return wi;
+}
+
+template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_mb_sm100_kernel(const __grid_constant__ MbMaps maps, float* __restrict__ lse,
-                        const __grid_constant__ MbParams p) {
+                        const __grid_constant__ MbParams p, uint64_t* __restrict__ trace) {
   extern __shared__ uint8_t smem_raw[];
   MbSmem& sm = *reinterpret_cast<MbSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t warp = ptx::warp_id();
@@ -177,6 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.stat_full[s], kBM);
       ptx::mbar_init(&sm.stat_empty[s], kBM);
     }
+    for (int i = 0; i < kSchedDepth; ++i) {
+      ptx::mbar_init(&sm.sched_full[i], 1);
+      ptx::mbar_init(&sm.sched_empty[i], kSchedConsumers);
+    }
     ptx::fence_barrier_init();
     ptx::tma_prefetch_desc(&maps.q);
     ptx::tma_prefetch_desc(&maps.o);
@@ -189,6 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tbase = sm.tmem_base;
   ptx::griddep_wait();
   ptx::griddep_launch_dependents();
+  if constexpr (kTrace) {
+    if (threadIdx.x == 0) trace[6 * kTraceCap + 2 * blockIdx.x] = ptx::globaltimer();
+  }
 
   // Registers: producers / MMA issuers 64, softmax 2 x 192, epilogue 64
   // (sum 65536); the work-list bounds are read inside each role so nothing
@@ -197,18 +245,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ============================================================ producer
     if (ptx::elect_one()) {
-      const int32_t w_begin = p.cta_off[blockIdx.x], w_end = p.cta_off[blockIdx.x + 1];
       const int32_t gr = 1 << p.gr_shift;
       const uint64_t pol = ptx::policy_evict_normal();  // key tiles are shared by several units
+      const bool tr_on = blockIdx.x == 0;
+      uint32_t tr_n = 0;
       uint32_t i = 0, g = 0;
-      for (int32_t wi = w_begin; wi < w_end; ++wi) {
+      for (uint32_t n = 0;; ++n) {
+        // claim the next unit once a Q stage is free (claimed work waits as little as possible)
+        const uint32_t qs = i % kQStages;
+        ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
+        const uint32_t slot = n % kSchedDepth;
+        ptx::mbar_wait(&sm.sched_empty[slot], ((n / kSchedDepth) & 1u) ^ 1u);
+        int32_t wi = atomicAdd(&p.counters[0], 1);
+        if (wi >= p.n_work) wi = -1;
+        sm.sched[slot] = wi;
+        ptx::mbar_arrive(&sm.sched_full[slot]);
+        if (wi < 0) break;
         const int2 wk = p.work[wi];
         const MbDesc& D = p.desc[wk.x];
         const int32_t n_tiles = D.n_tiles;
         if (n_tiles == 0) continue;
         const int32_t b = wk.y, j = D.j;
-        const uint32_t qs = i % kQStages;
-        ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
+        MB_TRACE(0, 1);
         const int act = (D.first[0] >= 0 ? 1 : 0) + (D.first[1] >= 0 ? 1 : 0);
         ptx::mbar_arrive_expect_tx(&sm.q_full[qs], act * kTileBytes);
         for (int s = 0; s < 2; ++s) {
@@ -222,7 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t w = D.tile[t];
           const int32_t br = tile_br(w);
           const uint32_t st = g % kKStages;
+          MB_TRACE(0, 2);
           ptx::mbar_wait(&sm.k_empty[st], ((g / kKStages) & 1) ^ 1);
+          MB_TRACE(0, 3);
           ptx::mbar_arrive_expect_tx(&sm.k_full[st], kTileBytes);
           ptx::tma_load_5d(sm.k[st], &maps.k[p.br_map[br]], &sm.k_full[st], 0, j, D.gamma[br], (int32_t)tile_tp(w),
                            b, pol);
@@ -232,10 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 3) {
     // ========================================================== V producer
     if (ptx::elect_one()) {
-      const int32_t w_begin = p.cta_off[blockIdx.x], w_end = p.cta_off[blockIdx.x + 1];
       const uint64_t pol = ptx::policy_evict_normal();
-      uint32_t g = 0;
-      for (int32_t wi = w_begin; wi < w_end; ++wi) {
+      uint32_t g = 0, n = 0;
+      for (;;) {
+        const int32_t wi = take_unit<false>(sm, n);
+        if (wi < 0) break;
         const int2 wk = p.work[wi];
         const MbDesc& D = p.desc[wk.x];
         const int32_t n_tiles = D.n_tiles, j = D.j;
@@ -253,22 +314,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ======================================================= Q K^T issuer
     if (ptx::elect_one()) {
-      const int32_t w_begin = p.cta_off[blockIdx.x], w_end = p.cta_off[blockIdx.x + 1];
       constexpr uint32_t idesc_qk = ptx::idesc_bf16(kBM, kBN, 0, 0);
       const uint64_t qdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.q[0][0]));
       const uint64_t kdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.k[0]));
       uint32_t b = 0, steps = 0, sfree_par = 0, gs = 0, gpar = 0, i = 0;
-      for (int32_t wi = w_begin; wi < w_end; ++wi) {
+      const bool tr_on = blockIdx.x == 0;
+      uint32_t tr_n = 0;
+      for (uint32_t n = 0;;) {
+        const int32_t wi = take_unit<false>(sm, n);
+        if (wi < 0) break;
         const MbDesc& D = p.desc[p.work[wi].x];
         const int32_t n_tiles = D.n_tiles;
         if (n_tiles == 0) continue;
         const uint32_t qs = i & 1;
+        MB_TRACE(1, 7);
         ptx::mbar_wait(&sm.q_full[qs], (i >> 1) & 1);
+        MB_TRACE(1, 19);
         ++i;
         for (int32_t t = 0; t < n_tiles; ++t) {
           const uint32_t mask = tile_mask(D.tile[t]);
           ptx::mbar_wait(&sm.k_full[gs], gpar);
           ptx::tc_fence_after();
+          MB_TRACE(1, 17);
           const uint64_t kd = kdesc0 + (uint64_t)(gs * (kTileBytes >> 4));
 #pragma unroll 1
           for (int sl = 0; sl < 2; ++sl) {
@@ -283,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kk = 0; kk < kD / 16; ++kk)
               ptx::mma_ss(tbase + col_s(b), qd + (uint64_t)(2 * kk), kd + (uint64_t)(2 * kk), idesc_qk, kk > 0);
             ptx::tc_commit(&sm.s_full[sl][b]);
+            MB_TRACE(1, 8);
             b = (b == kSBufs - 1) ? 0 : b + 1;
             ++steps;
           }
@@ -298,11 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {
     // ========================================================= P V issuer
     if (ptx::elect_one()) {
-      const int32_t w_begin = p.cta_off[blockIdx.x], w_end = p.cta_off[blockIdx.x + 1];
       constexpr uint32_t idesc_pv = ptx::idesc_bf16(kBM, kD, 0, 1);
       const uint64_t vdesc0 = ptx::sdesc_sw128(ptx::smem_u32(sm.v[0]));
       uint32_t b = 0, p_par = 0, oc_par = 0, gs = 0, gpar = 0;
-      for (int32_t wi = w_begin; wi < w_end; ++wi) {
+      const bool tr_on = blockIdx.x == 0;
+      uint32_t tr_n = 0;
+      for (uint32_t n = 0;;) {
+        const int32_t wi = take_unit<false>(sm, n);
+        if (wi < 0) break;
         const MbDesc& D = p.desc[p.work[wi].x];
         const int32_t n_tiles = D.n_tiles;
         const int32_t first0 = D.first[0], first1 = D.first[1], last0 = D.last[0], last1 = D.last[1];
@@ -314,7 +385,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int sl = 0; sl < 2; ++sl) {
             if (!((mask >> sl) & 1u)) continue;
             const bool first = t == (sl ? first1 : first0);
+            MB_TRACE(5, 4);
             ptx::mbar_wait(&sm.p_full[b], (p_par >> b) & 1u);
+            MB_TRACE(5, 5);
             p_par ^= 1u << b;
             if (first) ptx::mbar_wait(&sm.o_empty[sl], ((oc_par >> sl) & 1u) ^ 1u);
             if (!have_v) {
@@ -322,12 +395,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               have_v = true;
             }
             ptx::tc_fence_after();
+            MB_TRACE(5, 18);
 #pragma unroll
             for (int kk = 0; kk < kBN / 16; ++kk)
               ptx::mma_ts(tbase + col_o(sl), tbase + col_s(b) + kk * 8, vdesc + (uint64_t)(kk * (2048 >> 4)),
                           idesc_pv, (!first || kk > 0) ? 1u : 0u);
             ptx::tc_commit(&sm.pv_done[sl]);
             ptx::tc_commit(&sm.s_free[b]);
+            MB_TRACE(5, 6);
             if (t == (sl ? last1 : last0)) {
               ptx::tc_commit(&sm.o_full[sl]);
               oc_par ^= 1u << sl;
@@ -345,7 +420,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4 && warp < 12) {
     // ====================================================== softmax slots
     ptx::setmaxnreg_inc<192>();
-    const int32_t w_begin = p.cta_off[blockIdx.x], w_end = p.cta_off[blockIdx.x + 1];
     const int s = (warp - 4) / 4;
     const uint32_t row = (warp % 4) * 32 + lane;
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
@@ -354,7 +428,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int32_t rin = (int32_t)row & ((1 << p.gr_shift) - 1);
     uint32_t use_par = 0, pvc = 0, steps = 0, published = 0;
     uint32_t kbase = 0;  // CTA-global index of the unit's first step
-    for (int32_t wi = w_begin; wi < w_end; ++wi) {
+    const bool tr_on = blockIdx.x == 0 && row == 0;
+    uint32_t tr_n = 0;
+    for (uint32_t n = 0;;) {
+      const int32_t wi = take_unit<true>(sm, n);
+      if (wi < 0) break;
       const MbDesc& D = p.desc[p.work[wi].x];
       const int32_t n_tiles = D.n_tiles;
       const uint32_t k_unit = kbase;
@@ -387,7 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         const uint32_t b = (k_unit + here) % kSBufs;
+        MB_TRACE(2 + s, 9);
         ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
+        MB_TRACE(2 + s, 10);
         use_par ^= 1u << b;
         ptx::tc_fence_after();
         const uint32_t tS = tbase + lane_base + col_s(b);
@@ -477,10 +557,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_st32(tO + 32 * c, orow);
               }
             }
+            MB_TRACE(2 + s, 11);
             if (move) mref = tmax;
             l += exp_pass((mref == -INFINITY) ? 0.0f : -mref * p.c);
           }
         }  // rows with keys in this tile
+        MB_TRACE(2 + s, 12);
         if (!waited && steps > 0) {
           ptx::mbar_wait(&sm.pv_done[s], pvc & 1);
           ++pvc;
@@ -489,6 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&sm.p_full[b]);
+        MB_TRACE(2 + s, 13);
       }
       // rows no branch of this unit selects: l = 0 -> exact zeros in the epilogue
       const bool any = valid && ((D.anysel[s] >> grp) & 1u);
@@ -501,7 +584,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 12) {
     // ============================================================ epilogue
     ptx::setmaxnreg_dec<64>();
-    const int32_t w_begin = p.cta_off[blockIdx.x], w_end = p.cta_off[blockIdx.x + 1];
     const uint32_t row = (warp % 4) * 32 + lane;
     const uint32_t lane_base = ((warp % 4) * 32) << 16;
     const bool leader = warp == 12 && lane == 0;
@@ -509,7 +591,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int32_t rin = (int32_t)row & ((1 << p.gr_shift) - 1);
     const int32_t n_groups = kBM >> p.gr_shift;
     uint32_t par = 0;
-    for (int32_t wi = w_begin; wi < w_end; ++wi) {
+    const bool tr_on = blockIdx.x == 0 && leader;
+    uint32_t tr_n = 0;
+    for (uint32_t n = 0;;) {
+      const int32_t wi = take_unit<true>(sm, n);
+      if (wi < 0) break;
       const int2 wk = p.work[wi];
       const MbDesc& D = p.desc[wk.x];
       const int32_t b = wk.y, j = D.j;
@@ -533,7 +619,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint32_t ph = (par >> s) & 1u;
         par ^= 1u << s;
+        MB_TRACE(4, 14);
         ptx::mbar_wait(&sm.o_full[s], ph);
+        MB_TRACE(4, 15);
         ptx::mbar_wait(&sm.stat_full[s], ph);
         ptx::tc_fence_after();
         const float l = sm.stat_l[ph][s][row];
@@ -571,6 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tma_store_5d(&maps.o, sm.ostage[s] + gi * (128 << p.gr_shift), 0, j, D.cls[s][gi], qt, b);
           ptx::tma_store_commit();
         }
+        MB_TRACE(4, 16);
       }
     }
     if (leader) ptx::tma_store_wait_all<0>();
@@ -578,6 +667,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (kTrace) {
+    if (threadIdx.x == 0) trace[6 * kTraceCap + 2 * blockIdx.x + 1] = ptx::globaltimer();
+  }
+  if (threadIdx.x == 0) {
+    // every CTA has claimed past the end; the last one out re-arms the counters
+    __threadfence();
+    if (atomicAdd(&p.counters[1], 1) == (int32_t)gridDim.x - 1) {
+      p.counters[0] = 0;
+      p.counters[1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tbase);
@@ -626,22 +727,27 @@ struct TileInfo {
   int32_t lo[kMaxBranches], nt[kMaxBranches];
 };
 
+// A plan's work counters are claimed by one launch at a time: the key
+// includes the stream (launches on one stream are ordered; PDL waits for the
+// previous grid before any global access).
 struct PlanKey {
   int dev;
+  uintptr_t stream;
   int64_t N, h, B;
   int grid;
   std::vector<int64_t> br;  // w, r, offsets... per branch
   bool operator==(const PlanKey& o) const {
-    return dev == o.dev && N == o.N && h == o.h && B == o.B && grid == o.grid && br == o.br;
+    return dev == o.dev && stream == o.stream && N == o.N && h == o.h && B == o.B && grid == o.grid && br == o.br;
   }
 };
 
 struct DevicePlan {
   PlanKey key;
-  void* buf = nullptr;  // descs | work | cta_off
+  void* buf = nullptr;  // descs | work | counters
   const MbDesc* desc = nullptr;
   const int2* work = nullptr;
-  const int32_t* cta_off = nullptr;
+  int32_t* counters = nullptr;
+  int32_t n_work = 0;
   int32_t R = 1, gr_shift = 7, grid = 1;
   int n_maps = 0;
   int64_t r_of_map[kMbMaxMaps] = {};
@@ -812,72 +918,50 @@ bool build_plan(const Geometry* gb, int nb, int grid, DevicePlan* out, std::vect
       desc_su.push_back(std::min(ts[0]->su, ts[1] ? ts[1]->su : ts[0]->su));
     }
   }
-  // Replicate over the batch and assign to the persistent CTAs in time order
-  // (image, super-unit, head): each unit goes to the least-loaded CTA, so the
-  // units that share a super-unit's key tiles run at about the same time
-  // (their re-reads hit L2) while the mixed unit costs stay balanced.
+  // Replicate over the batch into ONE work list, most expensive units first
+  // (the CTAs claim them dynamically: longest-processing-time-first without a
+  // cost model); within a cost class image-major, then (super-unit, head), so
+  // CTAs running side by side read the h heads' column blocks of the same
+  // token rows and share super-units' key tiles in L2.
   const int64_t n_desc = (int64_t)descs.size();
   const int64_t n_work = n_desc * B;
   if (n_work > INT32_MAX / 2) return (*why = "too many work units"), false;
-  std::vector<int> dorder(n_desc);
-  std::iota(dorder.begin(), dorder.end(), 0);
-#ifndef DFA_MB_ORDER
-#define DFA_MB_ORDER 0
-#endif
-  std::stable_sort(dorder.begin(), dorder.end(), [&](int a, int b) {
-    if (DFA_MB_ORDER == 0) return descs[a].steps > descs[b].steps;
-    if (desc_su[a] != desc_su[b]) return desc_su[a] < desc_su[b];
-    if (descs[a].j != descs[b].j) return descs[a].j < descs[b].j;
-    return descs[a].steps > descs[b].steps;
+  std::vector<int2> seq;
+  seq.reserve((size_t)n_work);
+  for (int64_t e = 0; e < n_desc; ++e)
+    for (int64_t b = 0; b < B; ++b) seq.push_back(make_int2((int)e, (int)b));
+  std::stable_sort(seq.begin(), seq.end(), [&](int2 x, int2 y) {
+    const MbDesc &dx = descs[x.x], &dy = descs[y.x];
+    if (dx.steps != dy.steps) return dx.steps > dy.steps;
+    if (x.y != y.y) return x.y < y.y;
+    if (desc_su[x.x] != desc_su[y.x]) return desc_su[x.x] < desc_su[y.x];
+    return dx.j < dy.j;
   });
   grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, n_work));
-  std::vector<std::vector<int2>> lists(grid);
-  using Load = std::pair<int64_t, int>;
-  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-  for (int c = 0; c < grid; ++c) heap.push({0, c});
-  std::vector<int2> seq;
-  for (int e : dorder)
-    for (int64_t b = 0; b < B; ++b) seq.push_back(make_int2(e, (int)b));
-  if (DFA_MB_ORDER == 1)
-    std::stable_sort(seq.begin(), seq.end(), [](int2 a, int2 b) { return a.y < b.y; });
-  for (const int2& x : seq) {
-    {
-      const int e = x.x, b = x.y;
-      const int64_t cost = descs[e].steps + 2;  // + Q load / epilogue
-      Load ld = heap.top();
-      heap.pop();
-      lists[ld.second].push_back(make_int2(e, (int)b));
-      heap.push({ld.first + cost, ld.second});
-    }
-  }
   const size_t desc_bytes = sizeof(MbDesc) * (size_t)n_desc;
   const size_t work_bytes = sizeof(int2) * (size_t)n_work;
-  const size_t off_bytes = sizeof(int32_t) * (size_t)(grid + 1);
-  const size_t work_at = (desc_bytes + 255) & ~(size_t)255, off_at = (work_at + work_bytes + 255) & ~(size_t)255;
-  blob->assign(off_at + off_bytes, 0);
+  const size_t work_at = (desc_bytes + 255) & ~(size_t)255, cnt_at = (work_at + work_bytes + 255) & ~(size_t)255;
+  blob->assign(cnt_at + 256, 0);  // counters start at 0
   memcpy(blob->data(), descs.data(), desc_bytes);
-  int2* wl = reinterpret_cast<int2*>(blob->data() + work_at);
-  int32_t* off = reinterpret_cast<int32_t*>(blob->data() + off_at);
-  int32_t pos = 0;
-  for (int c = 0; c < grid; ++c) {
-    off[c] = pos;
-    for (const int2& x : lists[c]) wl[pos++] = x;
-  }
-  off[grid] = pos;
+  memcpy(blob->data() + work_at, seq.data(), work_bytes);
+  out->n_work = (int32_t)n_work;
   out->grid = grid;
   out->steps = total_steps * B;
-  // offsets of the three arrays inside the device buffer (patched by the caller)
+  // offsets of the arrays inside the device buffer (patched by the caller)
   out->desc = reinterpret_cast<const MbDesc*>(0);
   out->work = reinterpret_cast<const int2*>(work_at);
-  out->cta_off = reinterpret_cast<const int32_t*>(off_at);
+  out->counters = reinterpret_cast<int32_t*>(cnt_at);
   return true;
 }
 
 std::mutex g_plan_mu;
+std::atomic<uint64_t*> g_mb_trace{nullptr};
 std::vector<DevicePlan> g_plans;  // small LRU (front = most recent)
 constexpr size_t kMaxPlans = 16;
 
 }  // namespace
+
+void set_mb_trace(uint64_t* trace) { g_mb_trace.store(trace); }
 
 // Fused multi-branch forward: returns 1 (launch issued), 0 when the set is
 // outside the kernel's envelope (why set, nothing launched) or -1 on a CUDA
@@ -892,6 +976,7 @@ int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, co
   const Geometry& g0 = gb[0];
   PlanKey key;
   key.dev = current_device();
+  key.stream = reinterpret_cast<uintptr_t>(stream);
   key.N = g0.N;
   key.h = g0.h;
   key.B = g0.B;
@@ -934,7 +1019,7 @@ int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, co
       char* base = static_cast<char*>(plan.buf);
       plan.desc = reinterpret_cast<const MbDesc*>(base);
       plan.work = reinterpret_cast<const int2*>(base + reinterpret_cast<uintptr_t>(plan.work));
-      plan.cta_off = reinterpret_cast<const int32_t*>(base + reinterpret_cast<uintptr_t>(plan.cta_off));
+      plan.counters = reinterpret_cast<int32_t*>(base + reinterpret_cast<uintptr_t>(plan.counters));
       if (g_plans.size() == kMaxPlans) {
         cudaStreamSynchronize(stream);
         cudaFree(g_plans.back().buf);
@@ -974,15 +1059,23 @@ int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, co
   }
   p.desc = plan.desc;
   p.work = plan.work;
-  p.cta_off = plan.cta_off;
+  p.counters = plan.counters;
+  p.n_work = plan.n_work;
   const size_t smem = sizeof(MbSmem) + 1024;
-  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(dfa_mb_sm100_kernel), smem);
+  uint64_t* trace = g_mb_trace.load();
+  cudaError_t ae = ensure_smem_attr(
+      reinterpret_cast<const void*>(trace ? dfa_mb_sm100_kernel<true> : dfa_mb_sm100_kernel<false>), smem);
   if (ae != cudaSuccess) {
     *err = ae;
     *why = "cudaFuncSetAttribute failed";
     return -1;
   }
-  cudaError_t le = launch_pdl(dfa_mb_sm100_kernel, plan.grid, kThreads, smem, stream, maps, lse, p);
+  cudaError_t le = cudaSuccess;
+  if (trace)
+    dfa_mb_sm100_kernel<true><<<plan.grid, kThreads, smem, stream>>>(maps, lse, p, trace);
+  else
+    le = launch_pdl(dfa_mb_sm100_kernel<false>, plan.grid, kThreads, smem, stream, maps, lse, p,
+                    (uint64_t*)nullptr);
   *err = le != cudaSuccess ? le : cudaGetLastError();
   if (*err != cudaSuccess) {
     *why = "launch failed";

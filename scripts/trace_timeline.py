@@ -20,6 +20,38 @@ NAMES = {1: "Q_ISSUE", 2: "KV_WAIT", 3: "KV_ISSUE", 4: "P_WAIT", 5: "P_READY", 6
 ROLES = ["producer", "mma", "softmax_A", "softmax_B", "epilogue", "pv"]
 
 
+def run_mb(args):
+    """Fused multi-branch kernel (dfa_set_multibranch_trace) on --set."""
+    import torch
+
+    import paper_2403_09195_b200 as dfa
+
+    sets = {"longnet": [(512, 1), (1024, 2), (2048, 4), (4096, 8)], "long2": [(2048, 2), (4096, 4)],
+            "r2set": [(256, 2), (512, 2), (1024, 4)]}
+    br = sets[args.set]
+    h = 6
+    cfg = dfa.AttentionConfig(4096, 512, 1, h, 64, [0] * h)
+    q, k, v = (torch.randn((args.batch, 4096, h, 64), device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    o = torch.empty_like(q)
+    tr = torch.zeros(6 * CAP + 2048, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        dfa.dfa_forward_multibranch(q, k, v, cfg, br, out=o)
+    dfa.lib.dfa_set_multibranch_trace(tr.data_ptr())
+    dfa.dfa_forward_multibranch(q, k, v, cfg, br, out=o)
+    dfa.lib.dfa_set_multibranch_trace(None)
+    torch.cuda.synchronize()
+    out = os.path.join(ROOT, "gpurun_out", f"trace_mb_{args.set}.npy")
+    raw = tr.cpu().numpy().astype(np.uint64)
+    np.save(out, raw[:6 * CAP])
+    ct = raw[6 * CAP:].astype(np.int64).reshape(-1, 2)
+    ct = ct[ct[:, 0] > 0]
+    t0 = ct[:, 0].min()
+    ends = (ct[:, 1] - t0) / 1e3
+    print(f"per-CTA end (us): min {ends.min():.1f} median {np.median(ends):.1f} max {ends.max():.1f}; "
+          f"start spread {(ct[:, 0].max() - t0) / 1e3:.1f} us")
+    show(out)
+
+
 def run(args):
     import torch
 
@@ -103,10 +135,11 @@ def show(path):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("cmd", choices=["run", "show"])
+    ap.add_argument("cmd", choices=["run", "run_mb", "show"])
+    ap.add_argument("--set", default="longnet")
     ap.add_argument("path", nargs="?")
     ap.add_argument("--w", type=int, default=512)
     ap.add_argument("--r", type=int, default=2)
     ap.add_argument("--batch", type=int, default=64)
     a = ap.parse_args()
-    run(a) if a.cmd == "run" else show(a.path)
+    {"run": run, "run_mb": run_mb}[a.cmd](a) if a.cmd != "show" else show(a.path)
