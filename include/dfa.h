@@ -184,7 +184,7 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t n_branche
  * epilogue.  Process-wide. */
 enum { DFA_MB_AUTO = 0, DFA_MB_PER_BRANCH = 1 };
 void dfa_set_multibranch_mode(int32_t mode);
-/* Profiling hook: while `trace` (device, 6 x 4096 uint64) is non-NULL, fused
+/* Profiling hook: while `trace` (device, 6 x 4096 + 2 x #SMs uint64) is non-NULL, fused
  * multi-branch launches record CTA 0's timeline into it (dfa_forward_traced's
  * format; scripts/trace_timeline.py decodes it). */
 void dfa_set_multibranch_trace(uint64_t* trace);
@@ -262,7 +262,8 @@ dfa_status_t dfa_encoder_block_forward(const dfa_config_t* cfg, dfa_dtype_t dtyp
                                        size_t workspace_bytes, void* stream);
 
 /* Profiling hook: dfa_forward (bf16, tcgen05 path only) of a build of the
- * kernel that records a timeline of CTA 0 into `trace` (6 x 4096 uint64:
+ * kernel that records a timeline of CTA 0 into `trace` (6 x 4096 uint64, then each
+ * CTA's start / end %globaltimer at [6 x 4096 + 2 cta]: 6 x 4096 + 2 x #SMs entries;
  * per role producer / QK issuer / softmax A / softmax B / epilogue / PV issuer, entries
  * (event << 56) | clock64).  scripts/trace_timeline.py decodes it. */
 dfa_status_t dfa_forward_traced(const dfa_config_t* cfg, int64_t batch, const void* q, const void* k, const void* v,

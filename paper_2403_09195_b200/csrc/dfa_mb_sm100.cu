@@ -162,24 +162,6 @@ constexpr int kTraceCap = 4096;
     }                                                                                              \
   } while (0)
 
-// Next claimed work-list index for a consumer role (n = units taken so far);
-// -1 once the list is exhausted.  kWarp: a whole warp reads the slot and its
-// lane 0 frees it (after __syncwarp); otherwise one elected thread does both.
-template <bool kWarp>
-__device__ __forceinline__ int32_t take_unit(MbSmem& sm, uint32_t& n) {
-  const uint32_t slot = n % kSchedDepth;
-  ptx::mbar_wait(&sm.sched_full[slot], (n / kSchedDepth) & 1u);
-  const int32_t wi = sm.sched[slot];
-  if constexpr (kWarp) {
-    __syncwarp();
-    if (ptx::lane_id() == 0) ptx::mbar_arrive(&sm.sched_empty[slot]);
-  } else {
-    ptx::mbar_arrive(&sm.sched_empty[slot]);
-  }
-  ++n;
-  return wi;
-}
-
 template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_mb_sm100_kernel(const __grid_constant__ MbMaps maps, float* __restrict__ lse,
@@ -254,12 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // claim the next unit once a Q stage is free (claimed work waits as little as possible)
         const uint32_t qs = i % kQStages;
         ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
-        const uint32_t slot = n % kSchedDepth;
-        ptx::mbar_wait(&sm.sched_empty[slot], ((n / kSchedDepth) & 1u) ^ 1u);
-        int32_t wi = atomicAdd(&p.counters[0], 1);
-        if (wi >= p.n_work) wi = -1;
-        sm.sched[slot] = wi;
-        ptx::mbar_arrive(&sm.sched_full[slot]);
+        const int32_t wi =
+            ptx::claim_unit<kSchedDepth>(sm.sched_full, sm.sched_empty, sm.sched, n, p.counters, p.n_work);
         if (wi < 0) break;
         const int2 wk = p.work[wi];
         const MbDesc& D = p.desc[wk.x];
@@ -295,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol = ptx::policy_evict_normal();
       uint32_t g = 0, n = 0;
       for (;;) {
-        const int32_t wi = take_unit<false>(sm, n);
+        const int32_t wi = ptx::take_unit<kSchedDepth, false>(sm.sched_full, sm.sched_empty, sm.sched, n);
         if (wi < 0) break;
         const int2 wk = p.work[wi];
         const MbDesc& D = p.desc[wk.x];
@@ -321,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool tr_on = blockIdx.x == 0;
       uint32_t tr_n = 0;
       for (uint32_t n = 0;;) {
-        const int32_t wi = take_unit<false>(sm, n);
+        const int32_t wi = ptx::take_unit<kSchedDepth, false>(sm.sched_full, sm.sched_empty, sm.sched, n);
         if (wi < 0) break;
         const MbDesc& D = p.desc[p.work[wi].x];
         const int32_t n_tiles = D.n_tiles;
@@ -372,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool tr_on = blockIdx.x == 0;
       uint32_t tr_n = 0;
       for (uint32_t n = 0;;) {
-        const int32_t wi = take_unit<false>(sm, n);
+        const int32_t wi = ptx::take_unit<kSchedDepth, false>(sm.sched_full, sm.sched_empty, sm.sched, n);
         if (wi < 0) break;
         const MbDesc& D = p.desc[p.work[wi].x];
         const int32_t n_tiles = D.n_tiles;
@@ -431,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tr_on = blockIdx.x == 0 && row == 0;
     uint32_t tr_n = 0;
     for (uint32_t n = 0;;) {
-      const int32_t wi = take_unit<true>(sm, n);
+      const int32_t wi = ptx::take_unit<kSchedDepth, true>(sm.sched_full, sm.sched_empty, sm.sched, n);
       if (wi < 0) break;
       const MbDesc& D = p.desc[p.work[wi].x];
       const int32_t n_tiles = D.n_tiles;
@@ -594,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tr_on = blockIdx.x == 0 && leader;
     uint32_t tr_n = 0;
     for (uint32_t n = 0;;) {
-      const int32_t wi = take_unit<true>(sm, n);
+      const int32_t wi = ptx::take_unit<kSchedDepth, true>(sm.sched_full, sm.sched_empty, sm.sched, n);
       if (wi < 0) break;
       const int2 wk = p.work[wi];
       const MbDesc& D = p.desc[wk.x];
@@ -670,15 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (kTrace) {
     if (threadIdx.x == 0) trace[6 * kTraceCap + 2 * blockIdx.x + 1] = ptx::globaltimer();
   }
-  if (threadIdx.x == 0) {
-    // every CTA has claimed past the end; the last one out re-arms the counters
-    __threadfence();
-    if (atomicAdd(&p.counters[1], 1) == (int32_t)gridDim.x - 1) {
-      p.counters[0] = 0;
-      p.counters[1] = 0;
-      __threadfence();
-    }
-  }
+  if (threadIdx.x == 0) ptx::rearm_counters(p.counters);  // every CTA has claimed past the end
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tbase);

@@ -362,6 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // may start their own setup right away (they wait the same way).
   ptx::griddep_wait();
   ptx::griddep_launch_dependents();
+  if constexpr (kTrace) {  // per-CTA start / end (globaltimer) after the role timelines
+    if (threadIdx.x == 0) trace[6 * kTraceCap + 2 * blockIdx.x] = ptx::globaltimer();
+  }
 
   // Registers: 512 x 128 at launch; rebalanced per warpgroup to
   // producer/MMA 40, softmax 2 x 192, epilogue 80 (sum 64512 <= 65536).  192
@@ -803,6 +806,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
+  if constexpr (kTrace) {
+    if (threadIdx.x == 0) trace[6 * kTraceCap + 2 * blockIdx.x + 1] = ptx::globaltimer();
+  }
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tbase);

@@ -69,6 +69,49 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
+// ------------------------------------------------- dynamic unit scheduling
+// A persistent kernel's producer claims work units from a global counter and
+// hands each index to the CTA's other roles through a shared-memory ring of
+// `depth` slots (full: 1 arrival, empty: one per consumer agent).  The last
+// CTA to finish re-arms the counters (counters[0] = next unit, [1] = CTAs
+// done), so stream-ordered launches (incl. PDL, whose griddepcontrol.wait
+// precedes every global access) and graph replays reuse them.
+template <int kDepth>
+__device__ __forceinline__ int32_t claim_unit(uint64_t* full, uint64_t* empty, int32_t* ring, uint32_t n,
+                                              int32_t* counters, int32_t n_units) {
+  const uint32_t slot = n % kDepth;
+  mbar_wait(&empty[slot], ((n / kDepth) & 1u) ^ 1u);
+  int32_t u = counters ? atomicAdd(&counters[0], 1) : (int32_t)(blockIdx.x + n * gridDim.x);
+  if (u >= n_units) u = -1;
+  ring[slot] = u;
+  mbar_arrive(&full[slot]);
+  return u;
+}
+// Consumer side; kWarp: the whole warp reads, lane 0 frees the slot.
+template <int kDepth, bool kWarp>
+__device__ __forceinline__ int32_t take_unit(uint64_t* full, uint64_t* empty, const int32_t* ring, uint32_t& n) {
+  const uint32_t slot = n % kDepth;
+  mbar_wait(&full[slot], (n / kDepth) & 1u);
+  const int32_t u = *reinterpret_cast<const volatile int32_t*>(&ring[slot]);
+  if constexpr (kWarp) {
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(&empty[slot]);
+  } else {
+    mbar_arrive(&empty[slot]);
+  }
+  ++n;
+  return u;
+}
+__device__ __forceinline__ void rearm_counters(int32_t* counters) {
+  if (!counters) return;
+  __threadfence();
+  if (atomicAdd(&counters[1], 1) == (int32_t)gridDim.x - 1) {
+    counters[0] = 0;
+    counters[1] = 0;
+    __threadfence();
+  }
+}
+
 // --------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");

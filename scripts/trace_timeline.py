@@ -41,14 +41,19 @@ def run_mb(args):
     dfa.lib.dfa_set_multibranch_trace(None)
     torch.cuda.synchronize()
     out = os.path.join(ROOT, "gpurun_out", f"trace_mb_{args.set}.npy")
+    save_and_show(tr, out)
+
+
+def save_and_show(tr, out):
     raw = tr.cpu().numpy().astype(np.uint64)
     np.save(out, raw[:6 * CAP])
     ct = raw[6 * CAP:].astype(np.int64).reshape(-1, 2)
     ct = ct[ct[:, 0] > 0]
-    t0 = ct[:, 0].min()
-    ends = (ct[:, 1] - t0) / 1e3
-    print(f"per-CTA end (us): min {ends.min():.1f} median {np.median(ends):.1f} max {ends.max():.1f}; "
-          f"start spread {(ct[:, 0].max() - t0) / 1e3:.1f} us")
+    if len(ct):
+        t0 = ct[:, 0].min()
+        ends = (ct[:, 1] - t0) / 1e3
+        print(f"per-CTA end (us): min {ends.min():.1f} median {np.median(ends):.1f} max {ends.max():.1f}; "
+              f"start spread {(ct[:, 0].max() - t0) / 1e3:.1f} us")
     show(out)
 
 
@@ -63,7 +68,7 @@ def run(args):
     cfg = dfa.AttentionConfig(4096, args.w, args.r, h, 64, offs)
     q, k, v = (torch.randn((args.batch, 4096, h, 64), device="cuda", dtype=torch.bfloat16) for _ in range(3))
     o = torch.empty_like(q)
-    tr = torch.zeros(6 * CAP, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(6 * CAP + 2048, dtype=torch.int64, device="cuda")
     c = cfg._c()
     for _ in range(3):  # warm (clocks, L2 state)
         dfa.dfa_forward(q, k, v, cfg, out=o)
@@ -71,8 +76,7 @@ def run(args):
                                           o.data_ptr(), tr.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     out = os.path.join(ROOT, "gpurun_out", f"trace_w{args.w}_r{args.r}.npy")
-    np.save(out, tr.cpu().numpy().astype(np.uint64))
-    show(out)
+    save_and_show(tr, out)
 
 
 def decode(path):
