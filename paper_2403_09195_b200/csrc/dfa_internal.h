@@ -2,6 +2,7 @@
 // device kernels (dfa_simt.cu, dfa_sm100.cu).  Not installed.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdlib.h>
 #include <stdint.h>
@@ -104,6 +105,11 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, siz
 // fp32 arithmetic, online softmax over key tiles.  Returns launches issued.
 int launch_simt(const Geometry& g, int dtype, const void* q, const void* k, const void* v, void* o, float* lse,
                 cudaStream_t stream, cudaError_t* err);
+
+// [B][N/r][r][h][64] bf16 t'-stream tensor map (box 64 x rows, 128-byte
+// swizzle), from a per-thread cache of recent encodes (dfa_sm100.cu).
+bool encode_stream_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld,
+                       uint32_t rows);
 
 // True when the tcgen05/TMA kernel covers this call.
 bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o);

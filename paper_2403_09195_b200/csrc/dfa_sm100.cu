@@ -838,8 +838,8 @@ EncodeTiledFn get_encode_fn() {
 // out-of-range rows are zero-filled on load and dropped on store.  `ld` is
 // the token stride in elements (h * 64 when contiguous; 3 * h * 64 when q,
 // k, v are column blocks of one fused-projection output).
-bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld,
-              uint32_t box_rows = 128) {
+bool encode_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld,
+                uint32_t box_rows) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[5] = {(cuuint64_t)kD, (cuuint64_t)h, (cuuint64_t)r, (cuuint64_t)(N / r), (cuuint64_t)B};
@@ -852,7 +852,48 @@ bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t 
   return res == CUDA_SUCCESS;
 }
 
+// Encoding a tensor map costs a driver call (~2-4 us host time); callers
+// re-launch on the same buffers, so the last encodes are cached per host
+// thread (key: every input of the encoding).
+bool make_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld,
+              uint32_t box_rows = 128) {
+  struct Entry {
+    CUtensorMap map;
+    const void* base;
+    int64_t B, N, r, h, ld;
+    uint32_t rows;
+    int dev;
+  };
+  constexpr int kEntries = 32;
+  thread_local Entry cache[kEntries];
+  thread_local int used = 0, next = 0;
+  const int dev = current_device();
+  for (int i = 0; i < used; ++i) {
+    const Entry& e = cache[i];
+    if (e.base == base && e.B == B && e.N == N && e.r == r && e.h == h && e.ld == ld && e.rows == box_rows &&
+        e.dev == dev) {
+      *map = e.map;
+      return true;
+    }
+  }
+  if (!encode_map(map, base, B, N, r, h, ld, box_rows)) return false;
+  Entry& e = cache[next];
+  e.map = *map;
+  e.base = base;
+  e.B = B, e.N = N, e.r = r, e.h = h, e.ld = ld;
+  e.rows = box_rows;
+  e.dev = dev;
+  next = (next + 1) % kEntries;
+  if (used < kEntries) ++used;
+  return true;
+}
+
 }  // namespace
+
+bool encode_stream_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t r, int64_t h, int64_t ld,
+                       uint32_t rows) {
+  return make_map(map, base, B, N, r, h, ld, rows);
+}
 
 bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* o) {
   if (dtype != 1) return false;              // bf16 only
