@@ -633,7 +633,12 @@ def wl_config4(ctx, steps, warmup):
 
 
 def wl_lse(ctx, steps, warmup):
+    """LSE-combined LongNet set (extension, north_star item 3): the fused
+    single-kernel path (every branch + the combine in one tcgen05 launch) and,
+    timed beside it, the per-branch path (one launch per branch, epilogue merge)."""
     torch, dfa = ctx.torch, ctx.dfa
+    from paper_2403_09195_b200 import _lib, multibranch_mode
+
     hbm, tc, _ = peaks()
     B = 64
     q, k, v = (ctx.randn((B, N_TOK, H, D), 91 + i) for i in range(3))
@@ -646,14 +651,18 @@ def wl_lse(ctx, steps, warmup):
         return dfa.last_launch_count()
 
     total_ms, launches, clocks = ctx.timed(step, steps, warmup)
-    ms = total_ms / steps
+    with multibranch_mode(_lib.DFA_MB_PER_BRANCH):
+        pb_ms, pb_launches, pb_clocks = ctx.timed(step, steps, warmup)
+    ms, pb = total_ms / steps, pb_ms / steps
     fl = sum(flop_per_unit(w, r) for w, r in LSE_SET) * H * B
     by = (3 * 2 * D * N_TOK + 2 * D * N_TOK) * H * B  # q, k, v read once + o written once (fused ideal)
     tf = fl / (ms / 1e3) / 1e12
     return {"value": B * ctx.world / (ms / 1e3), "unit": "images/s", "ms_per_step": ms, "tflops": tf,
             "tensor_peak_frac": tf / tc, "gpu_launches": launches, "clocks": clocks, "dtype": "bf16",
             "scaling": "weak", "branches": LSE_SET, "launches_per_call": launches // max(1, steps),
-            "AI_fused": fl / by}
+            "kernel": "dfa_mb_sm100_kernel (all branches + LSE combine, one launch)", "AI_fused": fl / by,
+            "per_branch": {"ms_per_step": pb, "tflops": fl / (pb / 1e3) / 1e12,
+                           "launches_per_call": pb_launches // max(1, steps), "clocks": pb_clocks}}
 
 
 def wl_config5(ctx, steps, warmup):

@@ -63,10 +63,13 @@ constexpr int kThreads = 512;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kSBufs = 3;
 // Dynamic scheduling: the producer claims work units from a global counter
-// (most expensive first) and hands the index to the other roles through a
-// shared-memory ring; consumers = Q K^T issuer, P V issuer, V producer, 8
+// (most expensive first) and hands each to the other roles through a
+// shared-memory ring that also holds the unit's descriptor (bulk-copied from
+// global memory, so no role waits on an L2 round trip per unit or reads the
+// key-tile list from global memory per step).  A role frees its slot when it
+// takes the next unit; consumers = Q K^T issuer, P V issuer, V producer, 8
 // softmax warps and 4 epilogue warps.
-constexpr int kSchedDepth = 3;
+constexpr int kSchedDepth = 6;
 constexpr uint32_t kSchedConsumers = 15;
 __host__ __device__ constexpr uint32_t col_s(int buf) { return (uint32_t)kBN * buf; }
 __host__ __device__ constexpr uint32_t col_o(int slot) { return 384u + 64u * slot; }
@@ -140,7 +143,9 @@ struct __align__(1024) MbSmem {
   uint64_t o_full[2], o_empty[2];
   uint64_t stat_full[2], stat_empty[2];
   uint64_t sched_full[kSchedDepth], sched_empty[kSchedDepth];
-  int32_t sched[kSchedDepth];  // claimed work-list index per ring slot (-1: no more work)
+  int32_t sched[kSchedDepth];    // claimed work-list index per ring slot (-1: no more work)
+  int32_t sched_b[kSchedDepth];  // its image
+  MbDesc dring[kSchedDepth];     // its descriptor, bulk-copied by the producer
   float stat_l[2][2][kBM];
   float stat_m[2][2][kBM];
   uint32_t tmem_base;
@@ -161,6 +166,25 @@ constexpr int kTraceCap = 4096;
         trace[(seg) * kTraceCap + tr_n++] = ((uint64_t)(ev) << 56) | (clock64() & 0xFFFFFFFFFFFFFFull); \
     }                                                                                              \
   } while (0)
+
+// Consumer side of the ring: free the previous unit's slot (n > 0), wait for
+// unit n; returns its slot (the work index is sm.sched[slot], -1 = done).
+// kWarp: a whole warp takes the unit and its lane 0 frees the slot.
+template <bool kWarp>
+__device__ __forceinline__ uint32_t next_slot(MbSmem& sm, uint32_t n) {
+  if (n > 0) {
+    const uint32_t prev = (n - 1) % kSchedDepth;
+    if constexpr (kWarp) {
+      __syncwarp();
+      if (ptx::lane_id() == 0) ptx::mbar_arrive(&sm.sched_empty[prev]);
+    } else {
+      ptx::mbar_arrive(&sm.sched_empty[prev]);
+    }
+  }
+  const uint32_t slot = n % kSchedDepth;
+  ptx::mbar_wait(&sm.sched_full[slot], (n / kSchedDepth) & 1u);
+  return slot;
+}
 
 template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -236,11 +260,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         // claim the next unit once a Q stage is free (claimed work waits as little as possible)
         const uint32_t qs = i % kQStages;
         ptx::mbar_wait(&sm.q_empty[qs], ((i / kQStages) & 1) ^ 1);
-        const int32_t wi =
-            ptx::claim_unit<kSchedDepth>(sm.sched_full, sm.sched_empty, sm.sched, n, p.counters, p.n_work);
-        if (wi < 0) break;
+        const uint32_t slot = n % kSchedDepth;
+        ptx::mbar_wait(&sm.sched_empty[slot], ((n / kSchedDepth) & 1u) ^ 1u);
+        int32_t wi = atomicAdd(&p.counters[0], 1);
+        if (wi >= p.n_work) wi = -1;
+        sm.sched[slot] = wi;
+        if (wi < 0) {
+          ptx::mbar_arrive(&sm.sched_full[slot]);
+          break;
+        }
         const int2 wk = p.work[wi];
-        const MbDesc& D = p.desc[wk.x];
+        sm.sched_b[slot] = wk.y;
+        ptx::mbar_arrive_expect_tx(&sm.sched_full[slot], (uint32_t)sizeof(MbDesc));
+        ptx::bulk_g2s(&sm.dring[slot], p.desc + wk.x, (uint32_t)sizeof(MbDesc), &sm.sched_full[slot]);
+        ptx::mbar_wait(&sm.sched_full[slot], (n / kSchedDepth) & 1u);
+        const MbDesc& D = sm.dring[slot];
         const int32_t n_tiles = D.n_tiles;
         if (n_tiles == 0) continue;
         const int32_t b = wk.y, j = D.j;
@@ -271,13 +305,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ========================================================== V producer
     if (ptx::elect_one()) {
       const uint64_t pol = ptx::policy_evict_normal();
-      uint32_t g = 0, n = 0;
-      for (;;) {
-        const int32_t wi = ptx::take_unit<kSchedDepth, false>(sm.sched_full, sm.sched_empty, sm.sched, n);
-        if (wi < 0) break;
-        const int2 wk = p.work[wi];
-        const MbDesc& D = p.desc[wk.x];
-        const int32_t n_tiles = D.n_tiles, j = D.j;
+      uint32_t g = 0;
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t slot = next_slot<false>(sm, n);
+        if (sm.sched[slot] < 0) break;
+        const MbDesc& D = sm.dring[slot];
+        const int32_t n_tiles = D.n_tiles, j = D.j, img = sm.sched_b[slot];
         for (int32_t t = 0; t < n_tiles; ++t, ++g) {
           const uint32_t w = D.tile[t];
           const int32_t br = tile_br(w);
@@ -285,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait(&sm.v_empty[st], ((g / kVStages) & 1) ^ 1);
           ptx::mbar_arrive_expect_tx(&sm.v_full[st], kTileBytes);
           ptx::tma_load_5d(sm.v[st], &maps.v[p.br_map[br]], &sm.v_full[st], 0, j, D.gamma[br], (int32_t)tile_tp(w),
-                           wk.y, pol);
+                           img, pol);
         }
       }
     }
@@ -298,10 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t b = 0, steps = 0, sfree_par = 0, gs = 0, gpar = 0, i = 0;
       const bool tr_on = blockIdx.x == 0;
       uint32_t tr_n = 0;
-      for (uint32_t n = 0;;) {
-        const int32_t wi = ptx::take_unit<kSchedDepth, false>(sm.sched_full, sm.sched_empty, sm.sched, n);
-        if (wi < 0) break;
-        const MbDesc& D = p.desc[p.work[wi].x];
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t slot = next_slot<false>(sm, n);
+        if (sm.sched[slot] < 0) break;
+        const MbDesc& D = sm.dring[slot];
         const int32_t n_tiles = D.n_tiles;
         if (n_tiles == 0) continue;
         const uint32_t qs = i & 1;
@@ -349,10 +382,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t b = 0, p_par = 0, oc_par = 0, gs = 0, gpar = 0;
       const bool tr_on = blockIdx.x == 0;
       uint32_t tr_n = 0;
-      for (uint32_t n = 0;;) {
-        const int32_t wi = ptx::take_unit<kSchedDepth, false>(sm.sched_full, sm.sched_empty, sm.sched, n);
-        if (wi < 0) break;
-        const MbDesc& D = p.desc[p.work[wi].x];
+      for (uint32_t n = 0;; ++n) {
+        const uint32_t slot = next_slot<false>(sm, n);
+        if (sm.sched[slot] < 0) break;
+        const MbDesc& D = sm.dring[slot];
         const int32_t n_tiles = D.n_tiles;
         const int32_t first0 = D.first[0], first1 = D.first[1], last0 = D.last[0], last1 = D.last[1];
         for (int32_t t = 0; t < n_tiles; ++t) {
@@ -408,10 +441,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t kbase = 0;  // CTA-global index of the unit's first step
     const bool tr_on = blockIdx.x == 0 && row == 0;
     uint32_t tr_n = 0;
-    for (uint32_t n = 0;;) {
-      const int32_t wi = ptx::take_unit<kSchedDepth, true>(sm.sched_full, sm.sched_empty, sm.sched, n);
-      if (wi < 0) break;
-      const MbDesc& D = p.desc[p.work[wi].x];
+    for (uint32_t n = 0;; ++n) {
+      const uint32_t slot = next_slot<true>(sm, n);
+      if (sm.sched[slot] < 0) break;
+      const MbDesc& D = sm.dring[slot];
       const int32_t n_tiles = D.n_tiles;
       const uint32_t k_unit = kbase;
       kbase += (uint32_t)D.steps;
@@ -571,12 +604,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t par = 0;
     const bool tr_on = blockIdx.x == 0 && leader;
     uint32_t tr_n = 0;
-    for (uint32_t n = 0;;) {
-      const int32_t wi = ptx::take_unit<kSchedDepth, true>(sm.sched_full, sm.sched_empty, sm.sched, n);
-      if (wi < 0) break;
-      const int2 wk = p.work[wi];
-      const MbDesc& D = p.desc[wk.x];
-      const int32_t b = wk.y, j = D.j;
+    for (uint32_t n = 0;; ++n) {
+      const uint32_t slot = next_slot<true>(sm, n);
+      if (sm.sched[slot] < 0) break;
+      const MbDesc& D = sm.dring[slot];
+      const int32_t b = sm.sched_b[slot], j = D.j;
 #pragma unroll 1
       for (int s = 0; s < 2; ++s) {
         const int32_t qt = D.qt[s];
