@@ -665,6 +665,75 @@ def wl_lse(ctx, steps, warmup):
                            "launches_per_call": pb_launches // max(1, steps), "clocks": pb_clocks}}
 
 
+def wl_frows(ctx, steps, warmup):
+    """SURVEY §8(f) rows at config-2 shapes (B = 64, N = 4096, h = 6, (512, 2),
+    bf16), each timed back to back with its own clock record: the backward of
+    the core (Delta pass + tcgen05 backward), the multi-head layer
+    (multi_head_dilated: class-split QKV GEMM + core + Wo GEMM, own tcgen05
+    GEMM) and one encoder block (LN, attention mix, LN, erf-GELU MLP)."""
+    torch, dfa = ctx.torch, ctx.dfa
+    hbm, tc, _ = peaks()
+    B, Dm, hidden = 64, H * D, 4 * H * D
+    cfg = ctx.cfg(W, R)
+    fwd_flop = flop_per_unit(W, R) * H * B
+    out = {}
+    q, k, v, do = (ctx.randn((B, N_TOK, H, D), 131 + i) for i in range(4))
+    L = torch.empty((B, H, N_TOK), device=ctx.dev, dtype=torch.float32)
+    o = dfa.dfa_forward(q, k, v, cfg, lse=L, stream=ctx.stream)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ws = torch.empty(B * H * N_TOK * 4 + 256, dtype=torch.uint8, device=ctx.dev)
+
+    def bwd():
+        dfa.dfa_backward(q, k, v, o, L, do, cfg, dq, dk, dv, workspace=ws, stream=ctx.stream)
+        return dfa.last_launch_count()
+
+    t, n, clk = ctx.timed(bwd, steps, warmup)
+    ms = t / steps
+    kept = B * H * (N_TOK // R) * D * 2
+    by = 5 * kept + B * H * (N_TOK // R) * 4 * 2 + 3 * B * N_TOK * H * D * 2  # q,k,v,o,dO kept rows + lse, Delta + dq,dk,dv
+    out["backward"] = {"ms": ms, "tflops": 2.5 * fwd_flop / (ms / 1e3) / 1e12, "GBps": by / (ms / 1e3) / 1e9,
+                       "hbm_frac": by / (ms / 1e3) / 1e9 / hbm, "algorithmic_bytes": by,
+                       "launches_per_call": n // max(1, steps), "clocks": clk}
+    del q, k, v, do, o, dq, dk, dv, L, ws
+    x = ctx.randn((B, N_TOK, Dm), 141)
+    g = torch.Generator(device=ctx.dev).manual_seed(7)
+    wq, wk, wv = (torch.randn((H, Dm, D), device=ctx.dev, dtype=torch.bfloat16, generator=g) / Dm ** 0.5
+                  for _ in range(3))
+    wo = torch.randn((Dm, Dm), device=ctx.dev, dtype=torch.bfloat16, generator=g) / Dm ** 0.5
+    y = torch.empty_like(x)
+    wsp = torch.empty(4 * B * N_TOK * Dm * 2 + (40 << 20), dtype=torch.uint8, device=ctx.dev)
+
+    def mh():
+        dfa.multi_head_dilated(x, wq, wk, wv, wo, cfg, out=y, workspace=wsp, stream=ctx.stream)
+        return dfa.last_launch_count()
+
+    t, n, clk = ctx.timed(mh, steps, warmup)
+    ms = t / steps
+    proj = 2 * B * N_TOK * Dm * Dm * 4 // R  # executed: the class split does 1/r of the dense projections
+    out["multihead"] = {"ms": ms, "images_per_s": B / (ms / 1e3), "tflops": (proj + fwd_flop) / (ms / 1e3) / 1e12,
+                        "launches_per_call": n // max(1, steps), "clocks": clk}
+    s = 1.0 / Dm ** 0.5
+    prm = {"ln1_g": torch.ones(Dm), "ln1_b": torch.zeros(Dm), "wq": s * torch.randn(H, Dm, D),
+           "wk": s * torch.randn(H, Dm, D), "wv": s * torch.randn(H, Dm, D), "wo": s * torch.randn(Dm, Dm),
+           "bo": torch.zeros(Dm), "ln2_g": torch.ones(Dm), "ln2_b": torch.zeros(Dm),
+           "w1": s * torch.randn(Dm, hidden), "b1": torch.zeros(hidden), "w2": torch.randn(hidden, Dm) / hidden ** 0.5,
+           "b2": torch.zeros(Dm)}
+    prm = {kk: vv.to(ctx.dev, torch.bfloat16).contiguous() for kk, vv in prm.items()}
+    wsb = torch.empty(7 * B * N_TOK * Dm * 2 + 2 * B * N_TOK * hidden * 2 + (40 << 20), dtype=torch.uint8,
+                      device=ctx.dev)
+
+    def blk():
+        dfa.encoder_block_forward(x, prm, cfg, out=y, workspace=wsb, stream=ctx.stream)
+        return dfa.last_launch_count()
+
+    t, n, clk = ctx.timed(blk, max(3, steps // 2), warmup)
+    ms = t / max(3, steps // 2)
+    bf = proj + fwd_flop + 2 * 2 * B * N_TOK * Dm * hidden
+    out["block"] = {"ms": ms, "images_per_s": B / (ms / 1e3), "tflops": bf / (ms / 1e3) / 1e12,
+                    "launches_per_call": n // max(1, max(3, steps // 2)), "clocks": clk}
+    return out
+
+
 def wl_config5(ctx, steps, warmup):
     """8192 images x 6 layers, contiguous image shards per rank; the final NCCL
     gather of every image's output to rank 0 runs after the timed region and
@@ -755,6 +824,8 @@ def run_b200(args):
         ctx.torch.cuda.empty_cache()
         extras["config4"] = wl_config4(ctx, 20, 3)
         extras["lse"] = wl_lse(ctx, 20, 3)
+        ctx.torch.cuda.empty_cache()
+        extras["f_rows"] = wl_frows(ctx, 20, 3)
     ctx.sampler.close()
     if ctx.rank == 0:
         emit(args, ctx.world, res, extras)

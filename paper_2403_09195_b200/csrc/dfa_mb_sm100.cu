@@ -894,11 +894,8 @@ bool build_plan(const Geometry* gb, int nb, int grid, DevicePlan* out, std::vect
       desc_su.push_back(std::min(ts[0]->su, ts[1] ? ts[1]->su : ts[0]->su));
     }
   }
-  // Replicate over the batch into ONE work list, most expensive units first
-  // (the CTAs claim them dynamically: longest-processing-time-first without a
-  // cost model); within a cost class image-major, then (super-unit, head), so
-  // CTAs running side by side read the h heads' column blocks of the same
-  // token rows and share super-units' key tiles in L2.
+  // Replicate over the batch into ONE work list that the CTAs claim
+  // dynamically (no cost model needed for balance).
   const int64_t n_desc = (int64_t)descs.size();
   const int64_t n_work = n_desc * B;
   if (n_work > INT32_MAX / 2) return (*why = "too many work units"), false;
@@ -906,12 +903,20 @@ bool build_plan(const Geometry* gb, int nb, int grid, DevicePlan* out, std::vect
   seq.reserve((size_t)n_work);
   for (int64_t e = 0; e < n_desc; ++e)
     for (int64_t b = 0; b < B; ++b) seq.push_back(make_int2((int)e, (int)b));
+  // Image-major blocks (image, super-unit, head; most expensive unit first in
+  // a block), so the units that read a super-unit's key tiles run at about the
+  // same time and their re-reads hit L2; the last ~1/8 of the images is
+  // ordered most-expensive-first instead, so the claimed tail is short.
+  const int64_t b_tail = B - std::max<int64_t>(1, B / 8);
   std::stable_sort(seq.begin(), seq.end(), [&](int2 x, int2 y) {
     const MbDesc &dx = descs[x.x], &dy = descs[y.x];
-    if (dx.steps != dy.steps) return dx.steps > dy.steps;
+    const bool tx = x.y >= b_tail, ty = y.y >= b_tail;
+    if (tx != ty) return ty;  // block-ordered images first
+    if (tx && dx.steps != dy.steps) return dx.steps > dy.steps;
     if (x.y != y.y) return x.y < y.y;
     if (desc_su[x.x] != desc_su[y.x]) return desc_su[x.x] < desc_su[y.x];
-    return dx.j < dy.j;
+    if (dx.j != dy.j) return dx.j < dy.j;
+    return dx.steps > dy.steps;
   });
   grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, n_work));
   const size_t desc_bytes = sizeof(MbDesc) * (size_t)n_desc;
