@@ -125,3 +125,53 @@ def test_fused_outside_envelope_falls_back(dfa, cuda):
     assert dfa.last_launch_count() == len(branches)
     torch.cuda.synchronize()
     assert torch.isfinite(a.float()).all()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("n,branches", [
+    (2304, [(256, 1), (512, 2), (1024, 4)]),   # tail super-unit, tail segments
+    (1000, [(100, 1), (200, 2), (500, 4)]),    # short segments, N not a multiple of the tile span
+])
+def test_fused_tails_vs_oracle(dfa, port, cuda, n, branches):
+    torch = _torch()
+    B, h = 3, 4
+    q, k, v = _inputs(B, n, h, n)
+    cfg = dfa.AttentionConfig(n, branches[0][0], branches[0][1], h, 64,
+                              dfa.AttentionConfig.spread_offsets(h, branches[0][1]))
+    L = torch.empty((B, h, n), device="cuda")
+    o = torch.full((B, n, h, 64), float("nan"), device="cuda", dtype=torch.bfloat16)
+    dfa.dfa_forward_multibranch(q, k, v, cfg, branches, out=o, lse=L)
+    assert dfa.last_launch_count() == 1
+    torch.cuda.synchronize()
+    want, want_lse = port.multibranch_batched(*(x.double().cpu().numpy() for x in (q, k, v)),
+                                              _full(dfa, h, branches))
+    got = o.double().cpu().numpy()
+    err = np.abs(got - want)
+    assert np.isfinite(got).all()
+    assert err.max() <= BF16_MAX_ABS and err.sum() / np.abs(want).sum() <= BF16_MEAN_REL
+    fin = np.isfinite(want_lse)
+    assert np.array_equal(np.isfinite(L.cpu().numpy()), fin)
+
+
+def test_fused_small_batch_and_graph_replay(dfa, cuda):
+    """B = 1 (fewer units than SMs) and CUDA-graph replays of the fused launch
+    (the work counters re-arm at the end of every launch)."""
+    torch = _torch()
+    branches = SETS[0]
+    q, k, v = _inputs(1, 4096, 6, 11)
+    cfg = dfa.AttentionConfig(4096, 512, 1, 6, 64, [0] * 6)
+    s = torch.cuda.Stream()
+    o = torch.empty_like(q)
+    with torch.cuda.stream(s):
+        ref = dfa.dfa_forward_multibranch(q, k, v, cfg, branches, stream=s)  # uploads the schedule for s
+        assert dfa.last_launch_count() == 1
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        dfa.dfa_forward_multibranch(q, k, v, cfg, branches, out=o, stream=s)
+    assert dfa.last_launch_count() == 1, "fused kernel not captured"
+    for _ in range(3):
+        o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(o, ref)
