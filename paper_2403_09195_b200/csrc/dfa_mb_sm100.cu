@@ -968,8 +968,11 @@ int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, co
     for (int64_t j = 0; j < g0.h; ++j) key.br.push_back(gb[b].offsets[j]);
   }
   DevicePlan plan;
+  // The lock is held through the launch: a plan's buffer is only freed (LRU
+  // eviction, after a device-wide synchronize) by a thread holding it, so no
+  // launch can be enqueued on a buffer being freed.
+  std::lock_guard<std::mutex> lock(g_plan_mu);
   {
-    std::lock_guard<std::mutex> lock(g_plan_mu);
     bool found = false;
     for (size_t i = 0; i < g_plans.size(); ++i)
       if (g_plans[i].key == key) {
@@ -1002,7 +1005,7 @@ int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, co
       plan.work = reinterpret_cast<const int2*>(base + reinterpret_cast<uintptr_t>(plan.work));
       plan.counters = reinterpret_cast<int32_t*>(base + reinterpret_cast<uintptr_t>(plan.counters));
       if (g_plans.size() == kMaxPlans) {
-        cudaStreamSynchronize(stream);
+        cudaDeviceSynchronize();  // the evicted plan may be in flight on any stream
         cudaFree(g_plans.back().buf);
         g_plans.pop_back();
       }

@@ -175,3 +175,20 @@ def test_fused_small_batch_and_graph_replay(dfa, cuda):
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(o, ref)
+
+
+def test_fused_plan_cache_eviction(dfa, cuda):
+    """More branch sets than the schedule cache holds (16): evicted plans are
+    rebuilt on their next use and results stay identical."""
+    torch = _torch()
+    q, k, v = _inputs(1, 1024, 2, 21)
+    cfg = dfa.AttentionConfig(1024, 128, 1, 2, 64, [0, 0])
+    first = [(128, 1), (256, 2)]
+    a = dfa.dfa_forward_multibranch(q, k, v, cfg, first)
+    others = [[(64 * w, 1), (512, 2)] for w in range(1, 17)] + [[(64 * w, 1), (1024, 4)] for w in range(1, 5)]
+    for br in others:  # 20 further distinct sets
+        dfa.dfa_forward_multibranch(q, k, v, cfg, br)
+        assert dfa.last_launch_count() == 1
+    b = dfa.dfa_forward_multibranch(q, k, v, cfg, first)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
