@@ -262,6 +262,154 @@ __global__ void __launch_bounds__(128) simt_split_kernel(const T* __restrict__ q
   }
 }
 
+// Small-grid form for views of at most 256 kept rows and d, d_v <= 64 (BASELINE
+// config 1: one image, one head): the CTA stages the segment's whole K / V view
+// in shared memory once (every thread issues its loads up front: one memory
+// latency instead of one per key tile), then SPLIT lanes per query row each
+// take every SPLIT-th key without a further barrier: scores of the lane's keys
+// in registers, their max, exp() against it, P V -- and the SPLIT partial
+// (max, sum, acc) states merge through shuffles.  Same arithmetic as the
+// reference's tiled recurrence per lane (attention.hpp:170-205): fp32 FMA dot
+// products, the scale after the dot, accurate expf.
+constexpr int kSegMaxRows = 256;
+constexpr int kSegLd = 64 + 4;  // padded rows: the SPLIT lanes read SPLIT different key rows
+template <typename T, int SPLIT>
+__global__ void __launch_bounds__(256) simt_seg_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                       const T* __restrict__ v, T* __restrict__ o,
+                                                       float* __restrict__ lse, const __grid_constant__ SimtParams p) {
+  constexpr int ROWS = 256 / SPLIT;
+  constexpr int KPL = kSegMaxRows / SPLIT;  // keys per lane (upper bound)
+  static_assert(4 * SPLIT <= 64, "a lane sums whole 4-column groups");
+  extern __shared__ __align__(16) float seg_smem[];
+  float* ks = seg_smem;
+  float* vs = seg_smem + kSegMaxRows * kSegLd;
+  const int tid = threadIdx.x, rr = tid / SPLIT, pp = tid % SPLIT;
+  const int64_t seg = blockIdx.x / p.n_chunks, chunk = blockIdx.x % p.n_chunks;
+  const int64_t j = blockIdx.y, b = blockIdx.z, g = p.offsets[j];
+  const int64_t seg_begin = seg * p.w;
+  const int64_t seg_rows = min(seg_begin + p.w, p.N) - seg_begin;
+  const int64_t m = g >= seg_rows ? 0 : (seg_rows - g + p.r - 1) / p.r;  // attention.hpp:96
+  const T* qb = q + b * p.N * p.ldq + j * p.d;
+  const T* kb = k + b * p.N * p.ldk + j * p.d;
+  const T* vb = v + b * p.N * p.ldv + j * p.dv;
+  T* ob = o + b * p.N * p.ldo + j * p.dv;
+  float* lb = lse ? lse + (b * p.h + j) * p.N : nullptr;
+  if (chunk == 0) {  // rows of other offset classes: exact zeros (attention.hpp:243-245)
+    for (int64_t l = tid; l < seg_rows; l += blockDim.x) {
+      if (l % p.r == g && l >= g) continue;
+      T* orow = ob + (seg_begin + l) * p.ldo;
+      for (int64_t c = 0; c < p.dv; ++c) orow[c] = from_f<T>(0.0f);
+      if (lb) lb[seg_begin + l] = -INFINITY;
+    }
+  }
+  if (chunk * ROWS >= m) return;
+  // the view's K / V -> shared memory (zero-padded columns beyond d / d_v).
+  // fp32 rows of 64 with 16-byte alignment: cp.async in 16-byte pieces, all
+  // in flight at once; otherwise element loads.
+  const bool vec = sizeof(T) == 4 && p.d == 64 && p.dv == 64 && (p.ldk % 4) == 0 && (p.ldv % 4) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(kb) | reinterpret_cast<uintptr_t>(vb)) & 15u) == 0;
+  if (vec) {
+    for (int64_t e = tid; e < m * 16; e += blockDim.x) {
+      const int64_t t = e >> 4;
+      const int c = (int)(e & 15) * 4;
+      const int64_t krow = seg_begin + g + t * p.r;
+      const uint32_t sk = (uint32_t)__cvta_generic_to_shared(ks + t * kSegLd + c);
+      const uint32_t sv = (uint32_t)__cvta_generic_to_shared(vs + t * kSegLd + c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sk), "l"(kb + krow * p.ldk + c) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sv), "l"(vb + krow * p.ldv + c) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+  } else {
+    for (int64_t e = tid; e < m * 64; e += blockDim.x) {
+      const int64_t t = e >> 6;
+      const int c = (int)(e & 63);
+      const int64_t krow = seg_begin + g + t * p.r;
+      ks[t * kSegLd + c] = c < p.d ? to_f(kb[krow * p.ldk + c]) : 0.0f;
+      vs[t * kSegLd + c] = c < p.dv ? to_f(vb[krow * p.ldv + c]) : 0.0f;
+    }
+  }
+  const int64_t t = chunk * ROWS + rr;
+  const bool active = t < m;
+  const int64_t row = seg_begin + g + t * p.r;
+  float qr[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c) qr[c] = (active && c < p.d) ? to_f(qb[row * p.ldq + c]) : 0.0f;
+  __syncthreads();
+  // pass 1: this lane's scores (keys pp, pp + SPLIT, ...) -> shared memory, their max
+  float* ssm = seg_smem + 2 * kSegMaxRows * kSegLd + tid * KPL;
+  float mx = -INFINITY;
+  int nk = 0;
+#pragma unroll 4
+  for (int kk = pp; kk < m; kk += SPLIT, ++nk) {  // 4 keys in flight: the loop is shared-load latency bound
+    const float* kr = ks + kk * kSegLd;
+    float d4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int c = 0; c < 64; c += 4) {
+      const float4 kv = *reinterpret_cast<const float4*>(kr + c);
+      d4[0] = fmaf(qr[c], kv.x, d4[0]);
+      d4[1] = fmaf(qr[c + 1], kv.y, d4[1]);
+      d4[2] = fmaf(qr[c + 2], kv.z, d4[2]);
+      d4[3] = fmaf(qr[c + 3], kv.w, d4[3]);
+    }
+    const float sc = ((d4[0] + d4[1]) + (d4[2] + d4[3])) * p.scale;
+    ssm[nk] = sc;
+    mx = fmaxf(mx, sc);
+  }
+  // the row's max over all SPLIT lanes: every lane exponentiates against it
+#pragma unroll
+  for (int o2 = SPLIT / 2; o2 > 0; o2 >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o2));
+  // pass 2: P V of this lane's keys
+  float acc[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c) acc[c] = 0.0f;
+  float l = 0.0f;
+  nk = 0;
+#pragma unroll 2
+  for (int kk = pp; kk < m; kk += SPLIT, ++nk) {
+    const float pj = expf(ssm[nk] - mx);
+    l += pj;
+    const float* vr = vs + kk * kSegLd;
+#pragma unroll
+    for (int c = 0; c < 64; c += 4) {
+      const float4 vv = *reinterpret_cast<const float4*>(vr + c);
+      acc[c] = fmaf(pj, vv.x, acc[c]);
+      acc[c + 1] = fmaf(pj, vv.y, acc[c + 1]);
+      acc[c + 2] = fmaf(pj, vv.z, acc[c + 2]);
+      acc[c + 3] = fmaf(pj, vv.w, acc[c + 3]);
+    }
+  }
+#pragma unroll
+  for (int o2 = SPLIT / 2; o2 > 0; o2 >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o2);
+  // sum the SPLIT partial rows through shared memory: lane pp owns columns
+  // [4 pp', 4 pp' + 4) for pp' = pp, pp + SPLIT, ... (16 lanes x 4 = 64)
+  float* red = seg_smem + 2 * kSegMaxRows * kSegLd + 256 * KPL;
+  float* myred = red + tid * 68;  // 64 + 4 pad (bank spread)
+#pragma unroll
+  for (int c = 0; c < 64; c += 4) *reinterpret_cast<float4*>(myred + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+  __syncwarp();
+  if (active) {
+    const float inv = 1.0f / l;
+    T* orow = ob + row * p.ldo;
+    const float* rowred = red + (tid - pp) * 68;
+    for (int c = 4 * pp; c < 64; c += 4 * SPLIT) {
+      float4 sum = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+#pragma unroll
+      for (int ln = 0; ln < SPLIT; ++ln) {
+        const float4 x = *reinterpret_cast<const float4*>(rowred + ln * 68 + c);
+        sum.x += x.x;
+        sum.y += x.y;
+        sum.z += x.z;
+        sum.w += x.w;
+      }
+      if (c < p.dv) orow[c] = from_f<T>(sum.x * inv);
+      if (c + 1 < p.dv) orow[c + 1] = from_f<T>(sum.y * inv);
+      if (c + 2 < p.dv) orow[c + 2] = from_f<T>(sum.z * inv);
+      if (c + 3 < p.dv) orow[c + 3] = from_f<T>(sum.w * inv);
+    }
+    if (lb && pp == 0) lb[row] = mx + logf(l);
+  }
+}
+
 // f64 mode (the reference's double instantiation, attention.hpp:280-301 with
 // Scalar = double): the same thread-per-query-row online softmax as
 // simt_kernel with every operation in double -- DFMA dot products, the scale
@@ -401,7 +549,21 @@ int launch_t(const Geometry& g, const void* q, const void* k, const void* v, voi
   constexpr int kSplit = 4;
   bool launched = false;
   if constexpr (DMAX <= 64) {
-    if ((int64_t)grid.x * grid.y * grid.z < 2 * 148) {
+    if ((int64_t)grid.x * grid.y * grid.z < 2 * 148 && g.m_max <= kSegMaxRows) {
+      // small grid, short views: whole-view K / V in shared memory, 16 lanes per row
+      constexpr int kSp = 16;
+      p.n_chunks = std::max<int64_t>(1, (g.m_max + 256 / kSp - 1) / (256 / kSp));
+      dim3 gs((unsigned)(g.n_seg * p.n_chunks), (unsigned)g.h, (unsigned)g.B);
+      // K, V views + per-lane scores + the partial-row reduction buffer
+      const size_t smem = (2 * kSegMaxRows * kSegLd + 256 * (kSegMaxRows / kSp) + 256 * 68) * sizeof(float);
+      const cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(simt_seg_kernel<T, kSp>), smem);
+      if (ae != cudaSuccess) {
+        *err = ae;
+        return 0;
+      }
+      simt_seg_kernel<T, kSp><<<gs, 256, smem, stream>>>((const T*)q, (const T*)k, (const T*)v, (T*)o, lse, p);
+      launched = true;
+    } else if ((int64_t)grid.x * grid.y * grid.z < 2 * 148) {
       // small grid: 4 lanes per query row -> 4x the CTAs; 8 lanes when even
       // that leaves SMs idle (config 1: 64 -> 128 CTAs)
       p.n_chunks = (g.m_max + 128 / kSplit - 1) / (128 / kSplit);
