@@ -96,19 +96,21 @@ FastDivMb make_fastdiv_mb(uint32_t d) {
 
 // One work unit (replicated over the batch).  tile[i] = t' (bits 0-23, in
 // the branch's r-stream) | branch (bits 24-26) | slot mask (bits 28-29).
-struct alignas(16) MbDesc {
+struct alignas(16) MbDesc {  // sizeof % 16 == 0: bulk-copied into shared memory
   int32_t j;
   int32_t n_tiles;
   int32_t steps;                      // sum of the tiles' slot counts
   int32_t qt[2];                      // R-stream t' of the slot's rows; -1: slot absent
   int32_t first[2], last[2];          // first / last key tile of slot s (-1: slot has no steps)
-  int8_t cls[2][kMbMaxGroups];        // class of group g of slot s
+  int16_t cls[2][kMbMaxGroups];       // class of group g of slot s (< R <= 1024)
   uint8_t sel[2][kMaxBranches];       // bit g: group g of slot s selected by branch b
   uint8_t anysel[2];                  // bit g: group g selected by some branch
   uint8_t pad[2];
   int32_t gamma[kMaxBranches];        // offset of head j in branch b
   uint32_t tile[kMbMaxTiles];
 };
+
+static_assert(sizeof(MbDesc) % 16 == 0, "bulk copy size");
 
 struct MbParams {
   int32_t N, h, R, TR;     // TR = N / R
@@ -856,7 +858,7 @@ bool build_plan(const Geometry* gb, int nb, int grid, DevicePlan* out, std::vect
         d.qt[s] = -1;
         if (!ts[s]) continue;
         d.qt[s] = (int32_t)(ts[s]->su * gr);
-        for (int64_t gi = 0; gi < G; ++gi) d.cls[s][gi] = (int8_t)(ts[s]->c + gi * (R / G));
+        for (int64_t gi = 0; gi < G; ++gi) d.cls[s][gi] = (int16_t)(ts[s]->c + gi * (R / G));
         for (int k = 0; k < nb; ++k) {
           d.sel[s][k] = ts[s]->sel[k];
           d.anysel[s] |= ts[s]->sel[k];

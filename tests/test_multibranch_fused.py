@@ -131,6 +131,7 @@ def test_fused_outside_envelope_falls_back(dfa, cuda):
 @pytest.mark.parametrize("n,branches", [
     (2304, [(256, 1), (512, 2), (1024, 4)]),   # tail super-unit, tail segments
     (1000, [(100, 1), (200, 2), (500, 4)]),    # short segments, N not a multiple of the tile span
+    (4096, [(512, 1), (4096, 256)]),            # R = 256 offset classes
 ])
 def test_fused_tails_vs_oracle(dfa, port, cuda, n, branches):
     torch = _torch()
