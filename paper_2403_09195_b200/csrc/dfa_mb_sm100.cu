@@ -108,6 +108,10 @@ struct alignas(16) MbDesc {  // sizeof % 16 == 0: bulk-copied into shared memory
   uint8_t pad[2];
   int32_t gamma[kMaxBranches];        // offset of head j in branch b
   uint32_t tile[kMbMaxTiles];
+  // the softmax's view: slot s's steps in order, t' (bits 0-19) | branch
+  // (20-22) | step index within the unit (23-30)
+  int32_t sn[2];
+  uint32_t sstep[2][kMbMaxTiles];
 };
 
 static_assert(sizeof(MbDesc) % 16 == 0, "bulk copy size");
@@ -447,7 +451,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t slot = next_slot<true>(sm, n);
       if (sm.sched[slot] < 0) break;
       const MbDesc& D = sm.dring[slot];
-      const int32_t n_tiles = D.n_tiles;
       const uint32_t k_unit = kbase;
       kbase += (uint32_t)D.steps;
       if (D.first[s] < 0) continue;
@@ -458,14 +461,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t sel_row = valid ? 0xFFu : 0u;
       float mref = -INFINITY, l = 0.0f;
       int32_t cur_br = -1, seg_lo = 0, seg_hi = 0;
-      uint32_t pos = 0;  // steps of this unit before the current tile
-      for (int32_t t = 0; t < n_tiles; ++t) {
-        const uint32_t w = D.tile[t];
-        const uint32_t mask = tile_mask(w);
-        const uint32_t here = pos + ((s == 1 && (mask & 1u)) ? 1u : 0u);
-        pos += (mask & 1u) + (mask >> 1);
-        if (!((mask >> s) & 1u)) continue;
-        const int32_t br = tile_br(w);
+      const int32_t ns = D.sn[s];
+      const uint32_t k_unit3 = k_unit % kSBufs;
+      for (int32_t si = 0; si < ns; ++si) {
+        const uint32_t w = D.sstep[s][si];
+        const uint32_t here = w >> 23;  // step index within the unit
+        const int32_t br = (int32_t)((w >> 20) & 7u);
         if (br != cur_br) {
           cur_br = br;
           const bool sel = (sel_row & D.sel[s][br]) >> grp & 1u;
@@ -477,14 +478,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             seg_lo = seg_hi = 0;  // every key masked: this branch does not select the row
           }
         }
-        const uint32_t b = (k_unit + here) % kSBufs;
+        const uint32_t b = (k_unit3 + here) % kSBufs;
         MB_TRACE(2 + s, 9);
         ptx::mbar_wait(&sm.s_full[s][b], (use_par >> b) & 1u);
         MB_TRACE(2 + s, 10);
         use_par ^= 1u << b;
         ptx::tc_fence_after();
         const uint32_t tS = tbase + lane_base + col_s(b);
-        const int32_t k0 = (int32_t)tile_tp(w);
+        const int32_t k0 = (int32_t)(w & 0xFFFFFu);
         const int32_t lo = min(max(seg_lo - k0, 0), kBN);
         const int32_t hi = min(max(seg_hi - k0, 0), kBN);
         bool waited = false;
@@ -746,7 +747,7 @@ bool build_plan(const Geometry* gb, int nb, int grid, DevicePlan* out, std::vect
     if (R > 1024) return (*why = "lcm of the intervals > 1024"), false;
   }
   if (N % R != 0) return (*why = "lcm of the intervals does not divide N"), false;
-  if (N >= (1 << 24)) return (*why = "N >= 2^24 (key-tile t' is packed in 24 bits)"), false;
+  if (N >= (1 << 20)) return (*why = "N >= 2^20 (key-tile t' is packed in 20 bits)"), false;
   // distinct intervals -> tensor-map slots
   out->n_maps = 0;
   for (int b = 0; b < nb; ++b) {
@@ -872,6 +873,9 @@ bool build_plan(const Geometry* gb, int nb, int grid, DevicePlan* out, std::vect
             if (d.first[s] < 0) d.first[s] = d.n_tiles;
             d.last[s] = d.n_tiles;
           }
+        uint32_t at = (uint32_t)d.steps;  // step index of this tile's first step in the unit
+        for (int s = 0; s < 2; ++s)
+          if ((mask >> s) & 1u) d.sstep[s][d.sn[s]++] = (uint32_t)tp | ((uint32_t)k << 20) | (at++ << 23);
         d.tile[d.n_tiles++] = (uint32_t)tp | ((uint32_t)k << 24) | (mask << 28);
         d.steps += (int32_t)((mask & 1u) + (mask >> 1));
         return true;
