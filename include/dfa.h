@@ -188,6 +188,15 @@ void dfa_set_multibranch_mode(int32_t mode);
  * multi-branch launches record CTA 0's timeline into it (dfa_forward_traced's
  * format; scripts/trace_timeline.py decodes it). */
 void dfa_set_multibranch_trace(uint64_t* trace);
+/* Test hook (host only, no CUDA call): the work-unit schedule the fused
+ * multi-branch kernel uses for a branch set -- *n_desc descriptors of
+ * *desc_bytes bytes each (layout: csrc/dfa_mb_sm100.cu MbDesc) copied into
+ * `descs` (up to `capacity` bytes), the lcm R of the intervals and log2 of the
+ * rows per offset-class group.  DFA_ERR_UNSUPPORTED when the set is outside
+ * the fused kernel's envelope. */
+dfa_status_t dfa_multibranch_plan(const dfa_config_t* base, int32_t n_branches, const dfa_branch_t* branches,
+                                  int64_t batch, int32_t grid, void* descs, size_t capacity, int32_t* n_desc,
+                                  int32_t* lcm_interval, int32_t* rows_per_group_log2, int32_t* desc_bytes);
 
 /* Backward of the dilated core (the reference computes
  * it on its autodiff tape for the dilated branch of detail::attention_mix,

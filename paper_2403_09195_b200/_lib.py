@@ -53,6 +53,7 @@ EXPORTED = (
     "dfa_set_path_override",
     "dfa_set_multibranch_mode",
     "dfa_set_multibranch_trace",
+    "dfa_multibranch_plan",
     "dfa_forward_traced",
     "dfa_forward_debug",
     "dfa_multibranch_workspace_bytes",
@@ -139,6 +140,9 @@ def _load() -> ctypes.CDLL:
         "dfa_set_path_override": (None, [c_i32]),
         "dfa_set_multibranch_mode": (None, [c_i32]),
         "dfa_set_multibranch_trace": (None, [c_vp]),
+        "dfa_multibranch_plan": (c_i32, [p_cfg, c_i32, ctypes.POINTER(DfaBranch), c_i64, c_i32, c_vp, ctypes.c_size_t,
+                                         ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
+                                         ctypes.POINTER(c_i32)]),
         "dfa_forward_traced": (c_i32, [p_cfg, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
         "dfa_forward_debug": (c_i32, [p_cfg, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
         "dfa_multibranch_workspace_bytes": (c_i32, [p_cfg, c_i32, c_i32, c_i64, ctypes.POINTER(ctypes.c_size_t)]),

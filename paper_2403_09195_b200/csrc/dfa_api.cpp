@@ -530,6 +530,30 @@ dfa_status_t dfa_forward_multibranch(const dfa_config_t* base, int32_t nb, const
   return DFA_OK;
 }
 
+dfa_status_t dfa_multibranch_plan(const dfa_config_t* base, int32_t nb, const dfa_branch_t* branches, int64_t batch,
+                                  int32_t grid, void* descs, size_t capacity, int32_t* n_desc, int32_t* lcm_interval,
+                                  int32_t* rows_per_group_log2, int32_t* desc_bytes) {
+  if (nb < 2 || nb > dfa_impl::kMaxBranches)
+    return fail(DFA_ERR_CONFIG, "multibranch plan: need 2..%d branches, got %d", dfa_impl::kMaxBranches, (int)nb);
+  if (!branches || !n_desc || !lcm_interval || !rows_per_group_log2 || !desc_bytes)
+    return fail(DFA_ERR_DIMENSION, "multibranch plan: null argument");
+  dfa_config_t cfgs[dfa_impl::kMaxBranches];
+  dfa_impl::Geometry gb[dfa_impl::kMaxBranches];
+  for (int b = 0; b < nb; ++b) {
+    cfgs[b] = *base;
+    cfgs[b].segment_len = branches[b].segment_len;
+    cfgs[b].interval = branches[b].interval;
+    cfgs[b].head_offsets = branches[b].head_offsets;
+    dfa_status_t st = resolve(&cfgs[b], batch, &gb[b]);
+    if (st != DFA_OK) return st;
+  }
+  const char* why = "";
+  if (!dfa_impl::mb_plan_host(gb, nb, grid > 0 ? grid : 148, descs, capacity, n_desc, lcm_interval,
+                              rows_per_group_log2, desc_bytes, &why))
+    return fail(DFA_ERR_UNSUPPORTED, "multibranch plan: %s", why);
+  return DFA_OK;
+}
+
 dfa_status_t dfa_backward_workspace_bytes(const dfa_config_t* cfg, int64_t batch, size_t* bytes) {
   dfa_impl::Geometry g;
   dfa_status_t st = resolve(cfg, batch, &g);

@@ -136,6 +136,8 @@ constexpr int kMbMaxMaps = 4;     // distinct intervals in a set
 constexpr int kMbMaxTiles = 64;   // key tiles per work unit
 constexpr int kMbMaxGroups = 8;   // offset-class groups per query tile
 void set_mb_trace(uint64_t* trace);  // profiling: trace CTA 0 of the next fused launches (nullptr = off)
+int mb_plan_host(const Geometry* gb, int nb, int grid, void* out, size_t cap, int32_t* n_desc, int32_t* R,
+                 int32_t* gr_shift, int32_t* desc_bytes, const char** why);
 int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, const void* v, void* o, float* lse,
                     cudaStream_t stream, cudaError_t* err, const char** why, int64_t* steps_out);
 

@@ -950,6 +950,24 @@ constexpr size_t kMaxPlans = 16;
 
 void set_mb_trace(uint64_t* trace) { g_mb_trace.store(trace); }
 
+// Host-only: the schedule build_plan makes for a branch set (test / debug
+// hook; no CUDA call).  Copies up to `cap` bytes of descriptors.
+int mb_plan_host(const Geometry* gb, int nb, int grid, void* out, size_t cap, int32_t* n_desc, int32_t* R,
+                 int32_t* gr_shift, int32_t* desc_bytes, const char** why) {
+  DevicePlan plan;
+  std::vector<uint8_t> blob;
+  if (!build_plan(gb, nb, grid, &plan, &blob, why)) return 0;
+  const size_t work_at = reinterpret_cast<uintptr_t>(plan.work);  // descriptors end before the work list
+  const size_t n = plan.n_work / std::max<int64_t>(1, gb[0].B);
+  *n_desc = (int32_t)n;
+  *R = plan.R;
+  *gr_shift = plan.gr_shift;
+  *desc_bytes = (int32_t)sizeof(MbDesc);
+  const size_t bytes = std::min(cap, std::min(work_at, n * sizeof(MbDesc)));
+  if (out) memcpy(out, blob.data(), bytes);
+  return 1;
+}
+
 // Fused multi-branch forward: returns 1 (launch issued), 0 when the set is
 // outside the kernel's envelope (why set, nothing launched) or -1 on a CUDA
 // error (err set).
