@@ -367,6 +367,38 @@ __global__ void __launch_bounds__(256) pack_wo_class_kernel(const T* __restrict_
   }
 }
 
+// Both class packings in one launch, 16-byte vectors (d % V == 0, D % V ==
+// 0, aligned pointers): the per-call weight packing of the class-split layer
+// was two scalar kernels of ~5 us each (integer divides per element).
+template <typename T>
+__global__ void __launch_bounds__(256) pack_class_vec_kernel(const T* __restrict__ wq, const T* __restrict__ wk,
+                                                             const T* __restrict__ wv, const T* __restrict__ wo,
+                                                             T* __restrict__ qkv_out, T* __restrict__ wo_out,
+                                                             uint32_t h, uint32_t D, uint32_t d,
+                                                             const __grid_constant__ ClassPack cp) {
+  constexpr uint32_t V = 16 / sizeof(T);
+  const uint32_t dv = d / V, Dv = D / V;
+  const uint32_t n1 = 3u * D * h * dv, n2 = h * d * Dv;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n1 + n2; i += gridDim.x * blockDim.x) {
+    if (i < n1) {
+      // (c, which, j, e / V) -> the packed [D, class-major q|k|v] column block
+      const uint32_t i1 = i / dv, e = (i - i1 * dv) * V;
+      const uint32_t i2 = i1 / h, j = i1 - i2 * h;
+      const uint32_t c = i2 / 3u, which = i2 - c * 3u;
+      const T* src = which == 0 ? wq : (which == 1 ? wk : wv);
+      const uint32_t g = (uint32_t)cp.cls[j], jr = (uint32_t)(cp.pos[j] - cp.start[g]);
+      const uint32_t col = 3u * d * (uint32_t)cp.start[g] + (which * (uint32_t)cp.cnt[g] + jr) * d + e;
+      *reinterpret_cast<uint4*>(qkv_out + (size_t)c * 3u * D + col) =
+          *reinterpret_cast<const uint4*>(src + ((size_t)j * D + c) * d + e);
+    } else {
+      const uint32_t k = i - n1, r = k / Dv, cv = (k - r * Dv) * V;
+      const uint32_t j = r / d, e = r - j * d;
+      *reinterpret_cast<uint4*>(wo_out + ((size_t)cp.pos[j] * d + e) * D + cv) =
+          *reinterpret_cast<const uint4*>(wo + (size_t)r * D + cv);
+    }
+  }
+}
+
 }  // namespace
 
 int launch_layer_norm(int dtype, const void* x, const void* g, const void* b, void* y, int64_t rows, int cols,
@@ -425,6 +457,23 @@ int launch_pack_class(int dtype, const void* wq, const void* wk, const void* wv,
     cp.cnt[g] = at - cp.start[g];
   }
   const unsigned grid = (unsigned)std::min<int64_t>((3 * D * D + 255) / 256, 148 * 8);
+  const int64_t V = dtype == 0 ? 4 : 8;
+  const bool vec = d % V == 0 && D % V == 0 &&
+                   ((reinterpret_cast<uintptr_t>(wq) | reinterpret_cast<uintptr_t>(wk) | reinterpret_cast<uintptr_t>(wv) |
+                     reinterpret_cast<uintptr_t>(wo) | reinterpret_cast<uintptr_t>(qkv_out) |
+                     reinterpret_cast<uintptr_t>(wo_out)) & 15u) == 0;
+  if (vec) {
+    const unsigned gv = (unsigned)std::min<int64_t>((4 * D * h * d / V + 255) / 256, 148 * 8);
+    if (dtype == 0)
+      pack_class_vec_kernel<float><<<gv, 256, 0, stream>>>((const float*)wq, (const float*)wk, (const float*)wv,
+                                                          (const float*)wo, (float*)qkv_out, (float*)wo_out,
+                                                          (uint32_t)h, (uint32_t)D, (uint32_t)d, cp);
+    else
+      pack_class_vec_kernel<__nv_bfloat16><<<gv, 256, 0, stream>>>(
+          (const __nv_bfloat16*)wq, (const __nv_bfloat16*)wk, (const __nv_bfloat16*)wv, (const __nv_bfloat16*)wo,
+          (__nv_bfloat16*)qkv_out, (__nv_bfloat16*)wo_out, (uint32_t)h, (uint32_t)D, (uint32_t)d, cp);
+    return 1;
+  }
   if (dtype == 0) {
     pack_qkv_class_kernel<float><<<grid, 256, 0, stream>>>((const float*)wq, (const float*)wk, (const float*)wv,
                                                            (float*)qkv_out, (uint32_t)h, (uint32_t)D, (uint32_t)d, cp);
