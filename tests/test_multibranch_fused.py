@@ -193,3 +193,24 @@ def test_fused_plan_cache_eviction(dfa, cuda):
     b = dfa.dfa_forward_multibranch(q, k, v, cfg, first)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("branches,fused", [
+    ([(4096, 1), (2048, 1)], True),              # 48 key tiles per unit: still one launch
+    ([(4096, 1), (4096, 1), (4096, 2)], False),  # 80 > 64 key tiles per unit: per-branch launches
+])
+def test_long_segment_sets(dfa, cuda, branches, fused):
+    torch = _torch()
+    from paper_2403_09195_b200 import _lib, multibranch_mode
+
+    q, k, v = _inputs(4, 4096, 6, 17)
+    cfg = dfa.AttentionConfig(4096, 4096, 1, 6, 64, [0] * 6)
+    a = dfa.dfa_forward_multibranch(q, k, v, cfg, branches)
+    assert dfa.last_launch_count() == (1 if fused else len(branches))
+    with multibranch_mode(_lib.DFA_MB_PER_BRANCH):
+        b = dfa.dfa_forward_multibranch(q, k, v, cfg, branches)
+    torch.cuda.synchronize()
+    err = (a.float() - b.float()).abs()
+    assert err.max().item() <= BF16_MAX_ABS
+    assert (err.sum() / b.float().abs().sum()).item() <= BF16_MEAN_REL
