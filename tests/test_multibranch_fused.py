@@ -214,3 +214,24 @@ def test_long_segment_sets(dfa, cuda, branches, fused):
     err = (a.float() - b.float()).abs()
     assert err.max().item() <= BF16_MAX_ABS
     assert (err.sum() / b.float().abs().sum()).item() <= BF16_MEAN_REL
+
+
+def test_first_call_under_capture_takes_per_branch_path(dfa, cuda):
+    """A branch set seen for the first time inside a CUDA-graph capture cannot
+    upload its schedule: that call takes the per-branch launches (still
+    captured, still correct)."""
+    torch = _torch()
+    branches = [(512, 1), (1024, 2), (2048, 4)]
+    q, k, v = _inputs(2, 4096, 6, 23)
+    cfg = dfa.AttentionConfig(4096, 512, 1, 6, 64, [0] * 6)
+    ref = dfa.dfa_forward_multibranch(q, k, v, cfg, branches)  # default stream: its own plan
+    s = torch.cuda.Stream()
+    o = torch.empty_like(q)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        dfa.dfa_forward_multibranch(q, k, v, cfg, branches, out=o, stream=s)
+    assert dfa.last_launch_count() == len(branches)
+    g.replay()
+    torch.cuda.synchronize()
+    err = (o.float() - ref.float()).abs()
+    assert err.max().item() <= BF16_MAX_ABS
