@@ -89,3 +89,44 @@ def test_plan_rejects_out_of_envelope_sets():
 
     with pytest.raises(dfa.UnsupportedError):
         pm.plan(2048, 2, 1, branches(2, [(64, 1), (128, 2), (256, 4), (512, 8), (1024, 16)]))
+
+
+def _random_sets(seed, count):
+    """Random branch sets inside the fused kernel's envelope: intervals with
+    r | w, lcm(r) | N, arbitrary per-head offsets."""
+    rnd = random.Random(seed)
+    out = []
+    while len(out) < count:
+        n = rnd.choice([512, 768, 1024, 2048, 3072, 4096])
+        h = rnd.choice([1, 2, 3, 6])
+        nb = rnd.randint(2, 4)
+        spec = []
+        for _ in range(nb):
+            r = rnd.choice([1, 2, 3, 4, 8])
+            w = r * rnd.choice([8, 16, 32, 64, 100, 128, 256, 512])
+            if w > n:
+                continue
+            spec.append((w, r, [rnd.randrange(r) for _ in range(h)]))
+        if len(spec) < 2:
+            continue
+        lcm = 1
+        for _, r, _ in spec:
+            lcm = lcm * r // __import__("math").gcd(lcm, r)
+        if n % lcm:
+            continue
+        out.append((n, h, spec))
+    return out
+
+
+@pytest.mark.parametrize("case", _random_sets(7, 40))
+def test_random_sets_schedule(case):
+    """Property check of the schedule over random branch sets (sets outside the
+    envelope, e.g. > 64 key tiles per unit, must be rejected cleanly)."""
+    import paper_2403_09195_b200 as dfa
+
+    n, h, spec = case
+    try:
+        descs, R, gr = pm.plan(n, h, 1, spec)
+    except dfa.UnsupportedError:
+        return
+    pm.check_plan(descs, R, gr, n, h, spec)

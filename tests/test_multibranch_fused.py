@@ -235,3 +235,51 @@ def test_first_call_under_capture_takes_per_branch_path(dfa, cuda):
     torch.cuda.synchronize()
     err = (o.float() - ref.float()).abs()
     assert err.max().item() <= BF16_MAX_ABS
+
+
+def _random_sets(seed, count):
+    """Random branch sets (r | w, lcm(r) | N, random per-head offsets) -- the
+    same generator as tests/test_mb_plan.py's schedule property test, smaller
+    sizes so the f64 oracle stays fast."""
+    import math
+    import random
+
+    rnd = random.Random(seed)
+    out = []
+    while len(out) < count:
+        n = rnd.choice([512, 768, 1024, 2048])
+        h = rnd.choice([1, 2, 3])
+        spec = []
+        for _ in range(rnd.randint(2, 4)):
+            r = rnd.choice([1, 2, 3, 4, 8])
+            w = r * rnd.choice([8, 16, 32, 64, 100, 128, 256])
+            if w <= n:
+                spec.append((w, r, [rnd.randrange(r) for _ in range(h)]))
+        if len(spec) >= 2 and n % math.lcm(*(r for _, r, _ in spec)) == 0:
+            out.append((n, h, spec))
+    return out
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("case", _random_sets(11, 10))
+def test_random_sets_vs_oracle(dfa, port, cuda, case):
+    torch = _torch()
+    n, h, branches = case
+    B = 2
+    q, k, v = _inputs(B, n, h, n + h)
+    w0, r0, off0 = branches[0]
+    cfg = dfa.AttentionConfig(n, w0, r0, h, 64, off0)
+    L = torch.full((B, h, n), float("nan"), device="cuda")
+    o = torch.full((B, n, h, 64), float("nan"), device="cuda", dtype=torch.bfloat16)
+    dfa.dfa_forward_multibranch(q, k, v, cfg, branches, out=o, lse=L)
+    assert dfa.last_launch_count() == 1, "all these sets are inside the fused kernel's envelope"
+    torch.cuda.synchronize()
+    want, want_lse = port.multibranch_batched(*(x.double().cpu().numpy() for x in (q, k, v)), branches)
+    got = o.double().cpu().numpy()
+    assert np.isfinite(got).all()
+    err = np.abs(got - want)
+    assert err.max() <= BF16_MAX_ABS and err.sum() / max(np.abs(want).sum(), 1e-30) <= BF16_MEAN_REL, (case, err.max())
+    fin = np.isfinite(want_lse)
+    Lg = L.cpu().numpy()
+    assert np.array_equal(np.isfinite(Lg), fin)
+    assert np.abs(Lg[fin] - want_lse[fin]).max() <= 2e-2
