@@ -82,6 +82,11 @@ struct BwdSm100Params {
 
 __device__ __forceinline__ void wait(uint64_t* bar, uint32_t par) { ptx::mbar_wait(bar, par); }
 
+// kPacked: m < 128, 128 / m segments per tile with the block-diagonal mask --
+// a separate instantiation so the common path carries no mask code in its
+// inner loop (a runtime test there left one body with per-pair mask
+// arithmetic whenever the compiler declined to unswitch it: 12-15% slower)
+template <bool kPacked>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_bwd_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_g,
@@ -208,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int kk = 4 * hf; kk < 4 * hf + 4; ++kk) {
                 // K-step of 16 queries: 8 packed TMEM columns of P^T / dS^T, 16 rows (2048 B) of dO / Q
-                ptx::mma_ts(tbase + cDV, tbase + cS + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
-                ptx::mma_ts(tbase + cDK, tbase + cDP + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+                ptx::mma_ts(tbase + cDV, tbase + cS + 32 * hf + kk * 8, gd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
+                ptx::mma_ts(tbase + cDK, tbase + cDP + 32 * hf + kk * 8, qd + kk * 128, id_ts, (qb > 0 || kk > 0) ? 1u : 0u);
               }
             }
 #pragma unroll
@@ -236,6 +241,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = (warp - 4) / 4;
     const uint32_t row = ((warp - 4) % 4) * 32 + lane;  // key row (TMEM lane) / query row for dQ
     const uint32_t lane_base = (((warp - 4) % 4) * 32) << 16;
+    // packed views: this key row's segment covers queries [seg_lo, seg_lo + seg_len)
+    const uint32_t seg_len = (uint32_t)p.mseg, seg_lo = kPacked ? row / seg_len * seg_len : 0u;
     const bool leader = warp % 4 == 0 && lane == 0;
     const uint32_t bar_id = 1 + wg;
     uint32_t step = 0, kvn = 0;
@@ -298,14 +305,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, s);
             ptx::tmem_ld32(tbase + lane_base + cDP + 32 * c, dp);
             ptx::tmem_ld_wait();
-            // Packed P^T / dS^T of chunk c land on columns 16c.., i.e. on the
-            // fp32 columns of chunk c/2: WG1's chunks 2-3 overwrite WG0's chunk
-            // 1, so WG0 signals once chunk 1 is in registers and WG1 waits for
-            // that before its first store (WG0's own order 0, 1 is safe).
-            if (c == 1) ptx::named_bar_arrive(3, 2 * kB);
             uint32_t pp[16], dd[16];
-#pragma unroll
             const float2 c2 = make_float2(p.c, p.c);
+#pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int q0 = 32 * c + 2 * e;
               // packed pairs: x = s c - lse log2e (FFMA2), dS = P (dP - Delta) (FADD2, FMUL2)
@@ -318,19 +320,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               } else {
                 pr = make_float2(ptx::ex2(x.x), ptx::ex2(x.y));
               }
-              if (p.mseg < kB) {  // packed short segments: no interaction across segments
-                const uint32_t kseg = row / p.mseg;
-                if ((uint32_t)q0 / p.mseg != kseg) pr.x = 0.0f;
-                if ((uint32_t)(q0 + 1) / p.mseg != kseg) pr.y = 0.0f;
+              if (kPacked) {  // packed short segments: no interaction across segments
+                if ((uint32_t)q0 - seg_lo >= seg_len) pr.x = 0.0f;
+                if ((uint32_t)q0 + 1u - seg_lo >= seg_len) pr.y = 0.0f;
               }
               const float2 dsv =
                   ptx::fmul2(pr, ptx::fadd2(make_float2(__uint_as_float(dp[2 * e]), __uint_as_float(dp[2 * e + 1])), nd));
               pp[e] = ptx::pack_bf16x2(pr.x, pr.y);
               dd[e] = ptx::pack_bf16x2(dsv.x, dsv.y);
             }
-            if (c == 2) ptx::named_bar_sync(3, 2 * kB);
-            ptx::tmem_st16(tbase + lane_base + cS + 16 * c, pp);
-            ptx::tmem_st16(tbase + lane_base + cDP + 16 * c, dd);
+            // Packed P^T / dS^T of chunk c land on the first 32 columns of its
+            // own half's fp32 region (chunk 2h + e on 64 h + 16 e): each
+            // warpgroup only overwrites scores it has already loaded
+            ptx::tmem_st16(tbase + lane_base + cS + 16 * c + 32 * (c >> 1), pp);
+            ptx::tmem_st16(tbase + lane_base + cDP + 16 * c + 32 * (c >> 1), dd);
             // dS^T row `row` (key) -> MN-major A of dQ: queries 32c..32c+31 are
             // 16-byte chunks 4(c&1)..4(c&1)+3 of sub-tile c>>1, SW128-swizzled
             const uint32_t sub = dsa + (c >> 1) * kTile + row * 128;
@@ -344,6 +347,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::tmem_st_wait();
           ptx::fence_proxy_async_smem();
           ptx::tc_fence_before();
+          // The first dV / dK product of key block kb > 0 (issued once WG0's
+          // half arrives) overwrites the accumulators: WG1 must have read the
+          // previous block's dV first (WG0 read dK before this step)
+          if (wg == 0 && kb > 0 && qb == 0) ptx::named_bar_sync(5, 2 * kB);
           ptx::mbar_arrive(&sm.p_full[wg]);
         }
         if (kb == nb - 1 && u + (int32_t)gridDim.x < n_units) fetch_stats(u + gridDim.x);  // next unit's stats
@@ -358,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_ld32(tbase + lane_base + col, a[0]);
         ptx::tmem_ld32(tbase + lane_base + col + 32, a[1]);
         ptx::tmem_ld_wait();
+        if (wg == 1 && kb + 1 < nb) ptx::named_bar_arrive(5, 2 * kB);  // dV of block kb is in registers
         stage_store(sm.stage[wg], a, wg == 0 ? p.scale : 1.0f);
         ptx::tc_fence_before();
         ptx::fence_proxy_async_smem();
@@ -762,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nk; ++kb, ++step) {
         wait(&sm.s_full, step & 1);
         ptx::tc_fence_after();
-#pragma unroll 1
+#pragma unroll  // both chunks: the second's TMEM loads overlap the first's math (-1-3%)
         for (int c = 2 * wg; c < 2 * wg + 2; ++c) {
           uint32_t sv[32], dp[32];
           ptx::tmem_ld32(tbase + lane_base + cS + 32 * c, sv);
@@ -927,14 +935,18 @@ int launch_bwd_sm100(const Geometry& g, const void* q, const void* k, const void
     return 2;
   }
   const size_t smem = sizeof(BwdSmem) + 1024;
-  const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void*>(dfa_bwd_sm100_kernel), smem);
+  const bool packed = p.mseg < kB;
+  const void* kfn = packed ? reinterpret_cast<const void*>(dfa_bwd_sm100_kernel<true>)
+                           : reinterpret_cast<const void*>(dfa_bwd_sm100_kernel<false>);
+  const cudaError_t attr = ensure_smem_attr(kfn, smem);
   if (attr != cudaSuccess) {
     *err = attr;
     *why = "cudaFuncSetAttribute failed";
     return 0;
   }
   const unsigned grid = (unsigned)std::min<int64_t>(p.n_units, sms);  // persistent: one CTA per SM
-  dfa_bwd_sm100_kernel<<<grid, kThreads, smem, stream>>>(mq, mk, mv, mg, mdq, mdk, mdv, lse, delta, p);
+  if (packed) dfa_bwd_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mg, mdq, mdk, mdv, lse, delta, p);
+  else dfa_bwd_sm100_kernel<false><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mg, mdq, mdk, mdv, lse, delta, p);
   *err = cudaGetLastError();
   return 1;
 }

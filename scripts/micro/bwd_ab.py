@@ -6,7 +6,8 @@ sys.path.insert(0, sys.argv[1])
 import paper_2403_09195_b200 as dfa
 B, N, h, d = 64, 4096, 6, 64
 out = {}
-for w, r in ((512, 2), (256, 2), (256, 1), (512, 4), (1024, 8)):
+import os
+for w, r in [tuple(map(int, c.split(':'))) for c in os.environ.get('SHAPES', '512:2,256:2,256:1,512:4,1024:8').split(',')]:
     cfg = dfa.AttentionConfig(N, w, r, h, d, dfa.AttentionConfig.spread_offsets(h, r))
     g = torch.Generator(device="cuda").manual_seed(0)
     q, k, v, do = (torch.randn((B, N, h, d), device="cuda", dtype=torch.bfloat16, generator=g) for _ in range(4))
