@@ -131,7 +131,10 @@ dfa_status_t dfa_dilated_attention_host(const dfa_config_t* cfg, dfa_dtype_t dty
  * are pinned (mapped) host memory and the call takes the tcgen05 path, the
  * kernel TMA-reads only the kept rows straight from host memory over PCIe
  * (no staging copy; dfa_host_transfer_bytes reports the bytes); otherwise
- * they are copied in.  Pageable buffers work, slower. */
+ * they are copied in.  When o is pinned mapped memory too, the kernel writes
+ * the kept output rows straight into it and host threads zero-fill the rest
+ * (dfa_set_host_kept_out); otherwise o comes back by chunked D2H copies.
+ * Pageable buffers work, slower. */
 dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
                               const void* k, const void* v, void* o, float* lse, dfa_workspace_t* ws,
                               void* stream);
@@ -144,10 +147,18 @@ int32_t dfa_get_fault_perturb(void);
 /* Zero-copy input mode of dfa_forward_host (default on; 0 forces the copy-in
  * pipeline).  Process-wide. */
 void dfa_set_host_zero_copy(int32_t enabled);
+/* Output mode of dfa_forward_host when o is also pinned mapped host memory
+ * (default on): the kernel writes the kept rows straight into o over PCIe
+ * and host threads zero-fill the rows no view keeps, so only kept output
+ * rows cross the bus; 0 = device output + chunked D2H copies.  Process-wide. */
+void dfa_set_host_kept_out(int32_t enabled);
 /* Bytes dfa_forward_host moves host->device (h2d) and device->host (d2h) for
- * these buffers: kept rows of q, k, v in zero-copy mode, whole tensors otherwise. */
+ * these buffers: kept rows of q, k, v in zero-copy mode, whole tensors
+ * otherwise; kept rows of o when o is written in place (kept-out mode), the
+ * whole of o otherwise (o may be null: counted as not mapped). */
 dfa_status_t dfa_host_transfer_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
-                                     const void* k, const void* v, int32_t with_lse, size_t* h2d, size_t* d2h);
+                                     const void* k, const void* v, const void* o, int32_t with_lse, size_t* h2d,
+                                     size_t* d2h);
 
 /* Bytes a dfa_forward_host call needs in its workspace. */
 dfa_status_t dfa_workspace_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, int32_t with_lse,

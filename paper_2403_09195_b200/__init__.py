@@ -420,13 +420,25 @@ def host_zero_copy(enabled: bool):
         lib.dfa_set_host_zero_copy(1)
 
 
-def host_transfer_bytes(q, k, v, cfg: AttentionConfig, dtype: str = "bf16", with_lse: bool = False):
-    """(h2d, d2h) bytes dfa_forward_host moves for these host tensors."""
+@contextlib.contextmanager
+def host_kept_out(enabled: bool):
+    """Scope dfa_forward_host's kept-rows-out mode for a pinned host o (default on)."""
+    lib.dfa_set_host_kept_out(1 if enabled else 0)
+    try:
+        yield
+    finally:
+        lib.dfa_set_host_kept_out(1)
+
+
+def host_transfer_bytes(q, k, v, cfg: AttentionConfig, dtype: str = "bf16", with_lse: bool = False, out=None):
+    """(h2d, d2h) bytes dfa_forward_host moves for these host tensors (out: the
+    host output buffer -- kept rows only cross PCIe when it is pinned)."""
     c = cfg._c()
     c.value_dim = v.shape[-1]
     h2d, d2h = ctypes.c_size_t(0), ctypes.c_size_t(0)
     _check(lib.dfa_host_transfer_bytes(ctypes.byref(c), _code(dtype),
-                                       q.shape[0], q.data_ptr(), k.data_ptr(), v.data_ptr(), 1 if with_lse else 0,
+                                       q.shape[0], q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                       out.data_ptr() if out is not None else None, 1 if with_lse else 0,
                                        ctypes.byref(h2d), ctypes.byref(d2h)))
     return h2d.value, d2h.value
 

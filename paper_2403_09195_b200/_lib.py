@@ -46,6 +46,7 @@ EXPORTED = (
     "dfa_forward_host",
     "dfa_forward_strided",
     "dfa_set_host_zero_copy",
+    "dfa_set_host_kept_out",
     "dfa_host_transfer_bytes",
     "dfa_set_fault_perturb",
     "dfa_get_fault_perturb",
@@ -162,7 +163,8 @@ def _load() -> ctypes.CDLL:
         "dfa_forward_strided": (c_i32, [p_cfg, c_i32, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                         c_vp, c_vp]),
         "dfa_set_host_zero_copy": (None, [c_i32]),
-        "dfa_host_transfer_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_vp, c_vp, c_vp, c_i32,
+        "dfa_set_host_kept_out": (None, [c_i32]),
+        "dfa_host_transfer_bytes": (c_i32, [p_cfg, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_i32,
                                             ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
         "dfa_tensor_header": (c_i32, [ctypes.c_char_p, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32), p_i64]),
         "dfa_tensor_load": (c_i32, [ctypes.c_char_p, c_i32, c_vp, c_i64]),

@@ -11,7 +11,11 @@
 
 #include <atomic>
 #include <string>
+#include <thread>
 #include <vector>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 
 #include "../../include/dfa.h"
 #include "dfa_internal.h"
@@ -24,6 +28,9 @@ std::atomic<int32_t> g_fault{0};
 std::atomic<int32_t> g_path_override{0};
 std::atomic<int32_t> g_mb_mode{0};
 std::atomic<int32_t> g_host_zero_copy{1};
+// 1: a host-resident o is written in place too -- the kernel TMA-stores the
+// kept rows over PCIe and host threads zero-fill the rest meanwhile
+std::atomic<int32_t> g_host_kept_out{1};
 
 dfa_status_t fail(dfa_status_t st, const char* fmt, ...) {
   char buf[512];
@@ -106,6 +113,41 @@ int pick_path(const dfa_impl::Geometry& g, dfa_dtype_t dtype, const void* q, con
 size_t elem_size(dfa_dtype_t t) { return t == DFA_F64 ? 8 : t == DFA_F32 ? 4 : 2; }
 
 // Device address of pinned, mapped host memory (nullptr for pageable or device memory).
+// Zero the rows of a host-resident [B][N][h][dv] o that no segment view keeps
+// (n mod r != offset of head j; w % r == 0 on the tcgen05 path), split over
+// host threads; streaming stores (no read-for-ownership of the lines).
+void zero_unkept_rows_host(void* o, const dfa_impl::Geometry& g, size_t es) {
+  const size_t piece = (size_t)g.dv * es, row = (size_t)g.h * piece;
+  const int64_t rows = g.B * g.N;
+  auto work = [&](int64_t r0, int64_t r1) {
+    for (int64_t t = r0; t < r1; ++t) {
+      const int64_t n = t % g.N;
+      char* base = static_cast<char*>(o) + (size_t)t * row;
+      for (int64_t j = 0; j < g.h; ++j) {
+        if (n % g.r == g.offsets[j]) continue;
+        char* dst = base + (size_t)j * piece;
+#if defined(__x86_64__)
+        if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && piece % 16 == 0) {
+          const __m128i z = _mm_setzero_si128();
+          for (size_t b = 0; b < piece; b += 16) _mm_stream_si128(reinterpret_cast<__m128i*>(dst + b), z);
+          continue;
+        }
+#endif
+        memset(dst, 0, piece);
+      }
+    }
+#if defined(__x86_64__)
+    _mm_sfence();
+#endif
+  };
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t nt = std::min<int64_t>(std::min<unsigned>(hw, 16u), std::max<int64_t>(1, rows / 4096));
+  std::vector<std::thread> pool;
+  for (int64_t i = 1; i < nt; ++i) pool.emplace_back(work, rows * i / nt, rows * (i + 1) / nt);
+  work(0, rows / nt);
+  for (auto& th : pool) th.join();
+}
+
 const void* mapped_host(const void* p) {
   cudaPointerAttributes a;
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -154,10 +196,12 @@ void dfa_set_path_override(int32_t path) { g_path_override.store(path); }
 void dfa_set_multibranch_mode(int32_t mode) { g_mb_mode.store(mode); }
 void dfa_set_multibranch_trace(uint64_t* trace) { dfa_impl::set_mb_trace(trace); }
 void dfa_set_host_zero_copy(int32_t enabled) { g_host_zero_copy.store(enabled ? 1 : 0); }
+void dfa_set_host_kept_out(int32_t enabled) { g_host_kept_out.store(enabled ? 1 : 0); }
 void dfa_set_gemm_tile(int32_t bn) { dfa_impl::set_gemm_tile(bn); }
 
 dfa_status_t dfa_host_transfer_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_t batch, const void* q,
-                                     const void* k, const void* v, int32_t with_lse, size_t* h2d, size_t* d2h) {
+                                     const void* k, const void* v, const void* o, int32_t with_lse, size_t* h2d,
+                                     size_t* d2h) {
   dfa_impl::Geometry g;
   dfa_status_t st = resolve(cfg, batch, &g);
   if (st != DFA_OK) return st;
@@ -172,6 +216,9 @@ dfa_status_t dfa_host_transfer_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype,
     *h2d = (size_t)(g.B * g.N * g.h) * (2 * g.d + g.dv) * es;
     return DFA_OK;
   }
+  const void* zo = (o && g_host_kept_out.load()) ? mapped_host(o) : nullptr;
+  const bool kept_out = zo && pick_path(g, dtype, mapped_host(q), mapped_host(k), mapped_host(v), zo) ==
+                                  DFA_PATH_SM100_TCGEN05;
   // kept rows only: sum over heads and segments of the view sizes
   size_t rows = 0;
   for (int64_t j = 0; j < g.h; ++j)
@@ -181,6 +228,7 @@ dfa_status_t dfa_host_transfer_bytes(const dfa_config_t* cfg, dfa_dtype_t dtype,
       rows += (size_t)m;
     }
   *h2d = (size_t)g.B * rows * (size_t)(2 * g.d + g.dv) * es;
+  if (kept_out) *d2h = (size_t)g.B * rows * (size_t)g.dv * es + (with_lse ? (size_t)(g.B * g.h * g.N) * 4 : 0);
   return DFA_OK;
 }
 
@@ -388,6 +436,32 @@ dfa_status_t dfa_forward_host(const dfa_config_t* cfg, dfa_dtype_t dtype, int64_
   const void* zk = zq ? mapped_host(k) : nullptr;
   const void* zv = zk ? mapped_host(v) : nullptr;
   const bool zero_copy = zv && pick_path(g, dtype, zq, zk, zv, dout) == DFA_PATH_SM100_TCGEN05;
+  // Kept rows out in place: o itself is mapped pinned memory -- one launch
+  // writes the kept rows straight into it (the only output bytes that cross
+  // PCIe) while host threads zero-fill the rows no view keeps.
+  const void* zo = zero_copy && g_host_kept_out.load() ? mapped_host(o) : nullptr;
+  if (zo && pick_path(g, dtype, zq, zk, zv, zo) == DFA_PATH_SM100_TCGEN05) {
+    const char* why = "";
+    const int n = dfa_impl::launch_sm100(g, zq, zk, zv, const_cast<void*>(zo), dl, s, &err, &why, nullptr, nullptr,
+                                         false, /*kept_only=*/true);
+    if (n == 0 || err != cudaSuccess)
+      return fail(DFA_ERR_CUDA, "dfa_forward_host: sm100 path: %s (%s)", why, cudaGetErrorString(err));
+    int launches = n;
+    if (lse && (err = cudaMemcpyAsync(lse, dl, bl, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return fail(DFA_ERR_CUDA, "dfa_forward_host: lse D2H: %s", cudaGetErrorString(err));
+#ifndef DFA_PROBE_NO_HOST_ZERO
+    zero_unkept_rows_host(o, g, es);  // host threads, concurrent with the kernel
+#endif
+    if ((err = cudaStreamSynchronize(s)) != cudaSuccess)
+      return fail(DFA_ERR_CUDA, "dfa_forward_host: %s", cudaGetErrorString(err));
+    if (g_fault.load()) {  // after the zero fill: element 0 may lie in a zero-filled row
+      launches += dfa_impl::launch_perturb(dtype, const_cast<void*>(zo), s);
+      if ((err = cudaStreamSynchronize(s)) != cudaSuccess)
+        return fail(DFA_ERR_CUDA, "dfa_forward_host: fault hook: %s", cudaGetErrorString(err));
+    }
+    g_launches = launches;
+    return DFA_OK;
+  }
   // Pipeline over image chunks: H2D of chunk c+1 (copy engine 1) overlaps
   // the kernel of chunk c and the D2H of chunk c-1 (copy engine 2), so the
   // call costs ~max(H2D, D2H) instead of their sum.

@@ -119,9 +119,11 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 // merge: multi-(w, r) branch merge -- o and lse hold the running result of
 // the earlier branches; the kept rows of this branch are LSE-combined into
 // them in the epilogue (no zero boxes; lse required).
+// kept_only: write the kept rows only -- the caller zero-fills the others
+// (dfa_forward_host with a host-resident o).
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace = nullptr,
-                 unsigned long long* watchdog = nullptr, bool merge = false);
+                 unsigned long long* watchdog = nullptr, bool merge = false, bool kept_only = false);
 
 // LSE-weighted combine of nb <= 8 branch outputs (dfa_combine.cu).
 int launch_combine(int dtype, int64_t B, int64_t N, int64_t h, int64_t dv, int nb, const void* const* o,

@@ -175,6 +175,7 @@ struct Sm100Params {
   float c;           // scale * log2(e)
   float scale;
   int32_t merge;     // 1: merge into the running (o, lse) of earlier branches (no zero boxes)
+  int32_t zero_rows; // 0: the caller zero-fills the rows no view keeps (host-resident o, kept rows only cross PCIe)
   FastDiv div_pairs, div_h, div_m;
   int32_t offsets[kMaxHeads];
 };
@@ -791,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::named_bar_sync(1, kBM);
         if (leader) {
           ptx::tma_store_5d(&tm_o, sm.ostage[s % kOStages], 0, x.j, x.gamma, ts0, x.b);
-          if (!p.merge)
+          if (!p.merge && p.zero_rows)
             for (int32_t gz = 0; gz < p.r; ++gz)
               if (gz != x.gamma && !DFA_PROBE_NO_ZERO)
                 for (int32_t zr = 0; zr < kBM; zr += kZeroRows)
@@ -913,7 +914,7 @@ bool sm100_supported(const Geometry& g, int dtype, const void* q, const void* k,
 
 int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v, void* o, float* lse,
                  cudaStream_t stream, cudaError_t* err, const char** why, uint64_t* trace,
-                 unsigned long long* watchdog, bool merge) {
+                 unsigned long long* watchdog, bool merge, bool kept_only) {
   ensure_context();
   if (merge && !lse) {
     *why = "merge mode needs the running lse buffer";
@@ -945,6 +946,7 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.scale = g.scale;
   p.c = g.scale * kLog2e;
   p.merge = merge ? 1 : 0;
+  p.zero_rows = kept_only ? 0 : 1;
   p.div_pairs = make_fastdiv((uint32_t)p.n_pairs);
   p.div_h = make_fastdiv((uint32_t)p.h);
   p.div_m = make_fastdiv((uint32_t)p.m);

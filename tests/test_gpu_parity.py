@@ -428,8 +428,10 @@ def test_strided_qkv_equals_contiguous(dfa, cuda, dt, w, r):
 
 def test_host_entry_zero_copy_equals_copy_path(dfa, cuda):
     """dfa_forward_host with pinned inputs reads the kept rows straight from
-    host memory (zero-copy TMA); the copy-in pipeline and pageable inputs give
-    the same bits, and the reported PCIe bytes shrink to the kept rows."""
+    host memory (zero-copy TMA); with a pinned o it also writes only the kept
+    output rows in place (host threads zero-fill the rest).  Every mode --
+    kept-out, device output + D2H, copy-in, pageable -- gives the same bits on
+    a NaN-poisoned o, and the reported PCIe bytes shrink to the kept rows."""
     torch = _torch()
     B, n, h = 8, 4096, 6
     cfg = make_cfg(dfa, n, 512, 2, h, 64)
@@ -437,20 +439,51 @@ def test_host_entry_zero_copy_equals_copy_path(dfa, cuda):
     q, k, v = (torch.randn((B, n, h, 64), generator=g).to(torch.bfloat16) for _ in range(3))
     pq, pk, pv = (t.pin_memory() for t in (q, k, v))
     ws = dfa.Workspace(dfa.Workspace.bytes_for(cfg, "bf16", B))
+    full = 3 * q.numel() * 2
     outs = []
-    for args, zc in (((pq, pk, pv), True), ((pq, pk, pv), False), ((q, k, v), True)):
-        o = torch.empty_like(q).pin_memory()
-        with dfa.host_zero_copy(zc):
+    # (inputs, zero-copy in, pinned o, kept-out mode) -> expected (h2d, d2h)
+    modes = [((pq, pk, pv), True, True, True, (full // 2, q.numel())),
+             ((pq, pk, pv), True, True, False, (full // 2, 2 * q.numel())),
+             ((pq, pk, pv), True, False, True, (full // 2, 2 * q.numel())),
+             ((pq, pk, pv), False, True, True, (full, 2 * q.numel())),
+             ((q, k, v), True, True, True, (full, 2 * q.numel()))]
+    for args, zc, pinned_o, kept, want in modes:
+        o = torch.full_like(q, float("nan"))
+        if pinned_o:
+            o = o.pin_memory()
+        with dfa.host_zero_copy(zc), dfa.host_kept_out(kept):
             dfa.dfa_forward_host(*args, o, cfg, ws)
-            h2d, d2h = dfa.host_transfer_bytes(*args, cfg)
+            assert dfa.host_transfer_bytes(*args, cfg, out=o) == want
         outs.append(o)
-        full = 3 * q.numel() * 2
-        assert h2d == (full // 2 if (zc and args[0].is_pinned()) else full)
-        assert d2h == q.numel() * 2
     ws.close()
     ref = dfa.dfa_forward(q.cuda(), k.cuda(), v.cuda(), cfg).cpu()
     for o in outs:
         assert torch.equal(o, ref)
+
+
+@pytest.mark.parametrize("n,w,r,offs,with_lse", [
+    (4096, 1024, 4, [3, 1, 2, 0, 1, 3], True),   # r = 4, custom offsets, lse through the host call
+    (2048, 2048, 8, [0, 7, 7, 2, 5, 1], False),  # one segment, r = 8: 7 / 8 of o zero-filled on the host
+    (2304, 512, 2, [0, 1, 0, 1, 0, 1], True),    # tail segment
+])
+def test_host_kept_out_zero_fill(dfa, cuda, n, w, r, offs, with_lse):
+    """Kept-out mode: the host zero fill covers exactly the rows no view keeps
+    (NaN-poisoned pinned o), lse comes back alongside."""
+    torch = _torch()
+    B, h = 3, 6
+    cfg = dfa.AttentionConfig(n, w, r, h, 64, offs)
+    g = torch.Generator().manual_seed(n + r)
+    q, k, v = (torch.randn((B, n, h, 64), generator=g).to(torch.bfloat16).pin_memory() for _ in range(3))
+    o = torch.full((B, n, h, 64), float("nan")).to(torch.bfloat16).pin_memory()
+    L = torch.full((B, h, n), float("nan")).pin_memory() if with_lse else None
+    ws = dfa.Workspace(dfa.Workspace.bytes_for(cfg, "bf16", B, with_lse=with_lse))
+    dfa.dfa_forward_host(q, k, v, o, cfg, ws, lse=L)
+    ws.close()
+    Lr = torch.empty((B, h, n), device="cuda") if with_lse else None
+    ref = dfa.dfa_forward(q.cuda(), k.cuda(), v.cuda(), cfg, lse=Lr).cpu()
+    assert torch.equal(o, ref)
+    if with_lse:
+        assert torch.equal(L, Lr.cpu())
 
 
 def test_forward_and_backward_from_a_fresh_thread(dfa, cuda):
