@@ -565,6 +565,12 @@ int launch_dispatch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
   const int bn_res = force_bn ? force_bn : 128;
   const int64_t keys = (batch > 1 && sb != 0 ? batch : 1) * ((N + bn_res - 1) / bn_res);
   const int epi = (bias ? kEpiBias : 0) | (C ? kEpiC : 0) | (gelu ? kEpiGelu : 0);
+  // plain projections with K >= 256 whose N splits into 192-wide blocks (the
+  // class-split QKV GEMM: N = 3 h d / r): streaming 192-wide tiles measured
+  // 3-7% faster than the resident 128-wide panel (fewer A re-reads; the
+  // resident 192-wide panel leaves only 3 A stages and lost)
+  if (!force_bn && !DFA_GEMM_STG && epi == 0 && ktiles >= 4 && N % 192 == 0)
+    return launch_bn<192, false, 2>(DFA_GEMM_ARGS);
   if (ktiles <= 6 && keys <= device_sms() && (bn_res == 128 || bn_res == 64)) {
     if (bn_res == 64) return stg == 1 ? launch_bn<64, true, 1>(DFA_GEMM_ARGS) : launch_bn<64, true, 2>(DFA_GEMM_ARGS);
     if (!DFA_GEMM_STG && !force_bn) {  // the layers' epilogues, straight-line
