@@ -143,7 +143,11 @@ void zero_unkept_rows_host(void* o, const dfa_impl::Geometry& g, size_t es) {
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int64_t nt = std::min<int64_t>(std::min<unsigned>(hw, 16u), std::max<int64_t>(1, rows / 4096));
   std::vector<std::thread> pool;
-  for (int64_t i = 1; i < nt; ++i) pool.emplace_back(work, rows * i / nt, rows * (i + 1) / nt);
+  try {  // helper i zeroes rows [rows i / nt, rows (i + 1) / nt)
+    for (int64_t i = 1; i < nt; ++i) pool.emplace_back(work, rows * i / nt, rows * (i + 1) / nt);
+  } catch (...) {  // no more threads: this one takes the helpers' share that was not started (nothing escapes the C-ABI)
+    work(rows * (int64_t)(pool.size() + 1) / nt, rows);
+  }
   work(0, rows / nt);
   for (auto& th : pool) th.join();
 }
