@@ -550,11 +550,13 @@ std::atomic<int> g_force_bn{0};  // measurement knob (dfa_set_gemm_tile); 0 = au
 #ifndef DFA_GEMM_STG
 #define DFA_GEMM_STG 0
 #endif
-// Resident panel at BN = 128 whenever it fits (K <= 384): measured best on
-// every projection / w1 shape (BN = 192 leaves only 3 A stages; the main
-// loop is load-latency bound); light epilogues take a 6-deep A ring with one
-// staging tile per group, GELU / residual epilogues 4 stages and two.
-// Longer K streams A and B tiles (BN = 192, 4 stages).
+// Plain projections with K >= 256 and N % 192 == 0 (the class-split QKV
+// GEMM) stream 192-wide tiles; otherwise the resident panel at BN = 128
+// whenever it fits (K <= 384: a resident 192-wide panel leaves only 3 A
+// stages and the main loop is load-latency bound); light epilogues take a
+// 6-deep A ring with one staging tile per group, GELU / residual epilogues
+// 4 stages and two.  GELU epilogues with N % 256 == 0 stream 256-wide tiles;
+// longer K streams A and B tiles (BN = 192, 4 stages).
 int launch_dispatch(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sa, const void* B,
                     int64_t ldb, int64_t sb, void* D, int64_t ldd, int64_t sd, const void* C, int64_t ldc, float beta,
                     const void* bias, int batch, cudaStream_t stream, const char** why, bool gelu, int force_bn) {
