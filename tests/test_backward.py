@@ -166,3 +166,30 @@ def test_tcgen05_backward_vs_simt(dfa, cuda, w, r, B):
         scale = max(1.0, y.float().abs().max().item())
         assert err.max().item() <= 2e-2 * scale, err.max().item()
         assert (err.sum() / y.float().abs().sum()).item() <= 1e-2
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("w,r,B", [(512, 2, 64), (256, 1, 16), (256, 2, 16), (64, 1, 16)])
+def test_tcgen05_backward_repeatable_under_load(dfa, cuda, w, r, B):
+    """Stress: 30 back-to-back backward launches at bench scale give bitwise
+    identical gradients.  Two-block views exercise the dV read-before-overwrite
+    ordering at key-block transitions, one-block views the double-buffered
+    operand slots, (64, 1) the packed-segment instantiation."""
+    import torch
+
+    n, h = 4096, 6
+    cfg = dfa.AttentionConfig(n, w, r, h, 64, [j % r for j in range(h)])
+    g = torch.Generator(device="cuda").manual_seed(w + r)
+    q, k, v, do = (torch.randn((B, n, h, 64), device="cuda", generator=g, dtype=torch.bfloat16) for _ in range(4))
+    L = torch.empty((B, h, n), device="cuda")
+    o = dfa.dfa_forward(q, k, v, cfg, lse=L)
+    ws = torch.empty(B * h * n * 4 + 256, dtype=torch.uint8, device="cuda")
+    ref = [torch.empty_like(q) for _ in range(3)]
+    dfa.dfa_backward(q, k, v, o, L, do, cfg, *ref, workspace=ws)
+    got = [torch.empty_like(q) for _ in range(3)]
+    for _ in range(30):
+        dfa.dfa_backward(q, k, v, o, L, do, cfg, *got, workspace=ws)
+    torch.cuda.synchronize()
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
