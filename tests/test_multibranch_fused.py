@@ -283,3 +283,23 @@ def test_random_sets_vs_oracle(dfa, port, cuda, case):
     Lg = L.cpu().numpy()
     assert np.array_equal(np.isfinite(Lg), fin)
     assert np.abs(Lg[fin] - want_lse[fin]).max() <= 2e-2
+
+
+@pytest.mark.timeout(300)
+def test_fused_repeatable_back_to_back(dfa, cuda):
+    """Stress: 25 back-to-back fused launches (dynamic unit claiming, counters
+    re-armed by the last CTA of each launch, PDL overlap of consecutive
+    launches) on two alternating branch sets give bitwise identical outputs."""
+    torch = _torch()
+    q, k, v = _inputs(16, 4096, 6, 29)
+    cfg = dfa.AttentionConfig(4096, 512, 1, 6, 64, [0] * 6)
+    sets = [SETS[0], SETS[1]]
+    refs = [dfa.dfa_forward_multibranch(q, k, v, cfg, br) for br in sets]
+    outs = [torch.empty_like(q) for _ in sets]
+    for i in range(25):
+        j = i % 2
+        dfa.dfa_forward_multibranch(q, k, v, cfg, sets[j], out=outs[j])
+        assert dfa.last_launch_count() == 1
+        if i >= 23:
+            torch.cuda.synchronize()
+            assert torch.equal(outs[j], refs[j])
