@@ -102,7 +102,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 #endif
 constexpr float kRescaleThreshold = DFA_RESCALE_THR;  // log2 units: p <= 2^8 between rescales
 #ifndef DFA_SUMCHECK
-#define DFA_SUMCHECK 0
+#define DFA_SUMCHECK -1  // -1: by geometry (launch_sm100), 0: never, 1: always
 #endif
 // Sum-checked fast path (DFA_SUMCHECK): a tile whose row sum against the
 // running reference stays <= 2^thr needs no row max.
@@ -298,7 +298,7 @@ __device__ __forceinline__ void wait_site(uint64_t* bar, uint32_t parity, uint32
 }
 #define DFA_WAIT(bar, parity, site) wait_site<kTrace>((bar), (parity), (site), watchdog)
 
-template <bool kTrace>
+template <bool kTrace, bool kSumCheck = false>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -619,18 +619,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       bool exact = true;
       bool waited = false;
-#if DFA_SUMCHECK
-      // Fast path (every row of the warp already has a reference from an
-      // earlier tile of this unit): no row max.  The tile's row sum bounds
-      // each p, so sum <= 2^thr keeps every p within the lazy-rescale bound;
-      // otherwise (or on inf / NaN) the tile is redone on the exact path and
-      // P is simply re-stored over the same columns.
-      if (__all_sync(0xffffffffu, mref != -INFINITY)) {
-        const float fs = exp_pass(-mref * p.c, true);
-        exact = __any_sync(0xffffffffu, !(fs <= kSumBound));
-        if (!exact) l += fs;
+      if constexpr (kSumCheck) {
+        // Fast path (every row of the warp already has a reference from an
+        // earlier tile of this unit): no row max.  The tile's row sum bounds
+        // each p, so sum <= 2^thr keeps every p within the lazy-rescale bound;
+        // otherwise (or on inf / NaN) the tile is redone on the exact path and
+        // P is simply re-stored over the same columns.
+        if (__all_sync(0xffffffffu, mref != -INFINITY)) {
+          const float fs = exp_pass(-mref * p.c, true);
+          exact = __any_sync(0xffffffffu, !(fs <= kSumBound));
+          if (!exact) l += fs;
+        }
       }
-#endif
       if (exact) {
         float mx[8];
 #pragma unroll
@@ -951,10 +951,15 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.div_h = make_fastdiv((uint32_t)p.h);
   p.div_m = make_fastdiv((uint32_t)p.m);
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
+  // Sum-checked fast path (no row max on tiles after a unit's first): measured
+  // 1.3-3.5% faster on long views -- (1024, 1), (2048, 1), (4096, 1),
+  // (4096, 2) -- and 1-6% slower on the short / store-heavy ones ((512, 2),
+  // (1024, 2), (2048, 4), (4096, 4)), where its occasional redo of a tile
+  // lands on the critical path.
+  const bool sumcheck = DFA_SUMCHECK < 0 ? (p.m >= 2048 || (p.r == 1 && p.m >= 1024)) : DFA_SUMCHECK != 0;
   const size_t smem = sizeof(SmemLayout) + 1024;
-  cudaError_t attr_err = ensure_smem_attr(reinterpret_cast<const void*>(trace ? dfa_sm100_kernel<true>
-                                                                              : dfa_sm100_kernel<false>),
-                                          smem);
+  auto kfn = trace ? dfa_sm100_kernel<true> : sumcheck ? dfa_sm100_kernel<false, true> : dfa_sm100_kernel<false>;
+  cudaError_t attr_err = ensure_smem_attr(reinterpret_cast<const void*>(kfn), smem);
   if (attr_err != cudaSuccess) {
     *err = attr_err;
     *why = "cudaFuncSetAttribute failed";
@@ -965,8 +970,8 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   if (trace)
     dfa_sm100_kernel<true><<<grid, kThreads, smem, stream>>>(mq, mk, mv, mo, mz, lse, p, trace, watchdog);
   else
-    le = launch_pdl(dfa_sm100_kernel<false>, grid, kThreads, smem, stream, mq, mk, mv, mo, mz, lse, p,
-                    (uint64_t*)nullptr, (unsigned long long*)nullptr);
+    le = launch_pdl(kfn, grid, kThreads, smem, stream, mq, mk, mv, mo, mz, lse, p, (uint64_t*)nullptr,
+                    (unsigned long long*)nullptr);
   *err = le != cudaSuccess ? le : cudaGetLastError();
   return 1;
 }
