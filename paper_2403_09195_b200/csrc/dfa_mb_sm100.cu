@@ -75,6 +75,10 @@ __host__ __device__ constexpr uint32_t col_s(int buf) { return (uint32_t)kBN * b
 __host__ __device__ constexpr uint32_t col_o(int slot) { return 384u + 64u * slot; }
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThreshold = 8.0f;
+constexpr float kSumBound = 256.0f;  // sum-checked fast path: p <= sum <= 2^8 keeps the lazy-rescale bound
+#ifndef DFA_MB_SUMCHECK
+#define DFA_MB_SUMCHECK -1  // -1: by geometry (launch_mb_sm100), 0: never, 1: always
+#endif
 constexpr uint32_t kPolyMask = 0x0888u;  // as dfa_sm100.cu (3 of 16 pairs on the FMA pipe)
 
 struct FastDivMb {
@@ -192,7 +196,7 @@ __device__ __forceinline__ uint32_t next_slot(MbSmem& sm, uint32_t n) {
   return slot;
 }
 
-template <bool kTrace>
+template <bool kTrace, bool kSumCheck = false>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_mb_sm100_kernel(const __grid_constant__ MbMaps maps, float* __restrict__ lse,
                         const __grid_constant__ MbParams p, uint64_t* __restrict__ trace) {
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (col < lo || col >= hi) sr[c][e] = __float_as_uint(-INFINITY);
               }
           }
-          auto exp_pass = [&](float neg) -> float {
+          auto exp_pass = [&](float neg, bool clamp_hi) -> float {
             float2 ls2[2] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
             const float2 c2 = make_float2(p.c, p.c), n2 = make_float2(neg, neg);
 #pragma unroll
@@ -523,6 +527,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 if ((kPolyMask >> e) & 1u) {
+                  // the polynomial's exponent add wraps for x >= 128: clamp so an
+                  // overflowing tile shows up in the fast path's row sum
+                  if (clamp_hi) xv[e] = make_float2(fminf(xv[e].x, 126.0f), fminf(xv[e].y, 126.0f));
                   xv[e] = ptx::ex2_poly2(xv[e]);
                 } else {
                   xv[e].x = ptx::ex2(xv[e].x);
@@ -540,7 +547,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 lsum = ptx::fadd2(ls2[0], ls2[1]);
             return lsum.x + lsum.y;
           };
-          {
+          bool exact = true;
+          if constexpr (kSumCheck) {
+            // Fast path (every row of the warp already has a reference): no
+            // row max; the tile is redone exactly when a row sum exceeds 2^8
+            // against the reference (or is inf / NaN), P re-stored in place.
+            if (__all_sync(0xffffffffu, mref != -INFINITY)) {
+              const float fs = exp_pass(-mref * p.c, true);
+              exact = __any_sync(0xffffffffu, !(fs <= kSumBound));
+              if (!exact) l += fs;
+            }
+          }
+          if (exact) {
             float mx[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
@@ -573,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             MB_TRACE(2 + s, 11);
             if (move) mref = tmax;
-            l += exp_pass((mref == -INFINITY) ? 0.0f : -mref * p.c);
+            l += exp_pass((mref == -INFINITY) ? 0.0f : -mref * p.c, false);
           }
         }  // rows with keys in this tile
         MB_TRACE(2 + s, 12);
@@ -1071,8 +1089,16 @@ int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, co
   p.n_work = plan.n_work;
   const size_t smem = sizeof(MbSmem) + 1024;
   uint64_t* trace = g_mb_trace.load();
-  cudaError_t ae = ensure_smem_attr(
-      reinterpret_cast<const void*>(trace ? dfa_mb_sm100_kernel<true> : dfa_mb_sm100_kernel<false>), smem);
+  // Sum-checked fast path only when every branch's view is long (m = w / r
+  // >= 1024): measured -3% on {(2048, 2), (4096, 4)}, but +9% on the LongNet
+  // set and +20% on {(256, 2), (512, 2), (1024, 4)} (short views: the
+  // redone tiles land on the critical path).
+  int64_t min_m = INT64_MAX;
+  for (int b = 0; b < nb; ++b) min_m = std::min<int64_t>(min_m, gb[b].w / gb[b].r);
+  const bool sumcheck = DFA_MB_SUMCHECK < 0 ? min_m >= 1024 : DFA_MB_SUMCHECK != 0;
+  auto kfn = trace ? dfa_mb_sm100_kernel<true> : sumcheck ? dfa_mb_sm100_kernel<false, true>
+                                                          : dfa_mb_sm100_kernel<false>;
+  cudaError_t ae = ensure_smem_attr(reinterpret_cast<const void*>(kfn), smem);
   if (ae != cudaSuccess) {
     *err = ae;
     *why = "cudaFuncSetAttribute failed";
@@ -1082,8 +1108,7 @@ int launch_mb_sm100(const Geometry* gb, int nb, const void* q, const void* k, co
   if (trace)
     dfa_mb_sm100_kernel<true><<<plan.grid, kThreads, smem, stream>>>(maps, lse, p, trace);
   else
-    le = launch_pdl(dfa_mb_sm100_kernel<false>, plan.grid, kThreads, smem, stream, maps, lse, p,
-                    (uint64_t*)nullptr);
+    le = launch_pdl(kfn, plan.grid, kThreads, smem, stream, maps, lse, p, (uint64_t*)nullptr);
   *err = le != cudaSuccess ? le : cudaGetLastError();
   if (*err != cudaSuccess) {
     *why = "launch failed";
