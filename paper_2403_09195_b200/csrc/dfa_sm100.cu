@@ -112,6 +112,13 @@ constexpr float kSumBound = 256.0f;
 // measured with the 192-register softmax: 3 of 16 (pairs 3, 7, 11) beats
 // 2 and 4 of 16 by 1-3% and 6 of 16 by 5-8%)
 constexpr uint32_t kPolyMask = DFA_POLY_MASK;
+// The sum-checked kernel (no row max on most tiles) leaves less work on the
+// FMA / ALU side: 2 of 16 pairs (3 and 11) on the polynomial measured 1.7-4%
+// faster than 3 of 16 on (1024, 1) .. (4096, 2); 1 / 16 and 4 / 16 slower.
+#ifndef DFA_POLY_MASK_SC
+#define DFA_POLY_MASK_SC 0x0808u
+#endif
+constexpr uint32_t kPolyMaskSumCheck = DFA_POLY_MASK_SC;
 
 // Geometry of one work unit, identical in every role.
 struct Unit {
@@ -596,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int e = 0; e < 16; ++e) {
             if (DFA_PROBE_NO_EXP) {
               // profiling probe only (wrong results): no exponentials
-            } else if ((kPolyMask >> e) & 1u) {
+            } else if (((kSumCheck ? kPolyMaskSumCheck : kPolyMask) >> e) & 1u) {
               // the polynomial's exponent add wraps for x >= 128: clamp so an
               // overflowing tile shows up in the row sum (MUFU gives +inf)
               if (clamp_hi) xv[e] = make_float2(fminf(xv[e].x, 126.0f), fminf(xv[e].y, 126.0f));
