@@ -958,12 +958,13 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   p.div_h = make_fastdiv((uint32_t)p.h);
   p.div_m = make_fastdiv((uint32_t)p.m);
   for (int i = 0; i < kMaxHeads; ++i) p.offsets[i] = i < g.h ? g.offsets[i] : 0;
-  // Sum-checked fast path (no row max on tiles after a unit's first): measured
-  // 1.3-3.5% faster on long views -- (1024, 1), (2048, 1), (4096, 1),
-  // (4096, 2) -- and 1-6% slower on the short / store-heavy ones ((512, 2),
+  // Sum-checked fast path (no row max on tiles after a unit's first, 2/16
+  // polynomial share): measured 3-7% faster on long views with at most one
+  // zero box per row -- (1024, 1), (2048, 1), (4096, 1), (2048, 2), (4096, 2)
+  // -- and 2-10% slower on the short / store-heavy ones ((512, 1), (512, 2),
   // (1024, 2), (2048, 4), (4096, 4)), where its occasional redo of a tile
   // lands on the critical path.
-  const bool sumcheck = DFA_SUMCHECK < 0 ? (p.m >= 2048 || (p.r == 1 && p.m >= 1024)) : DFA_SUMCHECK != 0;
+  const bool sumcheck = DFA_SUMCHECK < 0 ? (p.m >= 1024 && p.r <= 2) : DFA_SUMCHECK != 0;
   const size_t smem = sizeof(SmemLayout) + 1024;
   auto kfn = trace ? dfa_sm100_kernel<true> : sumcheck ? dfa_sm100_kernel<false, true> : dfa_sm100_kernel<false>;
   cudaError_t attr_err = ensure_smem_attr(reinterpret_cast<const void*>(kfn), smem);
