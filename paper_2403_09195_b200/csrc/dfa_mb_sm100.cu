@@ -80,6 +80,7 @@ constexpr float kSumBound = 256.0f;  // sum-checked fast path: p <= sum <= 2^8 k
 #define DFA_MB_SUMCHECK -1  // -1: by geometry (launch_mb_sm100), 0: never, 1: always
 #endif
 constexpr uint32_t kPolyMask = 0x0888u;  // as dfa_sm100.cu (3 of 16 pairs on the FMA pipe)
+constexpr uint32_t kPolyMaskSumCheck = 0x0808u;  // sum-checked instantiation: 2 of 16 (-2% on {(2048, 2), (4096, 4)})
 
 struct FastDivMb {
   uint32_t d, mul, shift;
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 xv[e] = ptx::ffma2(make_float2(__uint_as_float(sr[c][2 * e]), __uint_as_float(sr[c][2 * e + 1])), c2, n2);
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                if ((kPolyMask >> e) & 1u) {
+                if (((kSumCheck ? kPolyMaskSumCheck : kPolyMask) >> e) & 1u) {
                   // the polynomial's exponent add wraps for x >= 128: clamp so an
                   // overflowing tile shows up in the fast path's row sum
                   if (clamp_hi) xv[e] = make_float2(fminf(xv[e].x, 126.0f), fminf(xv[e].y, 126.0f));
