@@ -131,15 +131,19 @@ struct Unit {
   __device__ __forceinline__ int32_t kt1(int s) const { return s ? kt1b : kt1a; }
 };
 
-struct __align__(1024) SmemLayout {
+// kKSt K-ring stages; the V ring takes the rest of the kKStages + kVStages
+// tiles (the same shared-memory footprint for every split).
+template <int kKSt = kKStages>
+struct __align__(1024) SmemLayoutT {
+  static constexpr int kVSt = kKStages + kVStages - kKSt;
   uint8_t q[kQStages][2][kTileBytes];  // contiguous: tile (stage, slot) at index stage * 2 + slot
-  uint8_t k[kKStages][kKVTileBytes];
-  uint8_t v[kVStages][kKVTileBytes];
+  uint8_t k[kKSt][kKVTileBytes];
+  uint8_t v[kVSt][kKVTileBytes];
   uint8_t ostage[kOStages][kTileBytes];
   uint8_t zero[kZeroRows * 128];
   uint64_t q_full[kQStages], q_empty[kQStages];
-  uint64_t k_full[kKStages], k_empty[kKStages];  // K ring: freed when its last Q K^T completes
-  uint64_t v_full[kVStages], v_empty[kVStages];  // V ring: freed when its last P V completes
+  uint64_t k_full[kKSt], k_empty[kKSt];  // K ring: freed when its last Q K^T completes
+  uint64_t v_full[kVSt], v_empty[kVSt];  // V ring: freed when its last P V completes
   uint64_t s_full[2][kSBufs];  // MMA -> slot s: S ready in buffer b
   uint64_t p_full[kSBufs];     // slot -> P V issuer: P written in buffer b (128 arrivals)
   uint64_t s_free[kSBufs];     // P V issuer -> Q K^T issuer: P V of buffer b completed
@@ -305,7 +309,7 @@ __device__ __forceinline__ void wait_site(uint64_t* bar, uint32_t parity, uint32
 }
 #define DFA_WAIT(bar, parity, site) wait_site<kTrace>((bar), (parity), (site), watchdog)
 
-template <bool kTrace, bool kSumCheck = false>
+template <bool kTrace, bool kSumCheck = false, int kKS = kKStages>
 __global__ void __launch_bounds__(kThreads, 1)
     dfa_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -313,6 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ Sm100Params p, uint64_t* __restrict__ trace,
                      unsigned long long* __restrict__ watchdog) {
   extern __shared__ uint8_t smem_raw[];
+  using SmemLayout = SmemLayoutT<kKS>;
+  constexpr int kVS = SmemLayout::kVSt;
   SmemLayout& sm =
       *reinterpret_cast<SmemLayout*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
@@ -329,11 +335,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&sm.q_full[s], 1);
       ptx::mbar_init(&sm.q_empty[s], 1);
     }
-    for (int s = 0; s < kKStages; ++s) {
+    for (int s = 0; s < kKS; ++s) {
       ptx::mbar_init(&sm.k_full[s], 1);
       ptx::mbar_init(&sm.k_empty[s], 1);
     }
-    for (int s = 0; s < kVStages; ++s) {
+    for (int s = 0; s < kVS; ++s) {
       ptx::mbar_init(&sm.v_full[s], 1);
       ptx::mbar_init(&sm.v_empty[s], 1);
     }
@@ -394,9 +400,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_load_5d(sm.q[qs][0], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0, x.b, pol);
         ptx::tma_load_5d(sm.q[qs][1], &tm_q, &sm.q_full[qs], 0, x.j, x.gamma, x.t0 + kBM, x.b, pol);
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
-          const uint32_t st = g % kKStages;
+          const uint32_t st = g % kKS;
           DFA_TRACE(0, TR_KV_WAIT);
-          DFA_WAIT(&sm.k_empty[st], ((g / kKStages) & 1) ^ 1, 3);
+          DFA_WAIT(&sm.k_empty[st], ((g / kKS) & 1) ^ 1, 3);
           DFA_TRACE(0, TR_KV_ISSUE);
           ptx::mbar_arrive_expect_tx(&sm.k_full[st], kKVTileBytes);
           ptx::tma_load_5d(sm.k[st], &tm_k, &sm.k_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
@@ -411,8 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int32_t u = blockIdx.x; u < p.n_units; u += gridDim.x) {
         const Unit x = make_unit(p, u);
         for (int32_t kt = 0; kt < x.n_kv; ++kt, ++g) {
-          const uint32_t st = g % kVStages;
-          DFA_WAIT(&sm.v_empty[st], ((g / kVStages) & 1) ^ 1, 4);
+          const uint32_t st = g % kVS;
+          DFA_WAIT(&sm.v_empty[st], ((g / kVS) & 1) ^ 1, 4);
           ptx::mbar_arrive_expect_tx(&sm.v_full[st], kKVTileBytes);
           ptx::tma_load_5d(sm.v[st], &tm_v, &sm.v_full[st], 0, x.j, x.gamma, x.kv_lo + kt * kBN, x.b, pol);
         }
@@ -466,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++steps;
           }
           ptx::tc_commit(&sm.k_empty[gs]);  // every Q K^T of this K tile issued
-          if (++gs == kKStages) {
+          if (++gs == kKS) {
             gs = 0;
             gpar ^= 1u;
           }
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             b = (b == kSBufs - 1) ? 0 : b + 1;
           }
           ptx::tc_commit(&sm.v_empty[gs]);  // every P V of this V tile issued
-          if (++gs == kVStages) {
+          if (++gs == kVS) {
             gs = 0;
             gpar ^= 1u;
           }
@@ -965,8 +971,17 @@ int launch_sm100(const Geometry& g, const void* q, const void* k, const void* v,
   // (1024, 2), (2048, 4), (4096, 4)), where its occasional redo of a tile
   // lands on the critical path.
   const bool sumcheck = DFA_SUMCHECK < 0 ? (p.m >= 1024 && p.r <= 2) : DFA_SUMCHECK != 0;
-  const size_t smem = sizeof(SmemLayout) + 1024;
-  auto kfn = trace ? dfa_sm100_kernel<true> : sumcheck ? dfa_sm100_kernel<false, true> : dfa_sm100_kernel<false>;
+  // r = 2 views of 256-512 rows (two to four key tiles per unit, one zero box
+  // per output tile) keep more K tiles than V tiles in flight: 4 + 2 instead
+  // of 3 + 3 measured -3% at config 2 ((512, 2)), neutral at (1024, 2); +1% on
+  // (256, 1) / (256, 2) and +2-3.5% on r >= 4 and long views, which keep 3 + 3.
+  const bool deep_k = !sumcheck && p.r == 2 && p.m >= 256 && p.m <= 512 && kKStages == 3 && kVStages == 3;
+  static_assert(sizeof(SmemLayoutT<4>) == sizeof(SmemLayoutT<kKStages>), "K / V splits share one footprint");
+  const size_t smem = sizeof(SmemLayoutT<>) + 1024;
+  auto kfn = trace      ? dfa_sm100_kernel<true>
+             : sumcheck ? dfa_sm100_kernel<false, true>
+             : deep_k   ? dfa_sm100_kernel<false, false, 4>
+                        : dfa_sm100_kernel<false>;
   cudaError_t attr_err = ensure_smem_attr(reinterpret_cast<const void*>(kfn), smem);
   if (attr_err != cudaSuccess) {
     *err = attr_err;
